@@ -1,0 +1,571 @@
+#!/usr/bin/env python3
+"""bench.py -- headline benchmark of the B200 angles->coordinates hot path.
+
+Metric (BASELINE.json): residues/s of forward+backward, backbone model,
+L = 700, batch 256 per GPU, at N = 1/2/4/8 GPUs (weak scaling: every rank
+runs its own 256-chain batch; nothing is exchanged on the data path), plus the
+fraction of the HBM roofline of the dominant kernel.
+
+    python bench.py [--steps K] [--warmup W] [--config metric|2|3|4|5]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+    python bench.py --impl reference ...   (the fp64 oracle, timed on host cores)
+
+One "step" = one tpl_*_forward + one tpl_*_backward over one batch with
+synthetic inputs already resident in HBM.  Cold L2: the step rotates over
+enough input/output buffer sets to exceed 4x the L2 size.  Each step set is
+captured once in a CUDA graph; the timed region replays exactly K steps
+bracketed by barrier + synchronize, timed with CUDA events on the launching
+stream, max over ranks.  Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+BYTES_PER_RES = {  # algorithmic bytes
+    "backbone": {"fwd": 12 + 36, "bwd": 12 + 36 + 12},
+    "fullatom": {"fwd": None, "bwd": None},  # computed from the actual atom count
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="metric")
+    p.add_argument("--repeats", type=int, default=7, help="timed regions of K steps; the median is reported")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds of the cpu_baseline sample")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def cfg_key(c):
+    return c if c == "metric" else int(c)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- distributed
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and world == 1:
+        raise SystemExit("--gpus N > 1 needs torchrun --nproc-per-node N (one process per GPU)")
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return world, rank, local, dist
+    if torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return 1, 0, 0, None
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def max_over_ranks(x, dist):
+    if dist is None:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, dist):
+    if dist is None:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# --------------------------------------------------------------- workloads
+class BackboneWork:
+    model = "backbone"
+
+    def __init__(self, c, rank):
+        cfg = synth.CONFIGS[c]
+        self.cfg = cfg
+        # weak scaling: rank r draws its own batch (seed offset by rank)
+        ang, lengths, grad = synth.backbone_inputs(c)
+        if rank:
+            ang = synth.angles_uniform(ang.shape[0], ang.shape[1], 3, 1000 + synth.config_id(c) + 7919 * rank)
+        self.host = dict(angles=ang, lengths=lengths, grad=grad)
+        self.B, self.Lmax = ang.shape[0], ang.shape[1]
+        self.residues = int(lengths.sum())
+
+    def alloc_set(self, ws_bytes):
+        from paper_1812_01108_b200 import _abi
+
+        h = self.host
+        s = dict(angles=h["angles"].cuda(), lengths=h["lengths"].cuda(), grad=h["grad"].cuda(),
+                 coords=torch.empty((self.B, 3 * self.Lmax, 3), device="cuda"),
+                 gang=torch.zeros((self.B, self.Lmax, 3), device="cuda"),
+                 ws=torch.zeros(_abi.tpl_workspace_bytes(0, self.B, self.Lmax), dtype=torch.uint8, device="cuda"))
+        return s
+
+    def footprint(self):
+        return self.B * self.Lmax * (12 + 36 + 36 + 12)
+
+    def fwd(self, s, stream=None):
+        from paper_1812_01108_b200 import _abi
+
+        _abi.tpl_backbone_forward(s["angles"], s["lengths"], s["coords"], s["ws"], stream)
+
+    def bwd(self, s, stream=None):
+        from paper_1812_01108_b200 import _abi
+
+        _abi.tpl_backbone_backward(s["angles"], s["lengths"], s["grad"], s["gang"], s["ws"], stream)
+
+    def algo_bytes(self):
+        return {k: v * self.residues for k, v in BYTES_PER_RES["backbone"].items()}
+
+    def e2e_io(self):
+        h = self.host
+        return ([("angles", h["angles"]), ("grad", h["grad"])], [("coords", (self.B, 3 * self.Lmax, 3)),
+                                                                  ("gang", (self.B, self.Lmax, 3))])
+
+    def config(self):
+        return {"workload": f"backbone phi,psi,omega -> N,CA,C; L={self.Lmax}, batch {self.B} per GPU",
+                "L": self.Lmax, "batch_per_gpu": self.B}
+
+
+class FullAtomWork:
+    model = "fullatom"
+
+    def __init__(self, c, rank):
+        import paper_1812_01108_b200 as tpl
+
+        cfg = synth.CONFIGS[c]
+        self.cfg = cfg
+        B = cfg["B"]
+        ang, rt, lengths = synth.fullatom_inputs(c, B=B)
+        if rank:
+            ang = synth.angles_uniform(B, cfg["L"], 8, 1000 + synth.config_id(c) + 7919 * rank)
+            rt = synth.restype_uniform(B, cfg["L"], 20, 4000 + synth.config_id(c) + 7919 * rank)
+        self.table = synth.load_residue_table()
+        self.tables = tpl.Tables(self.table)
+        apc, stride = self.tables.atoms(rt, lengths)
+        self.stride = stride
+        self.atoms = int(apc.sum())
+        grad = synth.fullatom_grad(B, stride, synth.config_id(c))
+        self.host = dict(angles=ang, restype=rt, lengths=lengths, grad=grad)
+        self.B, self.Lmax = B, cfg["L"]
+        self.residues = int(lengths.sum())
+
+    def alloc_set(self, ws_bytes):
+        from paper_1812_01108_b200 import _abi
+
+        h = self.host
+        return dict(angles=h["angles"].cuda(), restype=h["restype"].cuda(), lengths=h["lengths"].cuda(),
+                    grad=h["grad"].cuda(), coords=torch.empty((self.B, self.stride, 3), device="cuda"),
+                    gang=torch.zeros((self.B, self.Lmax, 8), device="cuda"),
+                    ws=torch.zeros(_abi.tpl_workspace_bytes(1, self.B, self.Lmax), dtype=torch.uint8,
+                                   device="cuda"))
+
+    def footprint(self):
+        return self.B * self.Lmax * (32 + 1 + 32) + self.B * self.stride * 24
+
+    def fwd(self, s, stream=None):
+        from paper_1812_01108_b200 import _abi
+
+        _abi.tpl_fullatom_forward(self.tables.handle, s["angles"], s["restype"], s["lengths"], s["coords"], s["ws"],
+                                  stream)
+
+    def bwd(self, s, stream=None):
+        from paper_1812_01108_b200 import _abi
+
+        _abi.tpl_fullatom_backward(self.tables.handle, s["angles"], s["restype"], s["lengths"], s["grad"],
+                                   s["gang"], s["ws"], stream)
+
+    def algo_bytes(self):
+        r, a = self.residues, self.atoms
+        return {"fwd": r * (32 + 1) + a * 12, "bwd": r * (32 + 1 + 32) + a * 12}
+
+    def e2e_io(self):
+        h = self.host
+        return ([("angles", h["angles"]), ("restype", h["restype"]), ("grad", h["grad"])],
+                [("coords", (self.B, self.stride, 3)), ("gang", (self.B, self.Lmax, 8))])
+
+    def config(self):
+        return {"workload": f"full-atom phi,psi,omega,chi1-5 -> heavy atoms; 20 random residue types; "
+                            f"L={self.Lmax}, batch {self.B} per GPU", "L": self.Lmax, "batch_per_gpu": self.B,
+                "atoms_per_gpu": self.atoms}
+
+
+def make_work(c, rank):
+    return (BackboneWork if synth.CONFIGS[c]["model"] == "backbone" else FullAtomWork)(c, rank)
+
+
+# --------------------------------------------------------------- graphs
+def capture(work, sets, steps, which):
+    """A CUDA graph of `steps` consecutive steps over the rotating sets."""
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        with torch.cuda.graph(g, stream=st):
+            for i in range(steps):
+                s = sets[i % len(sets)]
+                if which in ("step", "fwd"):
+                    work.fwd(s)
+                if which in ("step", "bwd"):
+                    work.bwd(s)
+    torch.cuda.current_stream().wait_stream(st)
+    torch.cuda.synchronize()
+    return g
+
+
+def timed_replays(graphs, dist):
+    """Replay the graph list once inside barrier + sync brackets; CUDA-event ms."""
+    barrier(dist)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for g in graphs:
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier(dist)
+    return e0.elapsed_time(e1)
+
+
+def run_ours(args):
+    import paper_1812_01108_b200 as tpl  # noqa: F401  (fails loudly without libtpl.so)
+
+    world, rank, local, dist = dist_setup(args)
+    c = cfg_key(args.config)
+    work = make_work(c, rank)
+    props = torch.cuda.get_device_properties(local)
+    l2 = getattr(props, "L2_cache_size", 126 * 2 ** 20)
+    n_sets = max(2, math.ceil(4 * l2 / work.footprint()))
+    n_sets = min(n_sets, max(2, int(0.5 * props.total_memory / work.footprint())))
+    sets = [work.alloc_set(0) for _ in range(n_sets)]
+    torch.cuda.synchronize()
+    K, W = args.steps, args.warmup
+
+    # warm-up (also sets kernel attributes before capture)
+    for i in range(max(W, 3)):
+        work.fwd(sets[i % n_sets])
+        work.bwd(sets[i % n_sets])
+    torch.cuda.synchronize()
+    from paper_1812_01108_b200 import _abi
+
+    _abi.tpl_sync_status(sets[0]["ws"])
+
+    def graphs_for(which):
+        full, rem = divmod(K, n_sets)
+        gs = []
+        if full:
+            g = capture(work, sets, n_sets, which)
+            gs += [g] * full
+        if rem:
+            gs.append(capture(work, sets, rem, which))
+        return gs
+
+    step_graphs = graphs_for("step")
+    fwd_graphs = graphs_for("fwd")
+    bwd_graphs = graphs_for("bwd")
+    # graph warm-up
+    for g in set(step_graphs):
+        g.replay()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    t_step, t_fwd, t_bwd = [], [], []
+    t_end = time.time() + 1.0
+    r = 0
+    while r < args.repeats or time.time() < t_end:
+        t_step.append(max_over_ranks(timed_replays(step_graphs, dist), dist))
+        t_fwd.append(max_over_ranks(timed_replays(fwd_graphs, dist), dist))
+        t_bwd.append(max_over_ranks(timed_replays(bwd_graphs, dist), dist))
+        r += 1
+        if r >= 200:
+            break
+    clocks = sampler.stop()
+    ms_step = statistics.median(t_step) / K
+    ms_fwd = statistics.median(t_fwd) / K
+    ms_bwd = statistics.median(t_bwd) / K
+    for s in sets[:1]:
+        _abi.tpl_sync_status(s["ws"])
+
+    residues_all = sum_over_ranks(work.residues, dist)
+    value = residues_all / (ms_step * 1e-3)
+
+    # e2e: the same step through the public binding with pinned HOST buffers,
+    # H2D of the inputs and D2H of the results inside the timed region.
+    e2e = None
+    if not args.no_e2e:
+        ins, outs = work.e2e_io()
+        host_in = {k: v.pin_memory() for k, v in ins}
+        host_out = {k: torch.empty(shape, dtype=torch.float32).pin_memory() for k, shape in outs}
+        s = sets[0]
+        h2d = sum(v.numel() * v.element_size() for v in host_in.values())
+        d2h = sum(v.numel() * v.element_size() for v in host_out.values())
+        Ke = max(3, min(K, 50))
+
+        def e2e_step():
+            for k, v in host_in.items():
+                s[k].copy_(v, non_blocking=True)
+            work.fwd(s)
+            work.bwd(s)
+            for k, v in host_out.items():
+                v.copy_(s[k], non_blocking=True)
+
+        for _ in range(3):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier(dist)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(Ke):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1) / Ke, dist)
+        e2e = {"value": residues_all / (ms_e2e * 1e-3), "unit": "residues/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e, "steps": Ke,
+               "path": "pinned host -> cudaMemcpyAsync -> tpl_*_forward/backward (C ABI) -> pinned host"}
+
+    # roofline of the dominant kernel
+    peak, peak_src = load_peaks()
+    ab = work.algo_bytes()
+    dom = "bwd" if ms_bwd >= ms_fwd else "fwd"
+    ms_dom = ms_bwd if dom == "bwd" else ms_fwd
+    achieved = ab[dom] / (ms_dom * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{work.model}_{args.config}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(dom)
+    roof = {"bound": "hbm", "kernel": f"{work.model}_{dom}", "achieved": round(achieved, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+            "algorithmic_bytes_per_launch": int(ab[dom]), "ms_per_launch": ms_dom, "peak_source": peak_src,
+            "fwd": {"ms": ms_fwd, "GB/s": ab["fwd"] / (ms_fwd * 1e-3) / 1e9},
+            "bwd": {"ms": ms_bwd, "GB/s": ab["bwd"] / (ms_bwd * 1e-3) / 1e9},
+            "step_GB/s": (ab["fwd"] + ab["bwd"]) / (ms_step * 1e-3) / 1e9,
+            "step_frac": (ab["fwd"] + ab["bwd"]) / (ms_step * 1e-3) / 1e9 / peak}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(work, args.cpu_seconds)
+
+    if rank == 0:
+        cfgd = work.config()
+        cfgd.update({"global_batch": work.B * world, "parallelism": f"dp{world} (chains sharded, no collective)",
+                     "l2_flush": f"rotating {n_sets} buffer sets ({n_sets * work.footprint() / 2**20:.0f} MiB > 4x L2)",
+                     "timing": f"CUDA graphs of K steps, median of {len(t_step)} timed regions"})
+        out = {"metric": f"residues/sec fwd+bwd ({work.model}, L={work.Lmax}, batch {work.B})",
+               "value": value, "unit": "residues/s", "n_gpus": world, "steps": K, "warmup": W,
+               "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "dtype": "f32", "data": "synthetic (seeded uniform angles, N(0,1) dL/dr)", "config": cfgd,
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": 2 * K,
+               "impl": "ours"}
+        print(json.dumps(out))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------------- CPU oracle
+def cpu_baseline(work, seconds):
+    """The fp64 oracle as it stands (paper-literal O(L^2) backward, OpenMP over
+    chains) on this host's cores, on a bounded sample of the same workload."""
+    import oracle
+
+    oracle.build()
+    h = work.host
+    a64 = synth.numpy64(h["angles"])
+    g64 = synth.numpy64(h["grad"])
+    ln = h["lengths"].numpy()
+    B = a64.shape[0]
+    threads = oracle.num_threads()
+
+    def run(idx):
+        if work.model == "backbone":
+            oracle.backbone_forward(a64[idx], ln[idx])
+            oracle.backbone_backward(a64[idx], ln[idx], g64[idx])
+        else:
+            rt = h["restype"].numpy()
+            oracle.fullatom_forward(work.table, a64[idx], rt[idx], ln[idx], work.stride)
+            oracle.fullatom_backward(work.table, a64[idx], rt[idx], ln[idx], g64[idx])
+
+    # calibrate on `threads` chains, then size the sample to ~`seconds`
+    idx = np.arange(min(B, threads))
+    t0 = time.perf_counter()
+    run(idx)
+    t1 = time.perf_counter() - t0
+    n = int(min(B, max(threads, threads * math.floor(seconds / max(t1, 1e-3)))))
+    idx = np.arange(n)
+    t0 = time.perf_counter()
+    run(idx)
+    dt = time.perf_counter() - t0
+    res = float(ln[idx].sum())
+    return {"value": res / dt, "unit": "residues/s", "cores": threads, "kind": "oracle",
+            "sample": f"{n} of {B} chains of the same workload (fwd + O(L^2) bwd, fp64), {dt:.1f} s",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed as the reference arm (rank 0 only)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    oracle.build()
+    c = cfg_key(args.config)
+    cfg = synth.CONFIGS[c]
+
+    class H:  # host-only view of the workload (no GPU needed)
+        pass
+
+    work = H()
+    work.model = cfg["model"]
+    if work.model == "backbone":
+        ang, lengths, grad = synth.backbone_inputs(c)
+    else:
+        ang, rt, lengths = synth.fullatom_inputs(c)
+        work.table = synth.load_residue_table()
+        na = oracle.chain_atom_counts(work.table, rt.numpy(), lengths.numpy())
+        work.stride = int(na.max())
+        grad = synth.fullatom_grad(ang.shape[0], work.stride, synth.config_id(c))
+        work.host_rt = rt
+    a64, g64, ln = synth.numpy64(ang), synth.numpy64(grad), lengths.numpy()
+    threads = oracle.num_threads()
+    K, W = args.steps, args.warmup
+
+    def run(idx):
+        if work.model == "backbone":
+            oracle.backbone_forward(a64[idx], ln[idx])
+            oracle.backbone_backward(a64[idx], ln[idx], g64[idx])
+        else:
+            r = work.host_rt.numpy()
+            oracle.fullatom_forward(work.table, a64[idx], r[idx], ln[idx], work.stride)
+            oracle.fullatom_backward(work.table, a64[idx], r[idx], ln[idx], g64[idx])
+
+    B = a64.shape[0]
+    t0 = time.perf_counter()
+    run(np.arange(min(B, threads)))
+    t1 = time.perf_counter() - t0
+    budget = 150.0  # seconds for the whole K + W run
+    per_step = budget / max(1, K + W)
+    n = int(max(1, min(B, threads * math.floor(per_step / max(t1, 1e-3))))) if per_step >= t1 else max(
+        1, int(threads * per_step / max(t1, 1e-3)))
+    n = min(n, B)
+    times, res = [], 0.0
+    for i in range(W + K):
+        idx = (np.arange(n) + i * n) % B
+        s = time.perf_counter()
+        run(idx)
+        e = time.perf_counter() - s
+        if i >= W:
+            times.append(e)
+            res += float(ln[idx].sum())
+    total = sum(times)
+    value = res / total
+    line = {"metric": f"residues/sec fwd+bwd ({work.model}, L={cfg['L']}, batch {cfg['B']})", "value": value,
+            "unit": "residues/s", "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": 1e3 * total / K,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded uniform angles, N(0,1) dL/dr)",
+            "config": {"workload": f"{work.model} L={cfg['L']} batch {cfg['B']}", "sample_chains_per_step": n},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "residues/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{n} chains per step of the {cfg['B']}-chain workload"},
+            "e2e": {"value": value, "unit": "residues/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,186 @@
+/*
+ * tpl.h -- C ABI v1 of libtpl.so: batched, differentiable dihedral-angle ->
+ * Cartesian-coordinate maps of arXiv 1812.01108 (TorchProteinLibrary) on B200.
+ *
+ * No CUDA headers: device pointers are plain pointers, streams are passed as
+ * void* (a cudaStream_t; NULL = the legacy default stream).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * Ownership   The caller owns every buffer.  fwd/bwd calls never allocate;
+ *             only tpl_tables_create allocates (device memory for the table).
+ * Streams     All device work is enqueued on `stream`; nothing synchronises
+ *             except tpl_sync_status.
+ * Memory      Every array argument of a fwd/bwd call is DEVICE memory
+ *             (lengths included), dense row-major as documented, 4-byte
+ *             aligned; 16-byte alignment lets more of it move by TMA bulk
+ *             copies but is not required.
+ * Padding     Entries of a chain past lengths[b] are neither read nor written.
+ * Errors      Host-detectable problems (NULL, B < 1, Lmax < 1, workspace too
+ *             small, atom_stride too small, bad table) return a status BEFORE
+ *             any launch and set tpl_last_error().  Device-detectable
+ *             problems (lengths[b] outside [1, Lmax], a restype >= n_types)
+ *             set a flag in the workspace, the offending chain is skipped,
+ *             and tpl_sync_status reports TPL_ERR_DEVICE_INPUT.  No C++
+ *             exception crosses the ABI.
+ * Workspace   Device buffer of tpl_workspace_bytes(model, B, Lmax) bytes,
+ *             ZERO-INITIALISED before first use; reusable across calls on
+ *             the same stream; one workspace per concurrently used stream.
+ * Determinism Bitwise identical results for identical inputs on one build
+ *             and device: no float atomics, fixed association order.
+ * Precision   fp32 arithmetic with FMA contraction, accurate sincosf (no
+ *             fast-math); fixed theta/d constants are rounded from fp64.
+ *             Scan aggregates are re-orthonormalised (one Newton-Schulz
+ *             step) unless the environment sets TPL_ORTHO=0.
+ */
+#ifndef TPL_H
+#define TPL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TPL_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define TPL_API __attribute__((visibility("default")))
+#else
+#define TPL_API
+#endif
+
+typedef enum {
+    TPL_OK = 0,
+    TPL_ERR_NULL = 1,         /* a required pointer is NULL */
+    TPL_ERR_SHAPE = 2,        /* B < 1, Lmax < 1, atom_stride too small, ... */
+    TPL_ERR_ALIGN = 3,        /* a pointer is not 4-byte aligned */
+    TPL_ERR_TABLE = 4,        /* residue-type table rejected */
+    TPL_ERR_CUDA = 5,         /* a CUDA runtime call failed (see tpl_last_error) */
+    TPL_ERR_DEVICE_INPUT = 6, /* a kernel flagged a bad length / restype */
+    TPL_ERR_WORKSPACE = 7     /* workspace NULL or smaller than tpl_workspace_bytes */
+} tpl_status;
+
+#define TPL_MODEL_BACKBONE 0
+#define TPL_MODEL_FULLATOM 1
+
+/* Slots of the per-residue angle record.  Backbone records have 3 slots
+ * (phi, psi, omega); full-atom records 8 (phi, psi, omega, chi1..chi5),
+ * reading Q10 of DESIGN.md ("up to 7 dihedral angles", plus chi5). */
+#define TPL_BB_SLOTS 3
+#define TPL_FA_SLOTS 8
+#define TPL_SLOT_PHI 0
+#define TPL_SLOT_PSI 1
+#define TPL_SLOT_OMEGA 2
+#define TPL_SLOT_CHI1 3
+
+#define TPL_MAX_GROUPS 8   /* side-chain rigid groups per residue type */
+#define TPL_MAX_ATOMS 16   /* atoms per residue type (N, CA, side chain, C, O) */
+#define TPL_MAX_TYPES 32   /* residue types per table */
+
+/* Owner of an atom in a residue type: the N, CA or C backbone frame, or a
+ * side-chain group index >= 0. */
+#define TPL_OWNER_N (-3)
+#define TPL_OWNER_CA (-2)
+#define TPL_OWNER_C (-1)
+
+/* Thread-local text describing the last non-OK status of this thread. */
+TPL_API const char* tpl_last_error(void);
+TPL_API int tpl_abi_version(void);
+
+/* Device workspace bytes needed by any fwd/bwd call of `model` with these
+ * B and Lmax (error word + per-tile prefix carries of long chains). */
+TPL_API size_t tpl_workspace_bytes(int32_t model, int32_t B, int32_t Lmax);
+
+/* Synchronise `stream`, then read and clear the device error flags of
+ * `workspace`.  TPL_ERR_DEVICE_INPUT if a kernel skipped a chain. */
+TPL_API tpl_status tpl_sync_status(void* stream, void* workspace);
+
+/* ======================================================================
+ * Backbone model (§3)
+ * ====================================================================== */
+
+/* Atoms of a backbone chain of L residues: 3L (N, CA, C). */
+TPL_API int64_t tpl_backbone_atoms(int32_t L);
+
+/* Forward.  P:143-175: r_i = R_0 R_1 ... R_i 0 with the transform table of
+ * atom 3j (N_j) via R(omega_{j-1}, pi-2.1186, 1.330), atom 3j+1
+ * (CA_j) via R(phi_j, pi-1.9391, 1.460), atom 3j+2 (C_j) via
+ * R(psi_j, pi-2.0610, 1.525); R_0 = I (N_0 at the origin, reading Q1) and
+ * omega_j is the C_j-N_{j+1} torsion (reading Q2).
+ *   angles   [B][Lmax][3] fp32, (phi, psi, omega) in radians, any real value
+ *   lengths  [B] int32, each in [1, Lmax]
+ *   coords   [B][3*Lmax][3] fp32 output, Angstrom, atoms N, CA, C per residue */
+TPL_API tpl_status tpl_backbone_forward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                float* coords, void* workspace, size_t ws_bytes, void* stream);
+
+/* Backward: dL/dangles for L with dL/dr = grad_coords (Eq. 2),
+ * recomputed from the angles (no saved forward state).
+ *   grad_coords [B][3*Lmax][3] fp32
+ *   grad_angles [B][Lmax][3]   fp32 output; psi_{L-1} and omega_{L-1} are 0 */
+TPL_API tpl_status tpl_backbone_backward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                 const float* grad_coords, float* grad_angles, void* workspace, size_t ws_bytes,
+                                 void* stream);
+
+/* ======================================================================
+ * Full-atom model (§2)
+ * ====================================================================== */
+
+/* One residue type (host memory, plain data).  The backbone nodes are
+ * implicit and use the §3 constants: N_j (from C_{j-1} by omega_{j-1}),
+ * CA_j (phi_j), C_j (psi_j).  Side-chain group g is reached from its parent
+ * frame P by  M_g = P * R_x(group_pre_rx[g]) * R(alpha, theta, d)  (R' of
+ * P:48 when pre_rx != 0) with alpha = angles[slot] for slot in 3..7
+ * (chi1..chi5) or the fixed group_alpha[g] when slot < 0.
+ * v1 restriction: group_parent[g] is -1 (the CA frame) or g-1.
+ * Atoms: r = M_owner r°, owner = TPL_OWNER_N/CA/C or a group;
+ * atoms are listed in output order, which must be owner-sorted as
+ *   N-owned, CA-owned, group 0, group 1, ..., C-owned
+ * (e.g. N, CA, side chain depth-first, C, O: reading Q9). */
+typedef struct tpl_residue_desc {
+    int32_t n_groups;
+    int32_t n_atoms;
+    int32_t group_parent[TPL_MAX_GROUPS];
+    int32_t group_slot[TPL_MAX_GROUPS];
+    double group_alpha[TPL_MAX_GROUPS];
+    double group_theta[TPL_MAX_GROUPS];
+    double group_d[TPL_MAX_GROUPS];
+    double group_pre_rx[TPL_MAX_GROUPS];
+    int32_t atom_owner[TPL_MAX_ATOMS];
+    double atom_r[TPL_MAX_ATOMS][3];
+} tpl_residue_desc;
+
+typedef struct tpl_tables tpl_tables; /* opaque, immutable after create */
+
+/* Validate and upload `n_types` (1..TPL_MAX_TYPES) residue types; uses the
+ * current CUDA device.  *out is NULL on failure. */
+TPL_API tpl_status tpl_tables_create(const tpl_residue_desc* types, int32_t n_types, tpl_tables** out);
+TPL_API void tpl_tables_destroy(tpl_tables* tables);
+TPL_API int32_t tpl_tables_n_types(const tpl_tables* tables);
+
+/* Host-side bookkeeping: atoms_per_chain[b] (may be NULL) and the padded
+ * *atom_stride = max_b atoms (rounded up to a multiple of 4) for HOST
+ * restype [B][Lmax] and lengths [B]. */
+TPL_API tpl_status tpl_fullatom_atoms(const tpl_tables* tables, const uint8_t* restype_host, const int32_t* lengths_host,
+                              int32_t B, int32_t Lmax, int32_t* atoms_per_chain, int32_t* atom_stride);
+
+/* Forward.  angles [B][Lmax][8] fp32, restype [B][Lmax] uint8 (device),
+ * coords [B][atom_stride][3] fp32 output: each chain's atoms packed from
+ * index 0, residue by residue, in the table's atom order. */
+TPL_API tpl_status tpl_fullatom_forward(const tpl_tables* tables, const float* angles, const uint8_t* restype,
+                                const int32_t* lengths, int32_t B, int32_t Lmax, int32_t atom_stride,
+                                float* coords, void* workspace, size_t ws_bytes, void* stream);
+
+/* Backward (Eq. 1, in O(L) with suffix sums): grad_coords in the
+ * coords layout, grad_angles [B][Lmax][8] output; fixed and unused slots
+ * and omega_{L-1} are 0. */
+TPL_API tpl_status tpl_fullatom_backward(const tpl_tables* tables, const float* angles, const uint8_t* restype,
+                                 const int32_t* lengths, int32_t B, int32_t Lmax, int32_t atom_stride,
+                                 const float* grad_coords, float* grad_angles, void* workspace, size_t ws_bytes,
+                                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPL_H */

@@ -1,0 +1,197 @@
+"""ctypes binding of libtpl.so (include/tpl.h).  Argument marshalling only.
+
+Every function named ``tpl_*`` here has the C entry point's name and argument
+order; tensors stand in for pointers (device tensors for the fwd/bwd calls,
+host tensors for the bookkeeping call).  All arithmetic of the method runs in
+the CUDA kernels of libtpl.so; if the library is missing this module raises
+on import -- there is no CPU fallback.
+"""
+import ctypes
+import os
+
+import torch  # loads libcudart.so.12 before libtpl.so resolves it
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtpl.so")
+
+TPL_OK = 0
+STATUS = {0: "TPL_OK", 1: "TPL_ERR_NULL", 2: "TPL_ERR_SHAPE", 3: "TPL_ERR_ALIGN", 4: "TPL_ERR_TABLE",
+          5: "TPL_ERR_CUDA", 6: "TPL_ERR_DEVICE_INPUT", 7: "TPL_ERR_WORKSPACE"}
+MODEL_BACKBONE, MODEL_FULLATOM = 0, 1
+MAX_GROUPS, MAX_ATOMS, MAX_TYPES = 8, 16, 32
+BB_SLOTS, FA_SLOTS = 3, 8
+OWNER_N, OWNER_CA, OWNER_C = -3, -2, -1
+
+# Every symbol include/tpl.h declares (checked by tests/test_abi_cpu.py).
+EXPORTS = [
+    "tpl_last_error", "tpl_abi_version", "tpl_workspace_bytes", "tpl_sync_status", "tpl_backbone_atoms",
+    "tpl_backbone_forward", "tpl_backbone_backward", "tpl_tables_create", "tpl_tables_destroy",
+    "tpl_tables_n_types", "tpl_fullatom_atoms", "tpl_fullatom_forward", "tpl_fullatom_backward",
+]
+
+
+class TplError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class ResidueDesc(ctypes.Structure):
+    """Mirror of ``tpl_residue_desc``."""
+
+    _fields_ = [
+        ("n_groups", ctypes.c_int32),
+        ("n_atoms", ctypes.c_int32),
+        ("group_parent", ctypes.c_int32 * MAX_GROUPS),
+        ("group_slot", ctypes.c_int32 * MAX_GROUPS),
+        ("group_alpha", ctypes.c_double * MAX_GROUPS),
+        ("group_theta", ctypes.c_double * MAX_GROUPS),
+        ("group_d", ctypes.c_double * MAX_GROUPS),
+        ("group_pre_rx", ctypes.c_double * MAX_GROUPS),
+        ("atom_owner", ctypes.c_int32 * MAX_ATOMS),
+        ("atom_r", (ctypes.c_double * 3) * MAX_ATOMS),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, sz, i32, i64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_int64
+    L.tpl_last_error.restype = ctypes.c_char_p
+    L.tpl_last_error.argtypes = []
+    L.tpl_abi_version.restype = ctypes.c_int
+    L.tpl_workspace_bytes.restype = sz
+    L.tpl_workspace_bytes.argtypes = [i32, i32, i32]
+    L.tpl_sync_status.restype = ctypes.c_int
+    L.tpl_sync_status.argtypes = [vp, vp]
+    L.tpl_backbone_atoms.restype = i64
+    L.tpl_backbone_atoms.argtypes = [i32]
+    L.tpl_backbone_forward.restype = ctypes.c_int
+    L.tpl_backbone_forward.argtypes = [vp, vp, i32, i32, vp, vp, sz, vp]
+    L.tpl_backbone_backward.restype = ctypes.c_int
+    L.tpl_backbone_backward.argtypes = [vp, vp, i32, i32, vp, vp, vp, sz, vp]
+    L.tpl_tables_create.restype = ctypes.c_int
+    L.tpl_tables_create.argtypes = [ctypes.POINTER(ResidueDesc), i32, ctypes.POINTER(vp)]
+    L.tpl_tables_destroy.restype = None
+    L.tpl_tables_destroy.argtypes = [vp]
+    L.tpl_tables_n_types.restype = i32
+    L.tpl_tables_n_types.argtypes = [vp]
+    L.tpl_fullatom_atoms.restype = ctypes.c_int
+    L.tpl_fullatom_atoms.argtypes = [vp, vp, vp, i32, i32, vp, ctypes.POINTER(i32)]
+    L.tpl_fullatom_forward.restype = ctypes.c_int
+    L.tpl_fullatom_forward.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, sz, vp]
+    L.tpl_fullatom_backward.restype = ctypes.c_int
+    L.tpl_fullatom_backward.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]
+    return L
+
+
+lib = _load()
+
+
+def _check(status):
+    if status != TPL_OK:
+        raise TplError(status, lib.tpl_last_error().decode(errors="replace"))
+
+
+def _dev(t, dtype, name):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (libtpl has no CPU path)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def tpl_abi_version():
+    return int(lib.tpl_abi_version())
+
+
+def tpl_workspace_bytes(model, B, Lmax):
+    return int(lib.tpl_workspace_bytes(int(model), int(B), int(Lmax)))
+
+
+def tpl_backbone_atoms(L):
+    return int(lib.tpl_backbone_atoms(int(L)))
+
+
+def tpl_sync_status(workspace, stream=None):
+    _check(lib.tpl_sync_status(_stream(stream), _dev(workspace, torch.uint8, "workspace")))
+
+
+def tpl_backbone_forward(angles, lengths, coords, workspace, stream=None):
+    B, Lmax, three = angles.shape
+    if three != BB_SLOTS or tuple(coords.shape) != (B, 3 * Lmax, 3) or tuple(lengths.shape) != (B,):
+        raise ValueError("shapes: angles [B,Lmax,3], lengths [B], coords [B,3*Lmax,3]")
+    _check(lib.tpl_backbone_forward(_dev(angles, torch.float32, "angles"), _dev(lengths, torch.int32, "lengths"),
+                                    B, Lmax, _dev(coords, torch.float32, "coords"),
+                                    _dev(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream)))
+
+
+def tpl_backbone_backward(angles, lengths, grad_coords, grad_angles, workspace, stream=None):
+    B, Lmax, three = angles.shape
+    if (three != BB_SLOTS or tuple(grad_coords.shape) != (B, 3 * Lmax, 3)
+            or tuple(grad_angles.shape) != (B, Lmax, 3) or tuple(lengths.shape) != (B,)):
+        raise ValueError("shapes: angles/grad_angles [B,Lmax,3], lengths [B], grad_coords [B,3*Lmax,3]")
+    _check(lib.tpl_backbone_backward(_dev(angles, torch.float32, "angles"), _dev(lengths, torch.int32, "lengths"),
+                                     B, Lmax, _dev(grad_coords, torch.float32, "grad_coords"),
+                                     _dev(grad_angles, torch.float32, "grad_angles"),
+                                     _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                     _stream(stream)))
+
+
+def tpl_tables_create(descs):
+    """descs: a ctypes array of ResidueDesc; returns the opaque handle (int)."""
+    h = ctypes.c_void_p()
+    _check(lib.tpl_tables_create(descs, len(descs), ctypes.byref(h)))
+    return h.value
+
+
+def tpl_tables_destroy(handle):
+    lib.tpl_tables_destroy(ctypes.c_void_p(handle))
+
+
+def tpl_tables_n_types(handle):
+    return int(lib.tpl_tables_n_types(ctypes.c_void_p(handle)))
+
+
+def tpl_fullatom_atoms(handle, restype_host, lengths_host):
+    """Host bookkeeping: (atoms_per_chain int32 [B], atom_stride)."""
+    rt = restype_host.to(torch.uint8).contiguous().cpu()
+    ln = lengths_host.to(torch.int32).contiguous().cpu()
+    B, Lmax = rt.shape
+    apc = torch.zeros(B, dtype=torch.int32)
+    stride = ctypes.c_int32(0)
+    _check(lib.tpl_fullatom_atoms(ctypes.c_void_p(handle), ctypes.c_void_p(rt.data_ptr()),
+                                  ctypes.c_void_p(ln.data_ptr()), B, Lmax, ctypes.c_void_p(apc.data_ptr()),
+                                  ctypes.byref(stride)))
+    return apc, int(stride.value)
+
+
+def tpl_fullatom_forward(handle, angles, restype, lengths, coords, workspace, stream=None):
+    B, Lmax, slots = angles.shape
+    if slots != FA_SLOTS or tuple(restype.shape) != (B, Lmax) or coords.dim() != 3 or coords.shape[0] != B:
+        raise ValueError("shapes: angles [B,Lmax,8], restype [B,Lmax], coords [B,atom_stride,3]")
+    _check(lib.tpl_fullatom_forward(ctypes.c_void_p(handle), _dev(angles, torch.float32, "angles"),
+                                    _dev(restype, torch.uint8, "restype"), _dev(lengths, torch.int32, "lengths"),
+                                    B, Lmax, coords.shape[1], _dev(coords, torch.float32, "coords"),
+                                    _dev(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream)))
+
+
+def tpl_fullatom_backward(handle, angles, restype, lengths, grad_coords, grad_angles, workspace, stream=None):
+    B, Lmax, slots = angles.shape
+    if slots != FA_SLOTS or tuple(grad_angles.shape) != (B, Lmax, FA_SLOTS) or grad_coords.shape[0] != B:
+        raise ValueError("shapes: angles/grad_angles [B,Lmax,8], grad_coords [B,atom_stride,3]")
+    _check(lib.tpl_fullatom_backward(ctypes.c_void_p(handle), _dev(angles, torch.float32, "angles"),
+                                     _dev(restype, torch.uint8, "restype"), _dev(lengths, torch.int32, "lengths"),
+                                     B, Lmax, grad_coords.shape[1], _dev(grad_coords, torch.float32, "grad_coords"),
+                                     _dev(grad_angles, torch.float32, "grad_angles"),
+                                     _dev(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream)))

@@ -1,0 +1,160 @@
+"""User-facing API: differentiable backbone / full-atom layers (§2, §3).
+
+    coords = backbone(angles, lengths)                      # [B, 3*Lmax, 3]
+    tables = Tables.from_json(synth.load_residue_table())   # or Tables(dict)
+    coords = fullatom(angles, restype, lengths, tables)     # [B, atom_stride, 3]
+
+Both are ``torch.autograd.Function``s running on the current CUDA stream;
+backward recomputes from the angles (nothing but the inputs is saved).
+"""
+import ctypes
+
+import torch
+
+from . import _abi
+from ._abi import MODEL_BACKBONE, MODEL_FULLATOM
+
+
+class Workspace:
+    """Zero-initialised device workspace (tpl_workspace_bytes), grown on demand.
+    One per (device, stream) in use; the error word is checked by ``check()``."""
+
+    def __init__(self, device=None):
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.buf = torch.zeros(256, dtype=torch.uint8, device=self.device)
+
+    def get(self, model, B, Lmax):
+        need = _abi.tpl_workspace_bytes(model, B, Lmax)
+        if self.buf.numel() < need:
+            self.buf = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        return self.buf
+
+    def check(self, stream=None):
+        """Synchronise and raise TplError if a kernel flagged a bad length/restype."""
+        _abi.tpl_sync_status(self.buf, stream)
+
+
+_workspaces = {}
+
+
+def default_workspace(device=None):
+    d = torch.cuda.current_device() if device is None else torch.device(device).index
+    key = (d, torch.cuda.current_stream(d).cuda_stream)
+    ws = _workspaces.get(key)
+    if ws is None:
+        ws = _workspaces[key] = Workspace(torch.device("cuda", d))
+    return ws
+
+
+class Tables:
+    """Device copy of a residue-type table (see synth/residue_table.json for
+    the format: per type, side-chain groups and atoms with standard
+    coordinates).  Immutable; freed with the object."""
+
+    def __init__(self, table):
+        types = table["types"] if isinstance(table, dict) else table
+        descs = (_abi.ResidueDesc * len(types))()
+        for t, ty in enumerate(types):
+            d = descs[t]
+            d.n_groups = len(ty["groups"])
+            d.n_atoms = len(ty["atoms"])
+            if d.n_groups > _abi.MAX_GROUPS or d.n_atoms > _abi.MAX_ATOMS:
+                raise ValueError(f"type {t}: too many groups/atoms")
+            for g, gr in enumerate(ty["groups"]):
+                d.group_parent[g] = int(gr["parent"])
+                d.group_slot[g] = int(gr["slot"])
+                d.group_alpha[g] = float(gr["alpha"])
+                d.group_theta[g] = float(gr["theta"])
+                d.group_d[g] = float(gr["d"])
+                d.group_pre_rx[g] = float(gr["pre_rx"])
+            for k, at in enumerate(ty["atoms"]):
+                d.atom_owner[k] = int(at["owner"])
+                for c in range(3):
+                    d.atom_r[k][c] = float(at["r"][c])
+        self._descs = descs
+        self.names = [ty.get("name", str(i)) for i, ty in enumerate(types)]
+        self.atoms_per_type = torch.tensor([len(ty["atoms"]) for ty in types], dtype=torch.int64)
+        self.handle = _abi.tpl_tables_create(descs)
+
+    @property
+    def n_types(self):
+        return _abi.tpl_tables_n_types(self.handle)
+
+    def atoms(self, restype, lengths):
+        """(atoms_per_chain [B] int32, atom_stride) -- host bookkeeping."""
+        return _abi.tpl_fullatom_atoms(self.handle, restype.cpu(), lengths.cpu())
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                _abi.tpl_tables_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+def _lengths_for(angles, lengths):
+    if lengths is None:
+        return torch.full((angles.shape[0],), angles.shape[1], dtype=torch.int32, device=angles.device)
+    return lengths.to(device=angles.device, dtype=torch.int32).contiguous()
+
+
+class BackboneFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, angles, lengths):
+        angles = angles.contiguous()
+        B, Lmax, _ = angles.shape
+        coords = torch.empty((B, 3 * Lmax, 3), dtype=torch.float32, device=angles.device)
+        ws = default_workspace(angles.device).get(MODEL_BACKBONE, B, Lmax)
+        _abi.tpl_backbone_forward(angles, lengths, coords, ws)
+        ctx.save_for_backward(angles, lengths)
+        ctx.mark_non_differentiable(lengths)
+        return coords
+
+    @staticmethod
+    def backward(ctx, grad_coords):
+        angles, lengths = ctx.saved_tensors
+        B, Lmax, _ = angles.shape
+        grad_angles = torch.zeros_like(angles)  # pads stay 0: the kernel never writes them
+        ws = default_workspace(angles.device).get(MODEL_BACKBONE, B, Lmax)
+        _abi.tpl_backbone_backward(angles, lengths, grad_coords.contiguous(), grad_angles, ws)
+        return grad_angles, None
+
+
+class FullAtomFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, angles, restype, lengths, tables, atom_stride):
+        angles = angles.contiguous()
+        B, Lmax, _ = angles.shape
+        coords = torch.zeros((B, atom_stride, 3), dtype=torch.float32, device=angles.device)
+        ws = default_workspace(angles.device).get(MODEL_FULLATOM, B, Lmax)
+        _abi.tpl_fullatom_forward(tables.handle, angles, restype, lengths, coords, ws)
+        ctx.save_for_backward(angles, restype, lengths)
+        ctx.tables = tables
+        return coords
+
+    @staticmethod
+    def backward(ctx, grad_coords):
+        angles, restype, lengths = ctx.saved_tensors
+        B, Lmax, _ = angles.shape
+        grad_angles = torch.zeros_like(angles)
+        ws = default_workspace(angles.device).get(MODEL_FULLATOM, B, Lmax)
+        _abi.tpl_fullatom_backward(ctx.tables.handle, angles, restype, lengths, grad_coords.contiguous(),
+                                   grad_angles, ws)
+        return grad_angles, None, None, None, None
+
+
+def backbone(angles, lengths=None):
+    """angles [B, Lmax, 3] fp32 CUDA (phi, psi, omega) -> coords [B, 3*Lmax, 3] (N, CA, C)."""
+    return BackboneFunction.apply(angles, _lengths_for(angles, lengths))
+
+
+def fullatom(angles, restype, lengths, tables, atom_stride=None):
+    """angles [B, Lmax, 8], restype [B, Lmax] uint8 -> packed coords [B, atom_stride, 3].
+    atom_stride defaults to tables.atoms(...) (a host round trip); pass it to avoid the sync."""
+    lengths = _lengths_for(angles, lengths)
+    restype = restype.to(device=angles.device, dtype=torch.uint8).contiguous()
+    if atom_stride is None:
+        _, atom_stride = tables.atoms(restype, lengths)
+    return FullAtomFunction.apply(angles, restype, lengths, tables, int(atom_stride))

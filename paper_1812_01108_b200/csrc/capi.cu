@@ -1,0 +1,384 @@
+// capi.cu -- the C ABI of libtpl.so (include/tpl.h): argument validation,
+// workspace sizing, residue-table upload and kernel launch configuration.
+// All arithmetic of the method lives in backbone.cu / fullatom.cu.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/tpl.h"
+#include "kernels.h"
+
+using namespace tpl;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+tpl_status fail(tpl_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+tpl_status fail(tpl_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+tpl_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(TPL_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
+
+bool ortho_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("TPL_ORTHO");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// the backbone transform table.  theta and d are the
+// paper's decimal constants; cos/sin are evaluated in fp64 and rounded once
+// (reading Q20).  k = 0: C-N (omega), 1: N-CA (phi), 2: CA-C (psi).
+BBConst backbone_constants() {
+    const double theta[3] = {M_PI - 2.1186, M_PI - 1.9391, M_PI - 2.0610};
+    const double d[3] = {1.330, 1.460, 1.525};
+    BBConst K;
+    for (int k = 0; k < 3; ++k) {
+        K.b[k].ct = static_cast<float>(std::cos(theta[k]));
+        K.b[k].st = static_cast<float>(std::sin(theta[k]));
+        K.b[k].d = static_cast<float>(d[k]);
+    }
+    return K;
+}
+
+constexpr size_t kWsHeader = 256;  // error word + reserved
+
+int tile_for(int model, int Lmax) { return model == TPL_MODEL_FULLATOM ? fa_tile_for(Lmax) : bb_tile_for(Lmax); }
+int max_tiles_for(int model, int Lmax) {
+    const int t = tile_for(model, Lmax);
+    return (Lmax + t - 1) / t;
+}
+
+tpl_status check_ws(int model, int B, int Lmax, void* ws, size_t ws_bytes) {
+    if (!ws) return fail(TPL_ERR_WORKSPACE, "workspace is NULL");
+    if (!aligned4(ws) || (reinterpret_cast<uintptr_t>(ws) & 15u))
+        return fail(TPL_ERR_ALIGN, "workspace must be 16-byte aligned");
+    const size_t need = tpl_workspace_bytes(model, B, Lmax);
+    if (ws_bytes < need) return fail(TPL_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+    return TPL_OK;
+}
+
+}  // namespace
+
+struct tpl_tables {
+    FAType* dev = nullptr;
+    int n_types = 0;
+    int atoms[TPL_MAX_TYPES] = {0};
+    int device = 0;
+};
+
+extern "C" {
+
+const char* tpl_last_error(void) { return g_last_error.c_str(); }
+int tpl_abi_version(void) { return TPL_ABI_VERSION; }
+int64_t tpl_backbone_atoms(int32_t L) { return L < 0 ? 0 : 3 * static_cast<int64_t>(L); }
+
+size_t tpl_workspace_bytes(int32_t model, int32_t B, int32_t Lmax) {
+    if (B < 1 || Lmax < 1) return kWsHeader;
+    const size_t tiles = static_cast<size_t>(max_tiles_for(model, Lmax));
+    return kWsHeader + static_cast<size_t>(B) * tiles * 16 * sizeof(float);
+}
+
+tpl_status tpl_sync_status(void* stream, void* workspace) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    if (!workspace) return fail(TPL_ERR_WORKSPACE, "workspace is NULL");
+    unsigned flags = 0;
+    e = cudaMemcpy(&flags, workspace, sizeof(flags), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(error word)");
+    if (flags) {
+        e = cudaMemset(workspace, 0, sizeof(unsigned));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(error word)");
+        return fail(TPL_ERR_DEVICE_INPUT, "device input error flags 0x%x (%s%s)", flags,
+                    (flags & 1u) ? "length outside [1, Lmax] " : "", (flags & 2u) ? "restype >= n_types" : "");
+    }
+    return TPL_OK;
+}
+
+// ---------------------------------------------------------------- backbone
+static tpl_status bb_common(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax, void* ws,
+                            size_t ws_bytes) {
+    if (!angles || !lengths) return fail(TPL_ERR_NULL, "angles/lengths is NULL");
+    if (B < 1 || Lmax < 1) return fail(TPL_ERR_SHAPE, "B=%d Lmax=%d must be >= 1", B, Lmax);
+    if (!aligned4(angles) || !aligned4(lengths)) return fail(TPL_ERR_ALIGN, "angles/lengths not 4-byte aligned");
+    return check_ws(TPL_MODEL_BACKBONE, B, Lmax, ws, ws_bytes);
+}
+
+tpl_status tpl_backbone_forward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                float* coords, void* workspace, size_t ws_bytes, void* stream) {
+    tpl_status s = bb_common(angles, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!coords) return fail(TPL_ERR_NULL, "coords is NULL");
+    if (!aligned4(coords)) return fail(TPL_ERR_ALIGN, "coords not 4-byte aligned");
+    BBArgs a{};
+    a.angles = angles;
+    a.lengths = lengths;
+    a.B = B;
+    a.Lmax = Lmax;
+    a.coords = coords;
+    a.err = static_cast<unsigned*>(workspace);
+    a.ws_prefix = reinterpret_cast<float*>(static_cast<char*>(workspace) + kWsHeader);
+    a.max_tiles = max_tiles_for(TPL_MODEL_BACKBONE, Lmax);
+    a.ortho = ortho_enabled();
+    a.K = backbone_constants();
+    cudaError_t e = bb_forward_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "backbone forward launch");
+    return TPL_OK;
+}
+
+tpl_status tpl_backbone_backward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                 const float* grad_coords, float* grad_angles, void* workspace, size_t ws_bytes,
+                                 void* stream) {
+    tpl_status s = bb_common(angles, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!grad_coords || !grad_angles) return fail(TPL_ERR_NULL, "grad_coords/grad_angles is NULL");
+    if (!aligned4(grad_coords) || !aligned4(grad_angles)) return fail(TPL_ERR_ALIGN, "grads not 4-byte aligned");
+    BBArgs a{};
+    a.angles = angles;
+    a.lengths = lengths;
+    a.B = B;
+    a.Lmax = Lmax;
+    a.grad_coords = grad_coords;
+    a.grad_angles = grad_angles;
+    a.err = static_cast<unsigned*>(workspace);
+    a.ws_prefix = reinterpret_cast<float*>(static_cast<char*>(workspace) + kWsHeader);
+    a.max_tiles = max_tiles_for(TPL_MODEL_BACKBONE, Lmax);
+    a.ortho = ortho_enabled();
+    a.K = backbone_constants();
+    cudaError_t e = bb_backward_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "backbone backward launch");
+    return TPL_OK;
+}
+
+// ---------------------------------------------------------------- tables
+static int owner_rank(int owner, int n_groups) {
+    if (owner == TPL_OWNER_N) return 0;
+    if (owner == TPL_OWNER_CA) return 1;
+    if (owner == TPL_OWNER_C) return 2 + n_groups;
+    return 2 + owner;
+}
+
+tpl_status tpl_tables_create(const tpl_residue_desc* types, int32_t n_types, tpl_tables** out) {
+    if (!out) return fail(TPL_ERR_NULL, "out is NULL");
+    *out = nullptr;
+    if (!types) return fail(TPL_ERR_NULL, "types is NULL");
+    if (n_types < 1 || n_types > TPL_MAX_TYPES)
+        return fail(TPL_ERR_TABLE, "n_types=%d outside [1, %d]", n_types, TPL_MAX_TYPES);
+    FAType host[TPL_MAX_TYPES];
+    std::memset(host, 0, sizeof(host));
+    tpl_tables* T = new (std::nothrow) tpl_tables();
+    if (!T) return fail(TPL_ERR_CUDA, "out of host memory");
+    for (int t = 0; t < n_types; ++t) {
+        const tpl_residue_desc& d = types[t];
+        FAType& h = host[t];
+        if (d.n_groups < 0 || d.n_groups > TPL_MAX_GROUPS || d.n_atoms < 0 || d.n_atoms > TPL_MAX_ATOMS) {
+            delete T;
+            return fail(TPL_ERR_TABLE, "type %d: n_groups=%d n_atoms=%d out of range", t, d.n_groups, d.n_atoms);
+        }
+        h.n_groups = d.n_groups;
+        h.n_atoms = d.n_atoms;
+        for (int g = 0; g < d.n_groups; ++g) {
+            const int p = d.group_parent[g];
+            const int sl = d.group_slot[g];
+            if (!(p == -1 || p == g - 1)) {
+                delete T;
+                return fail(TPL_ERR_TABLE, "type %d group %d: parent %d must be -1 (CA) or g-1 (v1)", t, g, p);
+            }
+            if (!(sl < 0 || (sl >= TPL_SLOT_CHI1 && sl < TPL_FA_SLOTS))) {
+                delete T;
+                return fail(TPL_ERR_TABLE, "type %d group %d: slot %d not in {-1, 3..7}", t, g, sl);
+            }
+            if (!std::isfinite(d.group_theta[g]) || !std::isfinite(d.group_d[g]) || !std::isfinite(d.group_alpha[g]) ||
+                !std::isfinite(d.group_pre_rx[g])) {
+                delete T;
+                return fail(TPL_ERR_TABLE, "type %d group %d: non-finite constant", t, g);
+            }
+            FAGroup& G = h.g[g];
+            G.ca = static_cast<float>(std::cos(d.group_alpha[g]));
+            G.sa = static_cast<float>(std::sin(d.group_alpha[g]));
+            G.ct = static_cast<float>(std::cos(d.group_theta[g]));
+            G.st = static_cast<float>(std::sin(d.group_theta[g]));
+            G.d = static_cast<float>(d.group_d[g]);
+            G.has_pre = d.group_pre_rx[g] != 0.0;
+            G.cb = static_cast<float>(std::cos(d.group_pre_rx[g]));
+            G.sb = static_cast<float>(std::sin(d.group_pre_rx[g]));
+            G.parent = p;
+            G.slot = sl;
+            G.first_atom = -1;
+            G.end_atom = -1;
+        }
+        int prev_rank = -1;
+        h.n_N = h.n_CA = 0;
+        h.first_C = d.n_atoms;
+        for (int k = 0; k < d.n_atoms; ++k) {
+            const int o = d.atom_owner[k];
+            if (!(o == TPL_OWNER_N || o == TPL_OWNER_CA || o == TPL_OWNER_C || (o >= 0 && o < d.n_groups))) {
+                delete T;
+                return fail(TPL_ERR_TABLE, "type %d atom %d: owner %d invalid", t, k, o);
+            }
+            const int r = owner_rank(o, d.n_groups);
+            if (r < prev_rank) {
+                delete T;
+                return fail(TPL_ERR_TABLE, "type %d atom %d: atoms must be owner-sorted (N, CA, groups, C)", t, k);
+            }
+            prev_rank = r;
+            for (int c = 0; c < 3; ++c) {
+                if (!std::isfinite(d.atom_r[k][c])) {
+                    delete T;
+                    return fail(TPL_ERR_TABLE, "type %d atom %d: non-finite r", t, k);
+                }
+                h.r[k][c] = static_cast<float>(d.atom_r[k][c]);
+            }
+            if (o == TPL_OWNER_N) h.n_N++;
+            if (o == TPL_OWNER_CA) h.n_CA++;
+            if (o == TPL_OWNER_C && h.first_C == d.n_atoms) h.first_C = k;
+            if (o >= 0) {
+                if (h.g[o].first_atom < 0) h.g[o].first_atom = k;
+                h.g[o].end_atom = k + 1;
+            }
+        }
+        // empty groups: give them an empty range at the right position
+        int next = h.n_N + h.n_CA;
+        for (int g = 0; g < d.n_groups; ++g) {
+            if (h.g[g].first_atom < 0) {
+                h.g[g].first_atom = next;
+                h.g[g].end_atom = next;
+            }
+            next = h.g[g].end_atom;
+        }
+        T->atoms[t] = d.n_atoms;
+    }
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        delete T;
+        return cuda_fail(e, "cudaGetDevice");
+    }
+    e = cudaMalloc(&T->dev, sizeof(FAType) * n_types);
+    if (e != cudaSuccess) {
+        delete T;
+        return cuda_fail(e, "cudaMalloc(tables)");
+    }
+    e = cudaMemcpy(T->dev, host, sizeof(FAType) * n_types, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(T->dev);
+        delete T;
+        return cuda_fail(e, "cudaMemcpy(tables)");
+    }
+    T->n_types = n_types;
+    T->device = dev;
+    *out = T;
+    return TPL_OK;
+}
+
+void tpl_tables_destroy(tpl_tables* T) {
+    if (!T) return;
+    if (T->dev) cudaFree(T->dev);
+    delete T;
+}
+
+int32_t tpl_tables_n_types(const tpl_tables* T) { return T ? T->n_types : 0; }
+
+tpl_status tpl_fullatom_atoms(const tpl_tables* T, const uint8_t* restype_host, const int32_t* lengths_host,
+                              int32_t B, int32_t Lmax, int32_t* atoms_per_chain, int32_t* atom_stride) {
+    if (!T || !restype_host || !lengths_host || !atom_stride) return fail(TPL_ERR_NULL, "NULL argument");
+    if (B < 1 || Lmax < 1) return fail(TPL_ERR_SHAPE, "B=%d Lmax=%d must be >= 1", B, Lmax);
+    int64_t mx = 0;
+    for (int b = 0; b < B; ++b) {
+        const int L = lengths_host[b];
+        if (L < 1 || L > Lmax) return fail(TPL_ERR_SHAPE, "lengths[%d]=%d outside [1, %d]", b, L, Lmax);
+        int64_t n = 0;
+        for (int j = 0; j < L; ++j) {
+            const int t = restype_host[static_cast<size_t>(b) * Lmax + j];
+            if (t >= T->n_types) return fail(TPL_ERR_SHAPE, "restype[%d][%d]=%d >= n_types %d", b, j, t, T->n_types);
+            n += T->atoms[t];
+        }
+        if (atoms_per_chain) atoms_per_chain[b] = static_cast<int32_t>(n);
+        if (n > mx) mx = n;
+    }
+    mx = (mx + 3) & ~int64_t(3);
+    if (mx > INT32_MAX) return fail(TPL_ERR_SHAPE, "atom stride overflows int32");
+    *atom_stride = static_cast<int32_t>(mx < 4 ? 4 : mx);
+    return TPL_OK;
+}
+
+static tpl_status fa_common(const tpl_tables* T, const float* angles, const uint8_t* restype, const int32_t* lengths,
+                            int32_t B, int32_t Lmax, int32_t atom_stride, void* ws, size_t ws_bytes) {
+    if (!T || !angles || !restype || !lengths) return fail(TPL_ERR_NULL, "tables/angles/restype/lengths is NULL");
+    if (B < 1 || Lmax < 1) return fail(TPL_ERR_SHAPE, "B=%d Lmax=%d must be >= 1", B, Lmax);
+    if (atom_stride < 1) return fail(TPL_ERR_SHAPE, "atom_stride=%d must be >= 1", atom_stride);
+    if (!aligned4(angles) || !aligned4(lengths)) return fail(TPL_ERR_ALIGN, "angles/lengths not 4-byte aligned");
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev != T->device)
+        return fail(TPL_ERR_TABLE, "tables were created on device %d, current device is %d", T->device, dev);
+    return check_ws(TPL_MODEL_FULLATOM, B, Lmax, ws, ws_bytes);
+}
+
+static FAArgs fa_args(const tpl_tables* T, const float* angles, const uint8_t* restype, const int32_t* lengths,
+                      int32_t B, int32_t Lmax, int32_t atom_stride, void* ws) {
+    FAArgs a{};
+    a.types = T->dev;
+    a.n_types = T->n_types;
+    a.angles = angles;
+    a.restype = restype;
+    a.lengths = lengths;
+    a.B = B;
+    a.Lmax = Lmax;
+    a.atom_stride = atom_stride;
+    a.err = static_cast<unsigned*>(ws);
+    a.ws_prefix = reinterpret_cast<float*>(static_cast<char*>(ws) + kWsHeader);
+    a.max_tiles = max_tiles_for(TPL_MODEL_FULLATOM, Lmax);
+    a.ortho = ortho_enabled();
+    a.K = backbone_constants();
+    return a;
+}
+
+tpl_status tpl_fullatom_forward(const tpl_tables* T, const float* angles, const uint8_t* restype,
+                                const int32_t* lengths, int32_t B, int32_t Lmax, int32_t atom_stride, float* coords,
+                                void* workspace, size_t ws_bytes, void* stream) {
+    tpl_status s = fa_common(T, angles, restype, lengths, B, Lmax, atom_stride, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!coords) return fail(TPL_ERR_NULL, "coords is NULL");
+    if (!aligned4(coords)) return fail(TPL_ERR_ALIGN, "coords not 4-byte aligned");
+    FAArgs a = fa_args(T, angles, restype, lengths, B, Lmax, atom_stride, workspace);
+    a.coords = coords;
+    cudaError_t e = fa_forward_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "full-atom forward launch");
+    return TPL_OK;
+}
+
+tpl_status tpl_fullatom_backward(const tpl_tables* T, const float* angles, const uint8_t* restype,
+                                 const int32_t* lengths, int32_t B, int32_t Lmax, int32_t atom_stride,
+                                 const float* grad_coords, float* grad_angles, void* workspace, size_t ws_bytes,
+                                 void* stream) {
+    tpl_status s = fa_common(T, angles, restype, lengths, B, Lmax, atom_stride, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!grad_coords || !grad_angles) return fail(TPL_ERR_NULL, "grad_coords/grad_angles is NULL");
+    if (!aligned4(grad_coords) || !aligned4(grad_angles)) return fail(TPL_ERR_ALIGN, "grads not 4-byte aligned");
+    FAArgs a = fa_args(T, angles, restype, lengths, B, Lmax, atom_stride, workspace);
+    a.grad_coords = grad_coords;
+    a.grad_angles = grad_angles;
+    cudaError_t e = fa_backward_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "full-atom backward launch");
+    return TPL_OK;
+}
+
+}  // extern "C"

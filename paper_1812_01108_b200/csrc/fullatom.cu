@@ -1,0 +1,630 @@
+// fullatom.cu -- batched full-atom model (§2) on sm_100a.
+//
+// Forward: the backbone chain N_j -> CA_j -> C_j -> N_{j+1} is the same
+// associative transform product as the backbone model (same §3 constants,
+// reading Q12), computed with the block-wide affine prefix scan.  After the
+// scan every residue owns its global N, CA and C frames, and places its
+// side-chain rigid groups locally:
+//     M_g = M_parent R_x(pre) R(alpha_g, theta_g, d_g),  r = M_owner r°
+// from the residue-type table staged in shared memory.  Atoms of a chain are
+// packed residue after residue; per-residue output offsets come from a
+// block-wide integer scan of the per-type atom counts, fused into the pass.
+//
+// Backward (Eq. 1): dL/dalpha_n = e_n . sum_{k in subtree(n)} (r_k - o_n) x g_k
+// (e_n = rotation axis = x-axis of frame n, o_n its origin).  With atoms
+// ordered N, CA, side chain, C, O the subtrees of the backbone nodes are
+// suffixes of the chain: phi_j -> {residue j minus N} + later residues,
+// psi_j -> {C-owned atoms of j} + later, omega_{j-1} -> residue j + later.
+// Chi subtrees are residue-local: a side-chain branch is walked from its tip
+// back to the CA frame (frames undone with the rigid inverse of each bond)
+// accumulating the local sums.  One reverse suffix scan per chain: O(L).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tpl {
+
+__host__ __device__ constexpr int r16(int x) { return (x + 15) & ~15; }
+
+template <int NT>
+struct FASmem {
+    static constexpr int NW = NT / 32;
+    static constexpr int kBar = 0;
+    static constexpr int kScan = 16;                         // NW*12 floats
+    static constexpr int kSuf = kScan + NW * 12 * 4;         // NW*6 floats
+    static constexpr int kInt = kSuf + NW * 6 * 4;           // NW ints
+    static constexpr int kTotal = r16(kInt + NW * 4);        // 12 floats
+    static constexpr int kMisc = kTotal + 48;                // 16 floats / ints
+    static constexpr int kTable = r16(kMisc + 64);           // n_types * sizeof(FAType)
+};
+
+template <int NT, int RPT>
+struct FALayout {
+    static constexpr int TILE = NT * RPT;
+    static constexpr int ang_bytes = r16(16 + 32 * (TILE + 1));
+    static constexpr int rt_bytes = r16(16 + TILE + 1);
+    // atom staging (coords out, or grad_coords in) sized at launch: 16 + 12*maxatoms*TILE
+    // grad-angle staging (backward): 16 + 32*TILE
+    static constexpr int go_bytes = r16(16 + 32 * TILE);
+};
+
+__device__ __forceinline__ void cross_acc(float s[6], float qx, float qy, float qz, float g0, float g1, float g2) {
+    s[0] += g0;
+    s[1] += g1;
+    s[2] += g2;
+    s[3] += fmaf(qy, g2, -qz * g1);
+    s[4] += fmaf(qz, g0, -qx * g2);
+    s[5] += fmaf(qx, g1, -qy * g0);
+}
+
+// e . (T - o x S) for a 6-vector (S, T)
+__device__ __forceinline__ float axis_moment(float ex, float ey, float ez, float ox, float oy, float oz,
+                                             const float s[6]) {
+    const float c0 = s[3] - fmaf(oy, s[2], -oz * s[1]);
+    const float c1 = s[4] - fmaf(oz, s[0], -ox * s[2]);
+    const float c2 = s[5] - fmaf(ox, s[1], -oy * s[0]);
+    return fmaf(ex, c0, fmaf(ey, c1, ez * c2));
+}
+
+// Backbone chunk of one thread: residues [rl0, rl0+RPT) of the tile.
+// Saves the local N, CA and C frames of every residue and returns the
+// chunk aggregate (product of all its transforms) in M.
+template <int RPT>
+__device__ __forceinline__ void fa_chunk(const float* s_ang, int rl0, int r0, int n, const BBConst& K, Aff& M,
+                                         Aff (&FN)[RPT], Aff (&FCA)[RPT], Aff (&FC)[RPT]) {
+    M = aff_identity();
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        const int rl = rl0 + q;
+        const int j = r0 + rl;
+        if (rl < n) {
+            float s, c;
+            if (j > 0) {  // N_j from C_{j-1} by omega_{j-1}  (R_0 = I for j = 0)
+                sincosf(s_ang[8 * rl - 6], &s, &c);
+                aff_bond(M, c, s, K.b[0]);
+            }
+            FN[q] = M;
+            sincosf(s_ang[8 * rl + 0], &s, &c);  // CA_j by phi_j
+            aff_bond(M, c, s, K.b[1]);
+            FCA[q] = M;
+            sincosf(s_ang[8 * rl + 1], &s, &c);  // C_j by psi_j
+            aff_bond(M, c, s, K.b[2]);
+            FC[q] = M;
+        } else {
+            FN[q] = M;
+            FCA[q] = M;
+            FC[q] = M;
+        }
+    }
+}
+
+template <int NT, int RPT, bool kOrtho>
+__global__ void __launch_bounds__(NT) fa_forward_kernel(FAArgs a, int stage_atoms_per_res) {
+    constexpr int TILE = NT * RPT;
+    using S = FASmem<NT>;
+    using Lay = FALayout<NT, RPT>;
+    extern __shared__ __align__(16) char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
+    float* s_scan = reinterpret_cast<float*>(smem + S::kScan);
+    int* s_int = reinterpret_cast<int*>(smem + S::kInt);
+    float* s_total = reinterpret_cast<float*>(smem + S::kTotal);
+    int* s_misc = reinterpret_cast<int*>(smem + S::kMisc);
+    const FAType* s_types = reinterpret_cast<const FAType*>(smem + S::kTable);
+    char* s_ang_base = smem + S::kTable + r16(a.n_types * int(sizeof(FAType)));
+    char* s_rt_base = s_ang_base + Lay::ang_bytes;
+    char* s_out_base = s_rt_base + Lay::rt_bytes;
+
+    const int b = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int L = a.lengths[b];
+    if (L < 1 || L > a.Lmax) {
+        if (tid == 0) atomicOr(a.err, ERR_LENGTH);
+        return;
+    }
+    unsigned phase = 0;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_barrier_init();
+        const unsigned tb = unsigned(a.n_types * sizeof(FAType));
+        mbar_arrive_expect_tx(bar, tb);
+        bulk_g2s(smem + S::kTable, a.types, tb, bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+
+    Aff carry = aff_identity();
+    int carry_atoms = 0;
+    const int rl0 = tid * RPT;
+    float* coords = a.coords + (size_t)b * a.atom_stride * 3;
+    for (int r0 = 0; r0 < L; r0 += TILE) {
+        const int n = min(TILE, L - r0);
+        const int pre = r0 > 0 ? 1 : 0;
+        const Span sa = make_span(a.angles + ((size_t)b * a.Lmax + r0 - pre) * kFASlots, (n + pre) * 32);
+        const Span sr = make_span(a.restype + (size_t)b * a.Lmax + r0, n);
+        if (tid == 0) {
+            bulk_wait_read_all();
+            mbar_arrive_expect_tx(bar, unsigned(sa.mid + sr.mid));
+            span_load_bulk(sa, s_ang_base, bar);
+            span_load_bulk(sr, s_rt_base, bar);
+        }
+        span_load_edges_f32(sa, s_ang_base);
+        span_load_edges_u8(sr, s_rt_base);
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        __syncthreads();
+        const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 8 * pre;
+        const unsigned char* s_rt = reinterpret_cast<const unsigned char*>(s_rt_base + sr.mis());
+
+        // residue types, atom counts, validity
+        int cnt = 0;
+        bool bad = false;
+        int typ[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const int rl = rl0 + q;
+            typ[q] = 0;
+            if (rl < n) {
+                const int t = s_rt[rl];
+                if (t >= a.n_types) bad = true;
+                else {
+                    typ[q] = t;
+                    cnt += s_types[t].n_atoms;
+                }
+            }
+        }
+        if (__syncthreads_or(bad)) {
+            if (tid == 0) {
+                atomicOr(a.err, ERR_RESTYPE);
+                bulk_wait_all();
+            }
+            return;
+        }
+        int tile_end_atoms;
+        const int off0 = block_exclusive_sum_int<NT>(cnt, carry_atoms, s_int, &tile_end_atoms);
+
+        Aff M;
+        Aff FN[RPT], FCA[RPT], FC[RPT];
+        fa_chunk<RPT>(s_ang, rl0, r0, n, a.K, M, FN, FCA, FC);
+        if (kOrtho) aff_orthonormalize(M);
+        const Aff P = block_exclusive_scan<NT, kOrtho>(M, carry, s_scan, s_total);
+        carry = load_aff(s_total);
+
+        const int n_tile_atoms = tile_end_atoms - carry_atoms;
+        const Span so = make_span(coords + (size_t)carry_atoms * 3, n_tile_atoms * 12);
+        float* s_out = reinterpret_cast<float*>(s_out_base + so.mis());
+        int off = off0 - carry_atoms;  // tile-local atom index of the thread's first atom
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const int rl = rl0 + q;
+            if (rl < n) {
+                const FAType& T = s_types[typ[q]];
+                const Aff gN = aff_compose(P, FN[q]);
+                const Aff gCA = aff_compose(P, FCA[q]);
+                const Aff gC = aff_compose(P, FC[q]);
+                const float* ang = s_ang + 8 * rl;
+                float* o = s_out + 3 * off;
+                int k = 0;
+                for (; k < T.n_N; ++k) apply(gN, T.r[k][0], T.r[k][1], T.r[k][2], o[3 * k], o[3 * k + 1], o[3 * k + 2]);
+                for (; k < T.n_N + T.n_CA; ++k)
+                    apply(gCA, T.r[k][0], T.r[k][1], T.r[k][2], o[3 * k], o[3 * k + 1], o[3 * k + 2]);
+                Aff G = gCA;
+                for (int g = 0; g < T.n_groups; ++g) {
+                    const FAGroup& gr = T.g[g];
+                    if (gr.parent < 0) {
+                        G = gCA;
+                        if (gr.has_pre) aff_rot_x(G, gr.cb, gr.sb);
+                    }
+                    float s, c;
+                    if (gr.slot >= 0) sincosf(ang[gr.slot], &s, &c);
+                    else { s = gr.sa; c = gr.ca; }
+                    const BondC bc{gr.ct, gr.st, gr.d};
+                    aff_bond(G, c, s, bc);
+                    for (k = gr.first_atom; k < gr.end_atom; ++k)
+                        apply(G, T.r[k][0], T.r[k][1], T.r[k][2], o[3 * k], o[3 * k + 1], o[3 * k + 2]);
+                }
+                for (k = T.first_C; k < T.n_atoms; ++k)
+                    apply(gC, T.r[k][0], T.r[k][1], T.r[k][2], o[3 * k], o[3 * k + 1], o[3 * k + 2]);
+                off += T.n_atoms;
+            }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            span_store_bulk(so, s_out_base);
+            bulk_commit();
+        }
+        span_store_edges_f32(so, s_out_base);
+        carry_atoms = tile_end_atoms;
+    }
+    (void)s_misc;
+    (void)stage_atoms_per_res;
+    if (tid == 0) bulk_wait_all();
+}
+
+// Residue-local backward: positions of every atom of one residue, the
+// chi gradients (written to go[slot]) and the residue's sums needed by the
+// backbone gradients.  CA-relative moments keep the local sums accurate.
+struct ResSums {
+    float all[6];  // S, T^CA over all atoms of the residue
+    float nN[6];   // over N-owned atoms
+    float cC[6];   // over C-owned atoms
+};
+
+__device__ __forceinline__ void fa_residue_backward(const FAType& T, const float* ang, const Aff& gN, const Aff& gCA,
+                                                    const Aff& gC, const float* gk, float* go, ResSums& R) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) R.all[k] = R.nN[k] = R.cC[k] = 0.f;
+    const float cx = gCA.t0, cy = gCA.t1, cz = gCA.t2;
+    int k = 0;
+    for (; k < T.n_N; ++k) {
+        float x, y, z;
+        apply(gN, T.r[k][0], T.r[k][1], T.r[k][2], x, y, z);
+        cross_acc(R.nN, x - cx, y - cy, z - cz, gk[3 * k], gk[3 * k + 1], gk[3 * k + 2]);
+    }
+    for (; k < T.n_N + T.n_CA; ++k) {
+        float x, y, z;
+        apply(gCA, T.r[k][0], T.r[k][1], T.r[k][2], x, y, z);
+        cross_acc(R.all, x - cx, y - cy, z - cz, gk[3 * k], gk[3 * k + 1], gk[3 * k + 2]);
+    }
+    for (k = T.first_C; k < T.n_atoms; ++k) {
+        float x, y, z;
+        apply(gC, T.r[k][0], T.r[k][1], T.r[k][2], x, y, z);
+        cross_acc(R.cC, x - cx, y - cy, z - cz, gk[3 * k], gk[3 * k + 1], gk[3 * k + 2]);
+    }
+    // side-chain branches: forward to the branch tip, then walk back
+    int g0 = 0;
+    while (g0 < T.n_groups) {
+        int g1 = g0;
+        while (g1 + 1 < T.n_groups && T.g[g1 + 1].parent == g1) ++g1;
+        Aff G = gCA;
+        if (T.g[g0].has_pre) aff_rot_x(G, T.g[g0].cb, T.g[g0].sb);
+        for (int g = g0; g <= g1; ++g) {
+            const FAGroup& gr = T.g[g];
+            float s, c;
+            if (gr.slot >= 0) sincosf(ang[gr.slot], &s, &c);
+            else { s = gr.sa; c = gr.ca; }
+            aff_bond(G, c, s, BondC{gr.ct, gr.st, gr.d});
+        }
+        float br[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int g = g1; g >= g0; --g) {
+            const FAGroup& gr = T.g[g];
+            for (k = gr.first_atom; k < gr.end_atom; ++k) {
+                float x, y, z;
+                apply(G, T.r[k][0], T.r[k][1], T.r[k][2], x, y, z);
+                cross_acc(br, x - cx, y - cy, z - cz, gk[3 * k], gk[3 * k + 1], gk[3 * k + 2]);
+            }
+            if (gr.slot >= 0) go[gr.slot] = axis_moment(G.r00, G.r10, G.r20, G.t0 - cx, G.t1 - cy, G.t2 - cz, br);
+            if (g > g0) {
+                float s, c;
+                if (gr.slot >= 0) sincosf(ang[gr.slot], &s, &c);
+                else { s = gr.sa; c = gr.ca; }
+                aff_unbond(G, c, s, BondC{gr.ct, gr.st, gr.d});
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 6; ++q) R.all[q] += br[q];
+        g0 = g1 + 1;
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) R.all[q] += R.nN[q] + R.cC[q];
+}
+
+template <int NT, int RPT, bool kOrtho>
+__global__ void __launch_bounds__(NT) fa_backward_kernel(FAArgs a, int stage_atoms_per_res) {
+    constexpr int TILE = NT * RPT;
+    using S = FASmem<NT>;
+    using Lay = FALayout<NT, RPT>;
+    extern __shared__ __align__(16) char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
+    float* s_scan = reinterpret_cast<float*>(smem + S::kScan);
+    float* s_suf = reinterpret_cast<float*>(smem + S::kSuf);
+    int* s_int = reinterpret_cast<int*>(smem + S::kInt);
+    float* s_total = reinterpret_cast<float*>(smem + S::kTotal);
+    float* s_misc = reinterpret_cast<float*>(smem + S::kMisc);
+    const FAType* s_types = reinterpret_cast<const FAType*>(smem + S::kTable);
+    char* s_ang_base = smem + S::kTable + r16(a.n_types * int(sizeof(FAType)));
+    char* s_rt_base = s_ang_base + Lay::ang_bytes;
+    char* s_go_base = s_rt_base + Lay::rt_bytes;
+    char* s_g_base = s_go_base + Lay::go_bytes;
+
+    const int b = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int L = a.lengths[b];
+    if (L < 1 || L > a.Lmax) {
+        if (tid == 0) atomicOr(a.err, ERR_LENGTH);
+        return;
+    }
+    unsigned phase = 0;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_barrier_init();
+        const unsigned tb = unsigned(a.n_types * sizeof(FAType));
+        mbar_arrive_expect_tx(bar, tb);
+        bulk_g2s(smem + S::kTable, a.types, tb, bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+
+    const int n_tiles = (L + TILE - 1) / TILE;
+    const int rl0 = tid * RPT;
+    float* pref = a.ws_prefix + (size_t)b * a.max_tiles * 16;
+
+    // ---- phase A: prefix transform and atom offset at every tile start
+    if (n_tiles > 1) {
+        Aff carry = aff_identity();
+        int carry_atoms = 0;
+        for (int t = 0; t + 1 < n_tiles; ++t) {
+            const int r0 = t * TILE;
+            const int pre = r0 > 0 ? 1 : 0;
+            const Span sa = make_span(a.angles + ((size_t)b * a.Lmax + r0 - pre) * kFASlots, (TILE + pre) * 32);
+            const Span sr = make_span(a.restype + (size_t)b * a.Lmax + r0, TILE);
+            if (tid == 0) {
+                mbar_arrive_expect_tx(bar, unsigned(sa.mid + sr.mid));
+                span_load_bulk(sa, s_ang_base, bar);
+                span_load_bulk(sr, s_rt_base, bar);
+            }
+            span_load_edges_f32(sa, s_ang_base);
+            span_load_edges_u8(sr, s_rt_base);
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+            __syncthreads();
+            const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 8 * pre;
+            const unsigned char* s_rt = reinterpret_cast<const unsigned char*>(s_rt_base + sr.mis());
+            int cnt = 0;
+            bool bad = false;
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                const int t2 = s_rt[rl0 + q];
+                if (t2 >= a.n_types) bad = true;
+                else cnt += s_types[t2].n_atoms;
+            }
+            if (__syncthreads_or(bad)) {
+                if (tid == 0) atomicOr(a.err, ERR_RESTYPE);
+                return;
+            }
+            int tile_end;
+            block_exclusive_sum_int<NT>(cnt, carry_atoms, s_int, &tile_end);
+            Aff M;
+            Aff FN[RPT], FCA[RPT], FC[RPT];
+            fa_chunk<RPT>(s_ang, rl0, r0, TILE, a.K, M, FN, FCA, FC);
+            if (kOrtho) aff_orthonormalize(M);
+            block_exclusive_scan<NT, kOrtho>(M, carry, s_scan, s_total);
+            carry = load_aff(s_total);
+            carry_atoms = tile_end;
+            if (tid < 12) pref[(t + 1) * 16 + tid] = s_total[tid];
+            if (tid == 12) pref[(t + 1) * 16 + 12] = __int_as_float(tile_end);
+        }
+        __syncthreads();
+    }
+
+    // ---- phase B: tiles last to first
+    float carry6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float omega_next = 0.f;
+    const float* gcb = a.grad_coords + (size_t)b * a.atom_stride * 3;
+    for (int t = n_tiles - 1; t >= 0; --t) {
+        const int r0 = t * TILE;
+        const int n = min(TILE, L - r0);
+        const int pre = r0 > 0 ? 1 : 0;
+        const Aff carry = (t == 0) ? aff_identity() : load_aff(pref + t * 16);
+        const int carry_atoms = (t == 0) ? 0 : __float_as_int(pref[t * 16 + 12]);
+        const Span sa = make_span(a.angles + ((size_t)b * a.Lmax + r0 - pre) * kFASlots, (n + pre) * 32);
+        const Span sr = make_span(a.restype + (size_t)b * a.Lmax + r0, n);
+        if (tid == 0) {
+            bulk_wait_read_all();
+            mbar_arrive_expect_tx(bar, unsigned(sa.mid + sr.mid));
+            span_load_bulk(sa, s_ang_base, bar);
+            span_load_bulk(sr, s_rt_base, bar);
+        }
+        span_load_edges_f32(sa, s_ang_base);
+        span_load_edges_u8(sr, s_rt_base);
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        __syncthreads();
+        const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 8 * pre;
+        const unsigned char* s_rt = reinterpret_cast<const unsigned char*>(s_rt_base + sr.mis());
+
+        int cnt = 0;
+        bool bad = false;
+        int typ[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const int rl = rl0 + q;
+            typ[q] = 0;
+            if (rl < n) {
+                const int t2 = s_rt[rl];
+                if (t2 >= a.n_types) bad = true;
+                else {
+                    typ[q] = t2;
+                    cnt += s_types[t2].n_atoms;
+                }
+            }
+        }
+        if (__syncthreads_or(bad)) {
+            if (tid == 0) {
+                atomicOr(a.err, ERR_RESTYPE);
+                bulk_wait_all();
+            }
+            return;
+        }
+        int tile_end;
+        const int off0 = block_exclusive_sum_int<NT>(cnt, carry_atoms, s_int, &tile_end);
+        // stage grad_coords of the tile's atoms (second round on the barrier)
+        const Span sg = make_span(gcb + (size_t)carry_atoms * 3, (tile_end - carry_atoms) * 12);
+        if (tid == 0) {
+            mbar_arrive_expect_tx(bar, unsigned(sg.mid));
+            span_load_bulk(sg, s_g_base, bar);
+        }
+        span_load_edges_f32(sg, s_g_base);
+
+        Aff M;
+        Aff FN[RPT], FCA[RPT], FC[RPT];
+        fa_chunk<RPT>(s_ang, rl0, r0, n, a.K, M, FN, FCA, FC);
+        if (kOrtho) aff_orthonormalize(M);
+        const Aff P = block_exclusive_scan<NT, kOrtho>(M, carry, s_scan, s_total);  // contains __syncthreads
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        __syncthreads();
+        const float* s_g = reinterpret_cast<const float*>(s_g_base + sg.mis());
+        float* s_go = reinterpret_cast<float*>(s_go_base + 16);  // 16-aligned; stored with plain edges below
+
+        // residue pass: positions, chi gradients, residue sums
+        float axN[RPT][6], axCA[RPT][6], axC[RPT][6];  // e (3) and o - CA (3) of the three backbone nodes
+        float cax[RPT][3];
+        ResSums RS[RPT];
+        float thr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        int off = off0 - carry_atoms;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const int rl = rl0 + q;
+            if (rl < n) {
+                const FAType& T = s_types[typ[q]];
+                const Aff gN = aff_compose(P, FN[q]);
+                const Aff gCA = aff_compose(P, FCA[q]);
+                const Aff gC = aff_compose(P, FC[q]);
+                float* go = s_go + 8 * rl;
+                go[0] = go[1] = 0.f;
+#pragma unroll
+                for (int s = 3; s < 8; ++s) go[s] = 0.f;
+                fa_residue_backward(T, s_ang + 8 * rl, gN, gCA, gC, s_g + 3 * off, go, RS[q]);
+                cax[q][0] = gCA.t0; cax[q][1] = gCA.t1; cax[q][2] = gCA.t2;
+                axN[q][0] = gN.r00; axN[q][1] = gN.r10; axN[q][2] = gN.r20;
+                axN[q][3] = gN.t0 - gCA.t0; axN[q][4] = gN.t1 - gCA.t1; axN[q][5] = gN.t2 - gCA.t2;
+                axCA[q][0] = gCA.r00; axCA[q][1] = gCA.r10; axCA[q][2] = gCA.r20;
+                axCA[q][3] = 0.f; axCA[q][4] = 0.f; axCA[q][5] = 0.f;
+                axC[q][0] = gC.r00; axC[q][1] = gC.r10; axC[q][2] = gC.r20;
+                axC[q][3] = gC.t0 - gCA.t0; axC[q][4] = gC.t1 - gCA.t1; axC[q][5] = gC.t2 - gCA.t2;
+                // absolute moment of the residue: T = T^CA + CA x S
+                const float* s6 = RS[q].all;
+                thr[0] += s6[0]; thr[1] += s6[1]; thr[2] += s6[2];
+                thr[3] += s6[3] + fmaf(gCA.t1, s6[2], -gCA.t2 * s6[1]);
+                thr[4] += s6[4] + fmaf(gCA.t2, s6[0], -gCA.t0 * s6[2]);
+                thr[5] += s6[5] + fmaf(gCA.t0, s6[1], -gCA.t1 * s6[0]);
+                off += T.n_atoms;
+            }
+        }
+        float suf[6], tot6[6];
+        block_exclusive_suffix6<NT>(thr, carry6, s_suf, suf, tot6);
+
+        // backbone gradients, residues last to first; suf = sums (absolute) over later residues
+#pragma unroll
+        for (int q = RPT - 1; q >= 0; --q) {
+            const int rl = rl0 + q;
+            const int j = r0 + rl;
+            if (rl < n) {
+                float* go = s_go + 8 * rl;
+                const float cx = cax[q][0], cy = cax[q][1], cz = cax[q][2];
+                // later residues as CA-relative moments: T^CA = T - CA x S
+                float aft[6];
+                aft[0] = suf[0]; aft[1] = suf[1]; aft[2] = suf[2];
+                aft[3] = suf[3] - fmaf(cy, suf[2], -cz * suf[1]);
+                aft[4] = suf[4] - fmaf(cz, suf[0], -cx * suf[2]);
+                aft[5] = suf[5] - fmaf(cx, suf[1], -cy * suf[0]);
+                float s6[6];
+                // psi_j: C-owned atoms + later residues, axis through C
+#pragma unroll
+                for (int k = 0; k < 6; ++k) s6[k] = RS[q].cC[k] + aft[k];
+                go[1] = axis_moment(axC[q][0], axC[q][1], axC[q][2], axC[q][3], axC[q][4], axC[q][5], s6);
+                // phi_j: residue minus N-owned + later, axis through CA
+#pragma unroll
+                for (int k = 0; k < 6; ++k) s6[k] = RS[q].all[k] - RS[q].nN[k] + aft[k];
+                go[0] = axis_moment(axCA[q][0], axCA[q][1], axCA[q][2], 0.f, 0.f, 0.f, s6);
+                // omega_{j-1}: residue + later, axis through N
+                if (j > 0) {
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) s6[k] = RS[q].all[k] + aft[k];
+                    const float gw = axis_moment(axN[q][0], axN[q][1], axN[q][2], axN[q][3], axN[q][4], axN[q][5], s6);
+                    if (rl > 0) s_go[8 * (rl - 1) + 2] = gw;
+                    else s_misc[0] = gw;
+                }
+                // fold this residue into the suffix
+                const float* r6 = RS[q].all;
+                suf[0] += r6[0]; suf[1] += r6[1]; suf[2] += r6[2];
+                suf[3] += r6[3] + fmaf(cy, r6[2], -cz * r6[1]);
+                suf[4] += r6[4] + fmaf(cz, r6[0], -cx * r6[2]);
+                suf[5] += r6[5] + fmaf(cx, r6[1], -cy * r6[0]);
+            }
+        }
+        if (tid == 0) s_go[8 * (n - 1) + 2] = (r0 + n == L) ? 0.f : omega_next;
+        __syncthreads();
+        // store the tile's grad record [n][8] (32 B per residue: 16-B aligned when the row base is)
+        {
+            float* dst = a.grad_angles + ((size_t)b * a.Lmax + r0) * kFASlots;
+            if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                fence_proxy_async_smem();
+                __syncthreads();
+                if (tid == 0) {
+                    bulk_s2g(dst, s_go, unsigned(n * 32));
+                    bulk_commit();
+                }
+            } else {
+                for (int i = tid; i < n * 8; i += NT) dst[i] = s_go[i];
+            }
+        }
+        omega_next = s_misc[0];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) carry6[k] = tot6[k];
+        __syncthreads();
+    }
+    (void)stage_atoms_per_res;
+    if (tid == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
+int fa_rpt_for(int Lmax) { return Lmax > kFAThreads ? 2 : 1; }
+int fa_tile_for(int Lmax) { return kFAThreads * fa_rpt_for(Lmax); }
+
+static int max_atoms_per_res_host() { return kMaxAtomsPerRes; }
+
+template <int RPT>
+static size_t fa_fwd_smem(int n_types) {
+    using S = FASmem<kFAThreads>;
+    using Lay = FALayout<kFAThreads, RPT>;
+    return S::kTable + r16(n_types * int(sizeof(FAType))) + Lay::ang_bytes + Lay::rt_bytes +
+           r16(16 + 12 * max_atoms_per_res_host() * Lay::TILE);
+}
+template <int RPT>
+static size_t fa_bwd_smem(int n_types) {
+    using Lay = FALayout<kFAThreads, RPT>;
+    return fa_fwd_smem<RPT>(n_types) + Lay::go_bytes;
+}
+
+template <int RPT, bool O>
+static cudaError_t fa_fwd(const FAArgs& a, cudaStream_t st) {
+    auto k = fa_forward_kernel<kFAThreads, RPT, O>;
+    const size_t sm = fa_fwd_smem<RPT>(a.n_types);
+    static size_t configured = 0;  // set the smem opt-in once per instance (not inside graph capture)
+    if (configured < sm) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+        configured = sm;
+    }
+    k<<<a.B, kFAThreads, sm, st>>>(a, kMaxAtomsPerRes);
+    return cudaGetLastError();
+}
+template <int RPT, bool O>
+static cudaError_t fa_bwd(const FAArgs& a, cudaStream_t st) {
+    auto k = fa_backward_kernel<kFAThreads, RPT, O>;
+    const size_t sm = fa_bwd_smem<RPT>(a.n_types);
+    static size_t configured = 0;  // set the smem opt-in once per instance (not inside graph capture)
+    if (configured < sm) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+        configured = sm;
+    }
+    k<<<a.B, kFAThreads, sm, st>>>(a, kMaxAtomsPerRes);
+    return cudaGetLastError();
+}
+
+cudaError_t fa_forward_launch(const FAArgs& a, cudaStream_t st) {
+    const int r = fa_rpt_for(a.Lmax);
+    if (a.ortho) return r == 1 ? fa_fwd<1, true>(a, st) : fa_fwd<2, true>(a, st);
+    return r == 1 ? fa_fwd<1, false>(a, st) : fa_fwd<2, false>(a, st);
+}
+cudaError_t fa_backward_launch(const FAArgs& a, cudaStream_t st) {
+    const int r = fa_rpt_for(a.Lmax);
+    if (a.ortho) return r == 1 ? fa_bwd<1, true>(a, st) : fa_bwd<2, true>(a, st);
+    return r == 1 ? fa_bwd<1, false>(a, st) : fa_bwd<2, false>(a, st);
+}
+
+}  // namespace tpl

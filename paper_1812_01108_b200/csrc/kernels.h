@@ -1,0 +1,92 @@
+// kernels.h -- internal launch interface between capi.cu and the kernels.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tpl {
+
+// Bond-transform constants of one node: cos/sin of the fixed theta and d.
+struct BondC {
+    float ct, st, d;
+};
+
+constexpr int kBBThreads = 256;
+constexpr int kFAThreads = 256;
+constexpr int kMaxGroups = 8;
+constexpr int kMaxAtomsPerRes = 16;
+constexpr int kMaxTypes = 32;
+constexpr int kFASlots = 8;
+
+// Backbone constants (cos theta, sin theta, d) for k = 0 (C-N, omega),
+// 1 (N-CA, phi), 2 (CA-C, psi): PAPER.md P:161-167, rounded from fp64.
+struct BBConst {
+    BondC b[3];
+};
+
+struct BBArgs {
+    const float* angles;
+    const int* lengths;
+    int B, Lmax;
+    float* coords;
+    const float* grad_coords;
+    float* grad_angles;
+    unsigned* err;
+    float* ws_prefix;
+    int max_tiles;
+    bool ortho;
+    BBConst K;
+};
+
+int bb_rpt_for(int Lmax);
+int bb_tile_for(int Lmax);
+size_t bb_forward_smem(int rpt);
+size_t bb_backward_smem(int rpt);
+cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st);
+cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st);
+
+// ---- full atom -------------------------------------------------------------
+// Device residue-type table (fp32, uploaded once by tpl_tables_create).
+// One record per type, 16-byte aligned, copied whole into shared memory.
+struct FAGroup {
+    float ca, sa;      // cos/sin of the fixed alpha (slot < 0)
+    float ct, st, d;   // bond constants
+    float cb, sb;      // R' = R_x(pre_rx); (1, 0) when absent
+    int parent;        // -1 = CA frame, else g-1 (v1 restriction, see tpl.h)
+    int slot;          // 3..7 = chi1..chi5, -1 fixed
+    int has_pre;       // pre_rx != 0
+    int first_atom;    // index of the group's first atom in the type's atom list
+    int end_atom;      // one past the group's last atom
+};
+struct alignas(16) FAType {
+    int n_groups, n_atoms;
+    int n_N, n_CA;            // atoms owned by the N / CA frames (first n_N, then n_CA)
+    int first_C;              // first atom owned by the C frame; C-owned atoms run to n_atoms
+    int pad[3];
+    FAGroup g[kMaxGroups];
+    float r[kMaxAtomsPerRes][4];  // r° xyz (w unused)
+};
+
+struct FAArgs {
+    const FAType* types;
+    int n_types;
+    const float* angles;
+    const unsigned char* restype;
+    const int* lengths;
+    int B, Lmax, atom_stride;
+    float* coords;
+    const float* grad_coords;
+    float* grad_angles;
+    unsigned* err;
+    float* ws_prefix;  // per chain per tile: 12 floats prefix + 1 int atom offset (stride 16)
+    int max_tiles;
+    bool ortho;
+    BBConst K;
+};
+
+int fa_rpt_for(int Lmax);
+int fa_tile_for(int Lmax);
+cudaError_t fa_forward_launch(const FAArgs& a, cudaStream_t st);
+cudaError_t fa_backward_launch(const FAArgs& a, cudaStream_t st);
+
+}  // namespace tpl
