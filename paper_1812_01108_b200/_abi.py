@@ -12,7 +12,9 @@ import os
 import torch  # loads libcudart.so.12 before libtpl.so resolves it
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtpl.so")
+# TPL_LIB selects another build of the same ABI (e.g. build/libtpl_phases.so
+# for latency studies); default: the in-tree product library.
+LIB_PATH = os.environ.get("TPL_LIB") or os.path.join(_HERE, "libtpl.so")
 
 TPL_OK = 0
 STATUS = {0: "TPL_OK", 1: "TPL_ERR_NULL", 2: "TPL_ERR_SHAPE", 3: "TPL_ERR_ALIGN", 4: "TPL_ERR_TABLE",

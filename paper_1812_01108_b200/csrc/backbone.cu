@@ -10,13 +10,21 @@
 // (e_i = x-axis of frame M_i, the rotation axis of R_x(alpha_i)), hence
 //   dL/dalpha_i = e_i . (T_i - r_i x S_i),  S_i = sum_{j>i} g_j,  T_i = sum_{j>i} r_j x g_j,
 // one reverse suffix sum per chain: O(L) instead of the paper's O(L^2).
-// The forward frames are recomputed from the angles (no saved state).
+// The forward frames are recomputed from the angles (no saved state).  Each
+// thread works in the local frame of its chunk (positions relative to the
+// chunk start, gradients rotated into it): fewer flops than moving every
+// position and axis to the global frame, and smaller moments.
 //
-// Work decomposition: one CTA per chain; a tile of NT*RPT residues per CTA
-// iteration; each thread owns RPT consecutive residues (3*RPT transforms).
-// Longer chains loop over tiles carrying the prefix transform (forward) or,
-// in backward, run a prefix pre-pass (phase A, tile prefixes to the
-// workspace) then walk tiles last-to-first carrying the suffix sums.
+// Work decomposition: one CTA of NT threads per chain; a tile of NT*RPT
+// residues per CTA iteration; each thread owns RPT consecutive residues
+// (3*RPT transforms) and composes them sequentially, then one block-wide
+// affine scan combines the chunks.  Longer chains loop over tiles carrying
+// the prefix transform (forward) or, in backward, run a prefix pre-pass
+// (phase A, tile prefixes to the workspace) then walk tiles last-to-first
+// carrying the suffix sums.  Tiles move global<->shared with TMA bulk copies.
+#include <cstdlib>
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -25,26 +33,34 @@ namespace tpl {
 template <int NT>
 struct BBSmem {
     static constexpr int NW = NT / 32;
-    static constexpr int kBar = 0;                        // uint64 mbarrier (16 B slot)
-    static constexpr int kScratch = 16;                   // NW*12 floats
-    static constexpr int kTotal = kScratch + NW * 12 * 4;  // 12 floats (+ misc)
-    static constexpr int kMisc = kTotal + 48;             // 16 floats of misc
+    static constexpr int kBar = 0;                         // uint64 mbarrier (16 B slot)
+    static constexpr int kScratch = 16;                    // NW*12 floats (affine scan)
+    static constexpr int kSuf = kScratch + NW * 12 * 4;    // NW*6 floats (suffix scan)
+    static constexpr int kTotal = kSuf + NW * 6 * 4;       // 12 floats
+    static constexpr int kMisc = kTotal + 48;              // 16 floats of misc
     static constexpr int kData = ((kMisc + 64 + 15) / 16) * 16;
 };
 
 __host__ __device__ constexpr int round16(int x) { return (x + 15) & ~15; }
 
-// Transform i of the chain (atom i): angle index into the staged tile.
-// s_ang points at local residue 0 of the tile; s_ang[-1] (omega of the
-// previous residue) is staged whenever the tile does not start the chain.
+// The three transforms of residue j (local index rl in the staged tile):
+// k = 0: C_{j-1} -> N_j by omega_{j-1} (identity for j = 0, reading Q1),
+// k = 1: N_j -> CA_j by phi_j, k = 2: CA_j -> C_j by psi_j.
+// kSlow = false: branch-free hot path, |angle| folded into *maxabs; the caller
+// redoes the tile with kSlow = true if any |angle| > kSinCosFastMax.
+template <bool kSlow>
+__device__ __forceinline__ void bb_residue_trig(const float* s_ang, int rl, int j, float (&c)[3], float (&s)[3],
+                                                float* maxabs) {
+    const float x[3] = {j > 0 ? s_ang[3 * rl - 1] : 0.f, s_ang[3 * rl + 0], s_ang[3 * rl + 1]};
+    if (kSlow) tpl_sincos_n<3>(x, s, c);
+    else tpl_sincos_hot<3>(x, s, c, maxabs);
+}
 
-template <int NT, int RPT, bool kOrtho>
+template <int NT, int RPT, int kNS>
 __global__ void __launch_bounds__(NT) bb_forward_kernel(const float* __restrict__ angles,
                                                         const int* __restrict__ lengths, int Lmax,
-                                                        float* __restrict__ coords, unsigned* __restrict__ err,
-                                                        BBConst K) {
+                                                        float* __restrict__ coords, unsigned* __restrict__ err) {
     constexpr int TILE = NT * RPT;
-    constexpr int APT = 3 * RPT;
     using S = BBSmem<NT>;
     extern __shared__ __align__(16) char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
@@ -55,19 +71,24 @@ __global__ void __launch_bounds__(NT) bb_forward_kernel(const float* __restrict_
 
     const int b = blockIdx.x;
     const int tid = threadIdx.x;
-    const int L = lengths[b];
-    if (L < 1 || L > Lmax) {
-        if (tid == 0) atomicOr(err, ERR_LENGTH);
-        return;
-    }
+    TPL_STAMP(0);
     if (tid == 0) {
         mbar_init(bar, 1);
         fence_barrier_init();
     }
+    pdl_wait();
+    pdl_trigger();
+    const int L = lengths[b];
+    TPL_STAMP(1);
     __syncthreads();
+    if (L < 1 || L > Lmax) {
+        if (tid == 0) atomicOr(err, ERR_LENGTH);
+        return;
+    }
 
     Aff carry = aff_identity();
     unsigned phase = 0;
+    const int rl0 = tid * RPT;
     for (int r0 = 0; r0 < L; r0 += TILE) {
         const int n = min(TILE, L - r0);
         const int pre = r0 > 0 ? 1 : 0;
@@ -79,76 +100,89 @@ __global__ void __launch_bounds__(NT) bb_forward_kernel(const float* __restrict_
             span_load_bulk(sa, s_ang_base, bar);
         }
         span_load_edges_f32(sa, s_ang_base);
+        const Span so = make_span(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3, n * 36);
+        float* s_out = reinterpret_cast<float*>(s_out_base + so.mis());
+        TPL_STAMP(2);
         mbar_wait(bar, phase);
         phase ^= 1u;
         __syncthreads();
+        TPL_STAMP(3);
         const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 3 * pre;
 
-        // ---- per-thread chunk: sequential compose from identity
-        Aff M = aff_identity();
-        float px[APT], py[APT], pz[APT];
-        const int rl0 = tid * RPT;
+        // ---- pass 1: the thread's chunk composed from the identity; local
+        //      atom positions stay in registers (RPT is small and odd, so the
+        //      strided shared-memory accesses below are bank-conflict free)
+        Aff M;
+        const int nq = max(0, min(RPT, n - rl0));
+        float px[3 * RPT], py[3 * RPT], pz[3 * RPT];
+        float maxabs = 0.f;
+        auto pass1 = [&](auto slow) {
+            constexpr bool kSlow = decltype(slow)::value;
+            M = aff_identity();
 #pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-            const int rl = rl0 + q;
-            const int j = r0 + rl;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                if (rl < n && (j | k) != 0) {
-                    const float a = (k == 0) ? s_ang[3 * rl - 1] : s_ang[3 * rl + k - 1];
-                    float s, c;
-                    sincosf(a, &s, &c);
-                    aff_bond(M, c, s, K.b[k]);
+            for (int q = 0; q < RPT; ++q) {
+                if (q < nq) {
+                    const int rl = rl0 + q;
+                    float c[3], s[3];
+                    bb_residue_trig<kSlow>(s_ang, rl, r0 + rl, c, s, &maxabs);
+                    if (r0 + rl > 0) aff_bond_bb<0>(M, c[0], s[0]);
+                    px[3 * q] = M.t0; py[3 * q] = M.t1; pz[3 * q] = M.t2;
+                    aff_bond_bb<1>(M, c[1], s[1]);
+                    px[3 * q + 1] = M.t0; py[3 * q + 1] = M.t1; pz[3 * q + 1] = M.t2;
+                    aff_bond_bb<2>(M, c[2], s[2]);
+                    px[3 * q + 2] = M.t0; py[3 * q + 2] = M.t1; pz[3 * q + 2] = M.t2;
                 }
-                px[3 * q + k] = M.t0;
-                py[3 * q + k] = M.t1;
-                pz[3 * q + k] = M.t2;
             }
-        }
-        if (kOrtho) aff_orthonormalize(M);
-        const Aff P = block_exclusive_scan<NT, kOrtho>(M, carry, scratch, s_total);
+        };
+        pass1(std::false_type{});
+        if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
+        if (kNS >= 1) aff_orthonormalize(M);
+        TPL_STAMP(4);
+        const Aff P = block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
         carry = load_aff(s_total);
+        TPL_STAMP(5);
 
-        // ---- global positions into the output staging buffer, then bulk store
-        const Span so = make_span(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3, n * 36);
-        float* s_out = reinterpret_cast<float*>(s_out_base + so.mis());
+        // ---- pass 2: chunk prefix applied, positions to the output staging buffer
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
-            const int rl = rl0 + q;
-            if (rl < n) {
+            if (q < nq) {
+                float* o = s_out + 9 * (rl0 + q);
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
-                    float x, y, z;
-                    apply(P, px[3 * q + k], py[3 * q + k], pz[3 * q + k], x, y, z);
-                    s_out[9 * rl + 3 * k + 0] = x;
-                    s_out[9 * rl + 3 * k + 1] = y;
-                    s_out[9 * rl + 3 * k + 2] = z;
+                    const int a = 3 * q + k;
+                    apply(P, px[a], py[a], pz[a], o[3 * k], o[3 * k + 1], o[3 * k + 2]);
                 }
             }
         }
+        TPL_STAMP(6);
         fence_proxy_async_smem();
         __syncthreads();
+        TPL_STAMP(7);
         if (tid == 0) {
             span_store_bulk(so, s_out_base);
             bulk_commit();
         }
         span_store_edges_f32(so, s_out_base);
     }
-    if (tid == 0) bulk_wait_all();
+    TPL_STAMP(8);
+    // Only the shared-memory source must outlive the CTA; grid completion (and the
+    // dependent's griddepcontrol.wait) covers visibility of the global writes.
+    if (tid == 0) bulk_wait_read_all();
+    TPL_STAMP(9);
 }
 
-template <int NT, int RPT, bool kOrtho>
+template <int NT, int RPT, int kNS>
 __global__ void __launch_bounds__(NT) bb_backward_kernel(const float* __restrict__ angles,
                                                          const int* __restrict__ lengths, int Lmax,
                                                          const float* __restrict__ grad_coords,
                                                          float* __restrict__ grad_angles, unsigned* __restrict__ err,
-                                                         float* __restrict__ ws_prefix, int max_tiles, BBConst K) {
+                                                         float* __restrict__ ws_prefix, int max_tiles) {
     constexpr int TILE = NT * RPT;
-    constexpr int APT = 3 * RPT;
     using S = BBSmem<NT>;
     extern __shared__ __align__(16) char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
     float* scratch = reinterpret_cast<float*>(smem + S::kScratch);
+    float* s_suf = reinterpret_cast<float*>(smem + S::kSuf);
     float* s_total = reinterpret_cast<float*>(smem + S::kTotal);
     float* s_misc = reinterpret_cast<float*>(smem + S::kMisc);
     char* s_ang_base = smem + S::kData;
@@ -157,16 +191,18 @@ __global__ void __launch_bounds__(NT) bb_backward_kernel(const float* __restrict
 
     const int b = blockIdx.x;
     const int tid = threadIdx.x;
-    const int L = lengths[b];
-    if (L < 1 || L > Lmax) {
-        if (tid == 0) atomicOr(err, ERR_LENGTH);
-        return;
-    }
     if (tid == 0) {
         mbar_init(bar, 1);
         fence_barrier_init();
     }
+    pdl_wait();
+    pdl_trigger();
+    const int L = lengths[b];
     __syncthreads();
+    if (L < 1 || L > Lmax) {
+        if (tid == 0) atomicOr(err, ERR_LENGTH);
+        return;
+    }
     const int n_tiles = (L + TILE - 1) / TILE;
     unsigned phase = 0;
     const int rl0 = tid * RPT;
@@ -188,23 +224,25 @@ __global__ void __launch_bounds__(NT) bb_backward_kernel(const float* __restrict
             phase ^= 1u;
             __syncthreads();
             const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 3 * pre;
-            Aff M = aff_identity();
-#pragma unroll
-            for (int q = 0; q < RPT; ++q) {
-                const int rl = rl0 + q;
-                const int j = r0 + rl;
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    if ((j | k) != 0) {
-                        const float a = (k == 0) ? s_ang[3 * rl - 1] : s_ang[3 * rl + k - 1];
-                        float s, c;
-                        sincosf(a, &s, &c);
-                        aff_bond(M, c, s, K.b[k]);
-                    }
+            Aff M;
+            float maxabs = 0.f;
+            auto chunk = [&](auto slow) {
+                constexpr bool kSlow = decltype(slow)::value;
+                M = aff_identity();
+#pragma unroll 2
+                for (int q = 0; q < RPT; ++q) {
+                    const int rl = rl0 + q;
+                    float c[3], s[3];
+                    bb_residue_trig<kSlow>(s_ang, rl, r0 + rl, c, s, &maxabs);
+                    if (r0 + rl > 0) aff_bond_bb<0>(M, c[0], s[0]);
+                    aff_bond_bb<1>(M, c[1], s[1]);
+                    aff_bond_bb<2>(M, c[2], s[2]);
                 }
-            }
-            if (kOrtho) aff_orthonormalize(M);
-            block_exclusive_scan<NT, kOrtho>(M, carry, scratch, s_total);
+            };
+            chunk(std::false_type{});
+            if (__syncthreads_or(maxabs > kSinCosFastMax)) chunk(std::true_type{});
+            if (kNS >= 1) aff_orthonormalize(M);
+            block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
             carry = load_aff(s_total);
             if (tid < 12) pref[(t + 1) * 12 + tid] = s_total[tid];
         }
@@ -233,86 +271,111 @@ __global__ void __launch_bounds__(NT) bb_backward_kernel(const float* __restrict
         phase ^= 1u;
         __syncthreads();
         const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 3 * pre;
-        const float* s_g = reinterpret_cast<const float*>(s_g_base + sg.mis());
+        float* s_g = reinterpret_cast<float*>(s_g_base + sg.mis());
+        const int nq = max(0, min(RPT, n - rl0));
 
-        // local chunk: positions and rotation axes (x-axis of each frame)
-        Aff M = aff_identity();
+        // pass 1: local chunk; positions and rotation axes stay in registers
+        constexpr int APT = 3 * RPT;
+        Aff M;
+        float maxabs = 0.f;
         float px[APT], py[APT], pz[APT], ex[APT], ey[APT], ez[APT];
+        auto pass1 = [&](auto slow) {
+            constexpr bool kSlow = decltype(slow)::value;
+            M = aff_identity();
 #pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-            const int rl = rl0 + q;
-            const int j = r0 + rl;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                if (rl < n && (j | k) != 0) {
-                    const float a = (k == 0) ? s_ang[3 * rl - 1] : s_ang[3 * rl + k - 1];
-                    float s, c;
-                    sincosf(a, &s, &c);
-                    aff_bond(M, c, s, K.b[k]);
+            for (int q = 0; q < RPT; ++q) {
+                if (q < nq) {
+                    const int rl = rl0 + q;
+                    float c[3], s[3];
+                    bb_residue_trig<kSlow>(s_ang, rl, r0 + rl, c, s, &maxabs);
+                    auto save = [&](int a) {
+                        px[a] = M.t0; py[a] = M.t1; pz[a] = M.t2;
+                        ex[a] = M.r00; ey[a] = M.r10; ez[a] = M.r20;
+                    };
+                    if (r0 + rl > 0) aff_bond_bb<0>(M, c[0], s[0]);
+                    save(3 * q);
+                    aff_bond_bb<1>(M, c[1], s[1]);
+                    save(3 * q + 1);
+                    aff_bond_bb<2>(M, c[2], s[2]);
+                    save(3 * q + 2);
                 }
-                px[3 * q + k] = M.t0;
-                py[3 * q + k] = M.t1;
-                pz[3 * q + k] = M.t2;
-                ex[3 * q + k] = M.r00;
-                ey[3 * q + k] = M.r10;
-                ez[3 * q + k] = M.r20;
             }
-        }
-        if (kOrtho) aff_orthonormalize(M);
-        const Aff P = block_exclusive_scan<NT, kOrtho>(M, carry, scratch, s_total);
+        };
+        pass1(std::false_type{});
+        if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
+        if (kNS >= 1) aff_orthonormalize(M);
+        const Aff P = block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
 
-        // global r, e; per-thread sums S = sum g, T = sum r x g
-        float sum6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        // pass 2: gradients rotated into the chunk frame (g_loc = R^T g)
+        float sl[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        float gx[APT], gy[APT], gz[APT];
 #pragma unroll
         for (int a = 0; a < APT; ++a) {
-            const int rl = rl0 + a / 3;
-            float x, y, z;
-            apply(P, px[a], py[a], pz[a], x, y, z);
-            px[a] = x; py[a] = y; pz[a] = z;
-            const float e0 = fmaf(P.r00, ex[a], fmaf(P.r01, ey[a], P.r02 * ez[a]));
-            const float e1 = fmaf(P.r10, ex[a], fmaf(P.r11, ey[a], P.r12 * ez[a]));
-            const float e2 = fmaf(P.r20, ex[a], fmaf(P.r21, ey[a], P.r22 * ez[a]));
-            ex[a] = e0; ey[a] = e1; ez[a] = e2;
-            if (rl < n) {
-                const float g0 = s_g[9 * rl + 3 * (a % 3) + 0];
-                const float g1 = s_g[9 * rl + 3 * (a % 3) + 1];
-                const float g2 = s_g[9 * rl + 3 * (a % 3) + 2];
-                sum6[0] += g0; sum6[1] += g1; sum6[2] += g2;
-                sum6[3] += fmaf(y, g2, -z * g1);
-                sum6[4] += fmaf(z, g0, -x * g2);
-                sum6[5] += fmaf(x, g1, -y * g0);
+            gx[a] = gy[a] = gz[a] = 0.f;
+            if (a / 3 < nq) {
+                const float* g = s_g + 9 * rl0 + 3 * a;
+                const float g0 = g[0], g1 = g[1], g2 = g[2];
+                gx[a] = fmaf(P.r00, g0, fmaf(P.r10, g1, P.r20 * g2));
+                gy[a] = fmaf(P.r01, g0, fmaf(P.r11, g1, P.r21 * g2));
+                gz[a] = fmaf(P.r02, g0, fmaf(P.r12, g1, P.r22 * g2));
+                sl[0] += gx[a]; sl[1] += gy[a]; sl[2] += gz[a];
+                sl[3] += fmaf(py[a], gz[a], -pz[a] * gy[a]);
+                sl[4] += fmaf(pz[a], gx[a], -px[a] * gz[a]);
+                sl[5] += fmaf(px[a], gy[a], -py[a] * gx[a]);
             }
         }
+        // thread totals in the global frame: S = R S_l, T = R T_l + t x S
+        float sum6[6];
+        sum6[0] = fmaf(P.r00, sl[0], fmaf(P.r01, sl[1], P.r02 * sl[2]));
+        sum6[1] = fmaf(P.r10, sl[0], fmaf(P.r11, sl[1], P.r12 * sl[2]));
+        sum6[2] = fmaf(P.r20, sl[0], fmaf(P.r21, sl[1], P.r22 * sl[2]));
+        sum6[3] = fmaf(P.r00, sl[3], fmaf(P.r01, sl[4], P.r02 * sl[5])) + fmaf(P.t1, sum6[2], -P.t2 * sum6[1]);
+        sum6[4] = fmaf(P.r10, sl[3], fmaf(P.r11, sl[4], P.r12 * sl[5])) + fmaf(P.t2, sum6[0], -P.t0 * sum6[2]);
+        sum6[5] = fmaf(P.r20, sl[3], fmaf(P.r21, sl[4], P.r22 * sl[5])) + fmaf(P.t0, sum6[1], -P.t1 * sum6[0]);
         float suf[6], tot6[6];
-        block_exclusive_suffix6<NT>(sum6, carry6, scratch, suf, tot6);
+        block_exclusive_suffix6<NT>(sum6, carry6, s_suf, suf, tot6);
+        // later atoms into the chunk frame: S_l = R^T S, T_l = R^T (T - t x S)
+        float su[6];
+        {
+            const float w0 = suf[3] - fmaf(P.t1, suf[2], -P.t2 * suf[1]);
+            const float w1 = suf[4] - fmaf(P.t2, suf[0], -P.t0 * suf[2]);
+            const float w2 = suf[5] - fmaf(P.t0, suf[1], -P.t1 * suf[0]);
+            su[0] = fmaf(P.r00, suf[0], fmaf(P.r10, suf[1], P.r20 * suf[2]));
+            su[1] = fmaf(P.r01, suf[0], fmaf(P.r11, suf[1], P.r21 * suf[2]));
+            su[2] = fmaf(P.r02, suf[0], fmaf(P.r12, suf[1], P.r22 * suf[2]));
+            su[3] = fmaf(P.r00, w0, fmaf(P.r10, w1, P.r20 * w2));
+            su[4] = fmaf(P.r01, w0, fmaf(P.r11, w1, P.r21 * w2));
+            su[5] = fmaf(P.r02, w0, fmaf(P.r12, w1, P.r22 * w2));
+        }
 
-        // walk atoms last to first: grad alpha_i = e_i . (T - r_i x S)
+        // pass 3: atoms last to first, grad alpha_i = e_i . (T - p_i x S)   (chunk frame)
         const Span so = make_span(grad_angles + ((size_t)b * Lmax + r0) * 3, n * 12);
         float* s_go = reinterpret_cast<float*>(s_go_base + so.mis());
 #pragma unroll
-        for (int a = APT - 1; a >= 0; --a) {
-            const int q = a / 3, k = a % 3;
-            const int rl = rl0 + q;
-            const int j = r0 + rl;
-            if (rl < n) {
-                const float x = px[a], y = py[a], z = pz[a];
-                const float c0 = suf[3] - fmaf(y, suf[2], -z * suf[1]);
-                const float c1 = suf[4] - fmaf(z, suf[0], -x * suf[2]);
-                const float c2 = suf[5] - fmaf(x, suf[1], -y * suf[0]);
-                const float ga = fmaf(ex[a], c0, fmaf(ey[a], c1, ez[a] * c2));
-                if (k == 1) s_go[3 * rl + 0] = ga;        // phi_j
-                else if (k == 2) s_go[3 * rl + 1] = ga;   // psi_j
-                else if (j > 0) {                          // omega_{j-1}
-                    if (rl > 0) s_go[3 * (rl - 1) + 2] = ga;
-                    else s_misc[0] = ga;                   // belongs to the previous tile
+        for (int q = RPT - 1; q >= 0; --q) {
+            if (q < nq) {
+                const int rl = rl0 + q;
+                const int j = r0 + rl;
+                float ga[3];
+#pragma unroll
+                for (int k = 2; k >= 0; --k) {
+                    const int a = 3 * q + k;
+                    const float x = px[a], y = py[a], z = pz[a];
+                    const float c0 = su[3] - fmaf(y, su[2], -z * su[1]);
+                    const float c1 = su[4] - fmaf(z, su[0], -x * su[2]);
+                    const float c2 = su[5] - fmaf(x, su[1], -y * su[0]);
+                    ga[k] = fmaf(ex[a], c0, fmaf(ey[a], c1, ez[a] * c2));
+                    su[0] += gx[a]; su[1] += gy[a]; su[2] += gz[a];
+                    su[3] += fmaf(y, gz[a], -z * gy[a]);
+                    su[4] += fmaf(z, gx[a], -x * gz[a]);
+                    su[5] += fmaf(x, gy[a], -y * gx[a]);
                 }
-                const float g0 = s_g[9 * rl + 3 * k + 0];
-                const float g1 = s_g[9 * rl + 3 * k + 1];
-                const float g2 = s_g[9 * rl + 3 * k + 2];
-                suf[0] += g0; suf[1] += g1; suf[2] += g2;
-                suf[3] += fmaf(y, g2, -z * g1);
-                suf[4] += fmaf(z, g0, -x * g2);
-                suf[5] += fmaf(x, g1, -y * g0);
+                s_go[3 * rl + 0] = ga[1];  // phi_j
+                s_go[3 * rl + 1] = ga[2];  // psi_j
+                if (j > 0) {               // omega_{j-1}
+                    if (rl > 0) s_go[3 * (rl - 1) + 2] = ga[0];
+                    else s_misc[0] = ga[0];  // belongs to the previous tile
+                }
             }
         }
         // omega of the tile's last residue: from the later tile, or a structural 0
@@ -329,90 +392,119 @@ __global__ void __launch_bounds__(NT) bb_backward_kernel(const float* __restrict
         for (int k = 0; k < 6; ++k) carry6[k] = tot6[k];
         __syncthreads();
     }
-    if (tid == 0) bulk_wait_all();
+    // Only the shared-memory source must outlive the CTA; grid completion (and the
+    // dependent's griddepcontrol.wait) covers visibility of the global writes.
+    if (tid == 0) bulk_wait_read_all();
 }
 
 // ---------------------------------------------------------------------------
 // Host-side launch helpers (called from capi.cu).
 
-int bb_rpt_for(int Lmax) {
-    int r = (Lmax + kBBThreads - 1) / kBBThreads;
-    return r < 1 ? 1 : (r > 4 ? 4 : r);
+// Launch shape: NT threads per chain, RPT residues per thread (tile NT*RPT).
+// Default NT = 128; TPL_BB_NT=64|256 selects the other variants (tuning).
+// Chains longer than the largest tile loop over tiles.
+struct BBShape {
+    int nt, rpt;
+};
+static int bb_nt_env() {  // TPL_BB_NT=128|256 forces the block size (tuning); 0 = default
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("TPL_BB_NT");
+        const int x = e ? std::atoi(e) : 0;
+        v = (x == 128 || x == 256) ? x : 0;
+    }
+    return v;
 }
-int bb_tile_for(int Lmax) { return kBBThreads * bb_rpt_for(Lmax); }
+// Odd residues-per-thread only: the per-thread strides 3*RPT (angles) and
+// 9*RPT (coordinates) in shared memory are then bank-conflict free.
+// Forward: 128 threads, RPT in {1,3,5,7} (tile <= 896).  Backward keeps 6
+// floats per atom in registers: 256 threads, RPT in {1,3} (tile <= 768).
+static BBShape bb_shape(bool fwd, int Lmax) {
+    int nt = bb_nt_env();
+    if (!nt) nt = (fwd || Lmax > 128) ? (fwd ? 128 : 256) : 128;
+    static const int f128[4] = {1, 3, 5, 7}, f256[3] = {1, 3, 5}, b128[2] = {1, 3}, b256[2] = {1, 3};
+    const int* opts = fwd ? (nt == 256 ? f256 : f128) : (nt == 256 ? b256 : b128);
+    const int n = fwd ? (nt == 256 ? 3 : 4) : 2;
+    for (int i = 0; i < n; ++i)
+        if (nt * opts[i] >= Lmax) return {nt, opts[i]};
+    return {nt, opts[n - 1]};
+}
+int bb_rpt_for(int Lmax) { return bb_shape(false, Lmax).rpt; }
+int bb_tile_for(int Lmax) {  // backward tile: sizes the workspace's per-tile prefixes
+    const BBShape s = bb_shape(false, Lmax);
+    return s.nt * s.rpt;
+}
 
-size_t bb_forward_smem(int rpt) {
-    const int tile = kBBThreads * rpt;
-    return BBSmem<kBBThreads>::kData + round16(16 + 12 * (tile + 1)) + round16(16 + 36 * tile);
+template <int NT>
+static size_t fwd_smem(int rpt) {
+    const int tile = NT * rpt;
+    return BBSmem<NT>::kData + round16(16 + 12 * (tile + 1)) + round16(16 + 36 * tile);
 }
-size_t bb_backward_smem(int rpt) {
-    const int tile = kBBThreads * rpt;
-    return BBSmem<kBBThreads>::kData + round16(16 + 12 * (tile + 1)) + round16(16 + 36 * tile) +
-           round16(16 + 12 * tile);
+template <int NT>
+static size_t bwd_smem(int rpt) {
+    const int tile = NT * rpt;
+    return BBSmem<NT>::kData + round16(16 + 12 * (tile + 1)) + round16(16 + 36 * tile) + round16(16 + 12 * tile);
 }
 
-template <int RPT, bool O>
+template <int NT, int RPT, int NS>
 static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
-    auto k = bb_forward_kernel<kBBThreads, RPT, O>;
-    const size_t sm = bb_forward_smem(RPT);
+    auto k = bb_forward_kernel<NT, RPT, NS>;
+    const size_t sm = fwd_smem<NT>(RPT);
     static size_t configured = 0;  // set the smem opt-in once per instance (not inside graph capture)
     if (configured < sm) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
         configured = sm;
     }
-    k<<<a.B, kBBThreads, sm, st>>>(a.angles, a.lengths, a.Lmax, a.coords, a.err, a.K);
-    return cudaGetLastError();
+    return launch_pdl(k, a.B, NT, sm, st, a.angles, a.lengths, a.Lmax, a.coords, a.err);
 }
-template <int RPT, bool O>
+template <int NT, int RPT, int NS>
 static cudaError_t launch_bwd(const BBArgs& a, cudaStream_t st) {
-    auto k = bb_backward_kernel<kBBThreads, RPT, O>;
-    const size_t sm = bb_backward_smem(RPT);
-    static size_t configured = 0;  // set the smem opt-in once per instance (not inside graph capture)
+    auto k = bb_backward_kernel<NT, RPT, NS>;
+    const size_t sm = bwd_smem<NT>(RPT);
+    static size_t configured = 0;
     if (configured < sm) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
         configured = sm;
     }
-    k<<<a.B, kBBThreads, sm, st>>>(a.angles, a.lengths, a.Lmax, a.grad_coords, a.grad_angles, a.err, a.ws_prefix,
-                                   a.max_tiles, a.K);
-    return cudaGetLastError();
+    return launch_pdl(k, a.B, NT, sm, st, a.angles, a.lengths, a.Lmax, a.grad_coords, a.grad_angles, a.err,
+                      a.ws_prefix, a.max_tiles);
 }
+
+template <bool kFwd, int NS>
+static cudaError_t dispatch(const BBArgs& a, cudaStream_t st) {
+    const BBShape s = bb_shape(kFwd, a.Lmax);
+    if (kFwd) {
+#define TPL_BB_FWD(NT_, R_) \
+    if (s.nt == NT_ && s.rpt == R_) return launch_fwd<NT_, R_, NS>(a, st);
+        TPL_BB_FWD(128, 1) TPL_BB_FWD(128, 3) TPL_BB_FWD(128, 5) TPL_BB_FWD(128, 7)
+        TPL_BB_FWD(256, 1) TPL_BB_FWD(256, 3) TPL_BB_FWD(256, 5)
+#undef TPL_BB_FWD
+    } else {
+#define TPL_BB_BWD(NT_, R_) \
+    if (s.nt == NT_ && s.rpt == R_) return launch_bwd<NT_, R_, NS>(a, st);
+        TPL_BB_BWD(128, 1) TPL_BB_BWD(128, 3) TPL_BB_BWD(256, 1) TPL_BB_BWD(256, 3)
+#undef TPL_BB_BWD
+    }
+    return cudaErrorInvalidConfiguration;
+}
+
+#ifdef TPL_PROFILE_PHASES
+extern "C" __attribute__((visibility("default"))) int tpl_debug_stamps(unsigned long long* host, int n) {
+    return int(cudaMemcpyFromSymbol(host, g_tpl_stamps, sizeof(unsigned long long) * n));
+}
+extern "C" __attribute__((visibility("default"))) int tpl_debug_stamps_clear(void) {
+    static unsigned long long zeros[1 << 16];
+    return int(cudaMemcpyToSymbol(g_tpl_stamps, zeros, sizeof(zeros)));
+}
+#endif
 
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st) {
-    const int r = bb_rpt_for(a.Lmax);
-    if (a.ortho) {
-        switch (r) {
-            case 1: return launch_fwd<1, true>(a, st);
-            case 2: return launch_fwd<2, true>(a, st);
-            case 3: return launch_fwd<3, true>(a, st);
-            default: return launch_fwd<4, true>(a, st);
-        }
-    }
-    switch (r) {
-        case 1: return launch_fwd<1, false>(a, st);
-        case 2: return launch_fwd<2, false>(a, st);
-        case 3: return launch_fwd<3, false>(a, st);
-        default: return launch_fwd<4, false>(a, st);
-    }
+    return a.ns == 0 ? dispatch<true, 0>(a, st) : dispatch<true, 1>(a, st);
 }
-
 cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st) {
-    const int r = bb_rpt_for(a.Lmax);
-    if (a.ortho) {
-        switch (r) {
-            case 1: return launch_bwd<1, true>(a, st);
-            case 2: return launch_bwd<2, true>(a, st);
-            case 3: return launch_bwd<3, true>(a, st);
-            default: return launch_bwd<4, true>(a, st);
-        }
-    }
-    switch (r) {
-        case 1: return launch_bwd<1, false>(a, st);
-        case 2: return launch_bwd<2, false>(a, st);
-        case 3: return launch_bwd<3, false>(a, st);
-        default: return launch_bwd<4, false>(a, st);
-    }
+    return a.ns == 0 ? dispatch<false, 0>(a, st) : dispatch<false, 1>(a, st);
 }
 
 }  // namespace tpl

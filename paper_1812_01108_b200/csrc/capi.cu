@@ -13,6 +13,16 @@
 
 using namespace tpl;
 
+// Programmatic dependent launch of the kernels (TPL_PDL=0 turns it off).
+bool tpl::pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("TPL_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -34,13 +44,16 @@ tpl_status cuda_fail(cudaError_t e, const char* where) {
 
 bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
 
-bool ortho_enabled() {
+// Newton-Schulz re-orthonormalisation policy of the affine scan (TPL_ORTHO):
+// 0 = off, 1 = chunk aggregates, scan results and carries (default),
+// 2 = additionally after every combine inside the scan.
+int ns_policy() {
     static int v = -1;
     if (v < 0) {
         const char* e = std::getenv("TPL_ORTHO");
-        v = (e && e[0] == '0') ? 0 : 1;
+        v = (e && (e[0] == '0' || e[0] == '2')) ? e[0] - '0' : 1;
     }
-    return v == 1;
+    return v;
 }
 
 // the backbone transform table.  theta and d are the
@@ -58,6 +71,19 @@ BBConst backbone_constants() {
     return K;
 }
 
+// The kernels use kBBct/kBBst/kBBd as compile-time literals; check once per
+// process that they are the fp64-evaluated constants rounded to fp32.
+bool constants_consistent() {
+    static int ok = -1;
+    if (ok < 0) {
+        const BBConst K = backbone_constants();
+        ok = 1;
+        for (int k = 0; k < 3; ++k)
+            if (K.b[k].ct != kBBct[k] || K.b[k].st != kBBst[k] || K.b[k].d != kBBd[k]) ok = 0;
+    }
+    return ok == 1;
+}
+
 constexpr size_t kWsHeader = 256;  // error word + reserved
 
 int tile_for(int model, int Lmax) { return model == TPL_MODEL_FULLATOM ? fa_tile_for(Lmax) : bb_tile_for(Lmax); }
@@ -67,6 +93,7 @@ int max_tiles_for(int model, int Lmax) {
 }
 
 tpl_status check_ws(int model, int B, int Lmax, void* ws, size_t ws_bytes) {
+    if (!constants_consistent()) return fail(TPL_ERR_CUDA, "internal: backbone constant literals do not match fp64");
     if (!ws) return fail(TPL_ERR_WORKSPACE, "workspace is NULL");
     if (!aligned4(ws) || (reinterpret_cast<uintptr_t>(ws) & 15u))
         return fail(TPL_ERR_ALIGN, "workspace must be 16-byte aligned");
@@ -137,7 +164,7 @@ tpl_status tpl_backbone_forward(const float* angles, const int32_t* lengths, int
     a.err = static_cast<unsigned*>(workspace);
     a.ws_prefix = reinterpret_cast<float*>(static_cast<char*>(workspace) + kWsHeader);
     a.max_tiles = max_tiles_for(TPL_MODEL_BACKBONE, Lmax);
-    a.ortho = ortho_enabled();
+    a.ns = ns_policy();
     a.K = backbone_constants();
     cudaError_t e = bb_forward_launch(a, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "backbone forward launch");
@@ -161,7 +188,7 @@ tpl_status tpl_backbone_backward(const float* angles, const int32_t* lengths, in
     a.err = static_cast<unsigned*>(workspace);
     a.ws_prefix = reinterpret_cast<float*>(static_cast<char*>(workspace) + kWsHeader);
     a.max_tiles = max_tiles_for(TPL_MODEL_BACKBONE, Lmax);
-    a.ortho = ortho_enabled();
+    a.ns = ns_policy();
     a.K = backbone_constants();
     cudaError_t e = bb_backward_launch(a, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "backbone backward launch");
@@ -346,7 +373,7 @@ static FAArgs fa_args(const tpl_tables* T, const float* angles, const uint8_t* r
     a.err = static_cast<unsigned*>(ws);
     a.ws_prefix = reinterpret_cast<float*>(static_cast<char*>(ws) + kWsHeader);
     a.max_tiles = max_tiles_for(TPL_MODEL_FULLATOM, Lmax);
-    a.ortho = ortho_enabled();
+    a.ns = ns_policy();
     a.K = backbone_constants();
     return a;
 }

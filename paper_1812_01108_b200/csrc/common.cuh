@@ -76,6 +76,27 @@ __device__ __forceinline__ void aff_bond(Aff& M, float ca, float sa, const BondC
     M.r02 = n02; M.r12 = n12; M.r22 = n22;
 }
 
+// aff_bond with the backbone constants of transform kind k as immediates.
+template <int k>
+__device__ __forceinline__ void aff_bond_bb(Aff& M, float ca, float sa) {
+    constexpr float ct = kBBct[k], st = kBBst[k], d = kBBd[k];
+    float u0 = fmaf(ct, M.r00, -st * M.r02);
+    float u1 = fmaf(ct, M.r10, -st * M.r12);
+    float u2 = fmaf(ct, M.r20, -st * M.r22);
+    float w0 = fmaf(st, M.r00, ct * M.r02);
+    float w1 = fmaf(st, M.r10, ct * M.r12);
+    float w2 = fmaf(st, M.r20, ct * M.r22);
+    float n01 = fmaf(ca, M.r01, sa * w0), n02 = fmaf(ca, w0, -sa * M.r01);
+    float n11 = fmaf(ca, M.r11, sa * w1), n12 = fmaf(ca, w1, -sa * M.r11);
+    float n21 = fmaf(ca, M.r21, sa * w2), n22 = fmaf(ca, w2, -sa * M.r21);
+    M.t0 = fmaf(d, u0, M.t0);
+    M.t1 = fmaf(d, u1, M.t1);
+    M.t2 = fmaf(d, u2, M.t2);
+    M.r00 = u0; M.r10 = u1; M.r20 = u2;
+    M.r01 = n01; M.r11 = n11; M.r21 = n21;
+    M.r02 = n02; M.r12 = n12; M.r22 = n22;
+}
+
 // M <- M * R_x(beta) (the out-of-plane R' of P:48): columns m1, m2 rotate.
 __device__ __forceinline__ void aff_rot_x(Aff& M, float cb, float sb) {
     float a1 = fmaf(cb, M.r01, sb * M.r02), a2 = fmaf(cb, M.r02, -sb * M.r01);
@@ -129,6 +150,86 @@ __device__ __forceinline__ void aff_orthonormalize(Aff& A) {
     A.r20 = c0; A.r21 = c1; A.r22 = c2;
 }
 
+// Accurate single-precision sincos for the dihedral angles.  Fast path for
+// |x| <= 2^17: x = j (pi/2) + r with a 3-term FMA Cody-Waite reduction, minimax polynomials
+// on [-pi/4, pi/4] (the Cephes/CUDA coefficient set, < 1.5 ulp), quadrant
+// fix-up by swaps/sign flips.  Larger |x| falls back to sincosf
+// (Payne-Hanek).  ~22 instructions; no MUFU, no fast-math.
+// Returned by value: taking the address of the caller's registers would force
+// them to the local-memory stack on the hot path.
+static __device__ __noinline__ float2 tpl_sincos_slow(float x) {
+    float2 r;
+    sincosf(x, &r.x, &r.y);
+    return r;
+}
+
+// Branch-free fast path (valid for |x| <= 2^17); callers batch several angles
+// and take the (out-of-line) slow path only when one of them is huge, so the
+// polynomial evaluations of independent angles interleave (ILP).
+__device__ __forceinline__ void tpl_sincos_fast(float x, float* sp, float* cp) {
+    // round-to-nearest-int of x*2/pi with the 1.5*2^23 magic constant: keeps
+    // the quadrant in the low mantissa bits (no FRND / F2I on the XU pipe)
+    const float jm = fmaf(x, 0.636619772f, 12582912.0f);
+    const int q = __float_as_int(jm);
+    const float j = jm - 12582912.0f;
+    // pi/2 = C1 + C2 + C3 with C1 = fl32(pi/2), C2 = fl32(pi/2 - C1), C3 = fl32(pi/2 - C1 - C2);
+    // each FMA forms j*Ck exactly (emulated: max 1.47 ulp over |x| <= 1e5).
+    float r = fmaf(j, -1.570796371e+00f, x);
+    r = fmaf(j, 4.371138829e-08f, r);
+    r = fmaf(j, 1.715124510e-15f, r);
+    const float r2 = r * r;
+    float s = fmaf(fmaf(-1.95152959e-4f, r2, 8.33216087e-3f), r2, -1.66666546e-1f);
+    s = fmaf(s * r2, r, r);
+    float c = fmaf(fmaf(2.44331571e-5f, r2, -1.38873163e-3f), r2, 4.16666457e-2f);
+    c = fmaf(fmaf(c, r2, -0.5f), r2, 1.0f);
+    float sn = (q & 1) ? c : s;
+    float cs = (q & 1) ? s : c;
+    if (q & 2) sn = -sn;
+    if ((q + 1) & 2) cs = -cs;
+    *sp = sn;
+    *cp = cs;
+}
+
+// sincos of N angles on the hot path: fast evaluations only, and the largest
+// |x| folded into *maxabs.  Kernels OR "maxabs > kSinCosFastMax" over the
+// block and redo the (rare) tile with tpl_sincos_n, so the hot loop carries
+// no call and no branch.
+constexpr float kSinCosFastMax = 131072.0f;
+template <int N>
+__device__ __forceinline__ void tpl_sincos_hot(const float (&x)[N], float (&s)[N], float (&c)[N], float* maxabs) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        tpl_sincos_fast(x[i], &s[i], &c[i]);
+        *maxabs = fmaxf(*maxabs, fabsf(x[i]));
+    }
+}
+
+// sincos of N angles: N independent fast evaluations, then one rare branch.
+template <int N>
+__device__ __forceinline__ void tpl_sincos_n(const float (&x)[N], float (&s)[N], float (&c)[N]) {
+    float m = 0.f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        tpl_sincos_fast(x[i], &s[i], &c[i]);
+        m = fmaxf(m, fabsf(x[i]));
+    }
+    if (m > 131072.0f) {  // out of line: keeps the hot loops small in the I-cache
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const float2 r = tpl_sincos_slow(x[i]);
+            s[i] = r.x;
+            c[i] = r.y;
+        }
+    }
+}
+
+__device__ __forceinline__ void tpl_sincos(float x, float* sp, float* cp) {
+    float xs[1] = {x}, s[1], c[1];
+    tpl_sincos_n<1>(xs, s, c);
+    *sp = s[0];
+    *cp = c[0];
+}
+
 __device__ __forceinline__ void apply(const Aff& M, float x, float y, float z, float& ox, float& oy, float& oz) {
     ox = fmaf(M.r00, x, fmaf(M.r01, y, fmaf(M.r02, z, M.t0)));
     oy = fmaf(M.r10, x, fmaf(M.r11, y, fmaf(M.r12, z, M.t1)));
@@ -165,9 +266,11 @@ __device__ __forceinline__ Aff load_aff(const float* s) {
 // thread index, earlier on the left).  Returns carry * A_0 * ... * A_{t-1}
 // for thread t and writes carry * A_0 * ... * A_{NT-1} to *total (smem,
 // visible after the call).  scratch: NT/32 * 12 floats of smem.
-// Newton-Schulz re-orthonormalisation after every combine (kOrtho).
-template <int NT, bool kOrtho>
+// Newton-Schulz policy kNS: 0 = never, 1 = on the returned prefix and the
+// total only, 2 = after every combine as well.
+template <int NT, int kNS>
 __device__ __forceinline__ Aff block_exclusive_scan(Aff a, const Aff& carry, float* scratch, float* total) {
+    constexpr int NW = NT / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // warp inclusive scan (Kogge-Stone); left operand = lower lane.
 #pragma unroll
@@ -175,7 +278,7 @@ __device__ __forceinline__ Aff block_exclusive_scan(Aff a, const Aff& carry, flo
         Aff o = shfl_up_aff(a, d);
         if (lane >= d) {
             a = aff_compose(o, a);
-            if (kOrtho) aff_orthonormalize(a);
+            if (kNS >= 2) aff_orthonormalize(a);
         }
     }
     if (lane == 31) store_aff(scratch + 12 * warp, a);
@@ -184,15 +287,18 @@ __device__ __forceinline__ Aff block_exclusive_scan(Aff a, const Aff& carry, flo
     __syncthreads();
     // prefix over the warp totals of warps < warp, starting at the carry
     Aff p = carry;
-    for (int w = 0; w < warp; ++w) {
-        p = aff_compose(p, load_aff(scratch + 12 * w));
-        if (kOrtho) aff_orthonormalize(p);
+#pragma unroll
+    for (int w = 0; w < NW - 1; ++w) {
+        if (w < warp) {
+            p = aff_compose(p, load_aff(scratch + 12 * w));
+            if (kNS >= 2) aff_orthonormalize(p);
+        }
     }
     Aff res = aff_compose(p, ex);
-    if (kOrtho) aff_orthonormalize(res);
+    if (kNS >= 1) aff_orthonormalize(res);
     if (threadIdx.x == NT - 1) {
         Aff tot = aff_compose(p, a);
-        if (kOrtho) aff_orthonormalize(tot);
+        if (kNS >= 1) aff_orthonormalize(tot);
         store_aff(total, tot);
     }
     __syncthreads();
@@ -285,8 +391,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+// mbarrier.init visible to the async (TMA) proxy; CTA scope is enough here
+// (no clusters), and far cheaper than fence.mbarrier_init.release.cluster.
 __device__ __forceinline__ void fence_barrier_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -321,6 +429,32 @@ __device__ __forceinline__ void bulk_wait_read_all() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Programmatic dependent launch (PDL).  Kernels are launched with
+// programmatic stream serialization: everything before pdl_wait() (CTA
+// launch, shared-memory and mbarrier setup) may overlap the tail of the
+// preceding kernel; no global memory is touched before it.  pdl_trigger()
+// lets the next kernel start launching; its own pdl_wait() still waits for
+// this grid to complete and flush, so it never sees partial results.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Host: launch with programmatic stream serialization (TPL_PDL=0 disables).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 // Split of a byte range into (head | 16-aligned middle | tail).
 struct Span {
@@ -385,6 +519,27 @@ __device__ __forceinline__ void span_store_edges_f32(const Span& s, const char* 
         g[idx] = d[idx];
     }
 }
+
+// Phase timestamps for latency studies (build with -DTPL_PROFILE_PHASES; the
+// product build compiles these to nothing): thread 0 of every CTA writes
+// %globaltimer (ns) at phase boundaries to g_tpl_stamps[blockIdx * 16 + i]
+// (read back with tpl_debug_stamps, exported by that build only).
+#ifdef TPL_PROFILE_PHASES
+static __device__ unsigned long long g_tpl_stamps[1 << 16];
+__device__ __forceinline__ unsigned long long tpl_globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TPL_STAMP(i)                                                                    \
+    do {                                                                                \
+        if (threadIdx.x == 0 && blockIdx.x < 4096) g_tpl_stamps[blockIdx.x * 16 + (i)] = tpl_globaltimer(); \
+    } while (0)
+#else
+#define TPL_STAMP(i) \
+    do {             \
+    } while (0)
+#endif
 
 // Device error word (workspace[0]): bit 0 = a chain length outside [1, Lmax],
 // bit 1 = a restype outside the table.  The offending chain is skipped.

@@ -69,7 +69,7 @@ __device__ __forceinline__ float axis_moment(float ex, float ey, float ez, float
 // Saves the local N, CA and C frames of every residue and returns the
 // chunk aggregate (product of all its transforms) in M.
 template <int RPT>
-__device__ __forceinline__ void fa_chunk(const float* s_ang, int rl0, int r0, int n, const BBConst& K, Aff& M,
+__device__ __forceinline__ void fa_chunk(const float* s_ang, int rl0, int r0, int n, Aff& M,
                                          Aff (&FN)[RPT], Aff (&FCA)[RPT], Aff (&FC)[RPT]) {
     M = aff_identity();
 #pragma unroll
@@ -77,17 +77,15 @@ __device__ __forceinline__ void fa_chunk(const float* s_ang, int rl0, int r0, in
         const int rl = rl0 + q;
         const int j = r0 + rl;
         if (rl < n) {
-            float s, c;
-            if (j > 0) {  // N_j from C_{j-1} by omega_{j-1}  (R_0 = I for j = 0)
-                sincosf(s_ang[8 * rl - 6], &s, &c);
-                aff_bond(M, c, s, K.b[0]);
-            }
+            // omega_{j-1} (C_{j-1} -> N_j; R_0 = I for j = 0), phi_j (-> CA_j), psi_j (-> C_j)
+            const float x[3] = {j > 0 ? s_ang[8 * rl - 6] : 0.f, s_ang[8 * rl + 0], s_ang[8 * rl + 1]};
+            float s[3], c[3];
+            tpl_sincos_n<3>(x, s, c);
+            if (j > 0) aff_bond_bb<0>(M, c[0], s[0]);
             FN[q] = M;
-            sincosf(s_ang[8 * rl + 0], &s, &c);  // CA_j by phi_j
-            aff_bond(M, c, s, K.b[1]);
+            aff_bond_bb<1>(M, c[1], s[1]);
             FCA[q] = M;
-            sincosf(s_ang[8 * rl + 1], &s, &c);  // C_j by psi_j
-            aff_bond(M, c, s, K.b[2]);
+            aff_bond_bb<2>(M, c[2], s[2]);
             FC[q] = M;
         } else {
             FN[q] = M;
@@ -97,7 +95,7 @@ __device__ __forceinline__ void fa_chunk(const float* s_ang, int rl0, int r0, in
     }
 }
 
-template <int NT, int RPT, bool kOrtho>
+template <int NT, int RPT, int kNS>
 __global__ void __launch_bounds__(NT) fa_forward_kernel(FAArgs a, int stage_atoms_per_res) {
     constexpr int TILE = NT * RPT;
     using S = FASmem<NT>;
@@ -184,9 +182,9 @@ __global__ void __launch_bounds__(NT) fa_forward_kernel(FAArgs a, int stage_atom
 
         Aff M;
         Aff FN[RPT], FCA[RPT], FC[RPT];
-        fa_chunk<RPT>(s_ang, rl0, r0, n, a.K, M, FN, FCA, FC);
-        if (kOrtho) aff_orthonormalize(M);
-        const Aff P = block_exclusive_scan<NT, kOrtho>(M, carry, s_scan, s_total);
+        fa_chunk<RPT>(s_ang, rl0, r0, n, M, FN, FCA, FC);
+        if (kNS >= 1) aff_orthonormalize(M);
+        const Aff P = block_exclusive_scan<NT, kNS>(M, carry, s_scan, s_total);
         carry = load_aff(s_total);
 
         const int n_tile_atoms = tile_end_atoms - carry_atoms;
@@ -215,7 +213,7 @@ __global__ void __launch_bounds__(NT) fa_forward_kernel(FAArgs a, int stage_atom
                         if (gr.has_pre) aff_rot_x(G, gr.cb, gr.sb);
                     }
                     float s, c;
-                    if (gr.slot >= 0) sincosf(ang[gr.slot], &s, &c);
+                    if (gr.slot >= 0) tpl_sincos(ang[gr.slot], &s, &c);
                     else { s = gr.sa; c = gr.ca; }
                     const BondC bc{gr.ct, gr.st, gr.d};
                     aff_bond(G, c, s, bc);
@@ -281,7 +279,7 @@ __device__ __forceinline__ void fa_residue_backward(const FAType& T, const float
         for (int g = g0; g <= g1; ++g) {
             const FAGroup& gr = T.g[g];
             float s, c;
-            if (gr.slot >= 0) sincosf(ang[gr.slot], &s, &c);
+            if (gr.slot >= 0) tpl_sincos(ang[gr.slot], &s, &c);
             else { s = gr.sa; c = gr.ca; }
             aff_bond(G, c, s, BondC{gr.ct, gr.st, gr.d});
         }
@@ -296,7 +294,7 @@ __device__ __forceinline__ void fa_residue_backward(const FAType& T, const float
             if (gr.slot >= 0) go[gr.slot] = axis_moment(G.r00, G.r10, G.r20, G.t0 - cx, G.t1 - cy, G.t2 - cz, br);
             if (g > g0) {
                 float s, c;
-                if (gr.slot >= 0) sincosf(ang[gr.slot], &s, &c);
+                if (gr.slot >= 0) tpl_sincos(ang[gr.slot], &s, &c);
                 else { s = gr.sa; c = gr.ca; }
                 aff_unbond(G, c, s, BondC{gr.ct, gr.st, gr.d});
             }
@@ -309,7 +307,7 @@ __device__ __forceinline__ void fa_residue_backward(const FAType& T, const float
     for (int q = 0; q < 6; ++q) R.all[q] += R.nN[q] + R.cC[q];
 }
 
-template <int NT, int RPT, bool kOrtho>
+template <int NT, int RPT, int kNS>
 __global__ void __launch_bounds__(NT) fa_backward_kernel(FAArgs a, int stage_atoms_per_res) {
     constexpr int TILE = NT * RPT;
     using S = FASmem<NT>;
@@ -387,9 +385,9 @@ __global__ void __launch_bounds__(NT) fa_backward_kernel(FAArgs a, int stage_ato
             block_exclusive_sum_int<NT>(cnt, carry_atoms, s_int, &tile_end);
             Aff M;
             Aff FN[RPT], FCA[RPT], FC[RPT];
-            fa_chunk<RPT>(s_ang, rl0, r0, TILE, a.K, M, FN, FCA, FC);
-            if (kOrtho) aff_orthonormalize(M);
-            block_exclusive_scan<NT, kOrtho>(M, carry, s_scan, s_total);
+            fa_chunk<RPT>(s_ang, rl0, r0, TILE, M, FN, FCA, FC);
+            if (kNS >= 1) aff_orthonormalize(M);
+            block_exclusive_scan<NT, kNS>(M, carry, s_scan, s_total);
             carry = load_aff(s_total);
             carry_atoms = tile_end;
             if (tid < 12) pref[(t + 1) * 16 + tid] = s_total[tid];
@@ -459,9 +457,9 @@ __global__ void __launch_bounds__(NT) fa_backward_kernel(FAArgs a, int stage_ato
 
         Aff M;
         Aff FN[RPT], FCA[RPT], FC[RPT];
-        fa_chunk<RPT>(s_ang, rl0, r0, n, a.K, M, FN, FCA, FC);
-        if (kOrtho) aff_orthonormalize(M);
-        const Aff P = block_exclusive_scan<NT, kOrtho>(M, carry, s_scan, s_total);  // contains __syncthreads
+        fa_chunk<RPT>(s_ang, rl0, r0, n, M, FN, FCA, FC);
+        if (kNS >= 1) aff_orthonormalize(M);
+        const Aff P = block_exclusive_scan<NT, kNS>(M, carry, s_scan, s_total);  // contains __syncthreads
         mbar_wait(bar, phase);
         phase ^= 1u;
         __syncthreads();
@@ -589,7 +587,7 @@ static size_t fa_bwd_smem(int n_types) {
     return fa_fwd_smem<RPT>(n_types) + Lay::go_bytes;
 }
 
-template <int RPT, bool O>
+template <int RPT, int O>
 static cudaError_t fa_fwd(const FAArgs& a, cudaStream_t st) {
     auto k = fa_forward_kernel<kFAThreads, RPT, O>;
     const size_t sm = fa_fwd_smem<RPT>(a.n_types);
@@ -602,7 +600,7 @@ static cudaError_t fa_fwd(const FAArgs& a, cudaStream_t st) {
     k<<<a.B, kFAThreads, sm, st>>>(a, kMaxAtomsPerRes);
     return cudaGetLastError();
 }
-template <int RPT, bool O>
+template <int RPT, int O>
 static cudaError_t fa_bwd(const FAArgs& a, cudaStream_t st) {
     auto k = fa_backward_kernel<kFAThreads, RPT, O>;
     const size_t sm = fa_bwd_smem<RPT>(a.n_types);
@@ -618,13 +616,15 @@ static cudaError_t fa_bwd(const FAArgs& a, cudaStream_t st) {
 
 cudaError_t fa_forward_launch(const FAArgs& a, cudaStream_t st) {
     const int r = fa_rpt_for(a.Lmax);
-    if (a.ortho) return r == 1 ? fa_fwd<1, true>(a, st) : fa_fwd<2, true>(a, st);
-    return r == 1 ? fa_fwd<1, false>(a, st) : fa_fwd<2, false>(a, st);
+    if (a.ns == 0) return r == 1 ? fa_fwd<1, 0>(a, st) : fa_fwd<2, 0>(a, st);
+    if (a.ns == 2) return r == 1 ? fa_fwd<1, 2>(a, st) : fa_fwd<2, 2>(a, st);
+    return r == 1 ? fa_fwd<1, 1>(a, st) : fa_fwd<2, 1>(a, st);
 }
 cudaError_t fa_backward_launch(const FAArgs& a, cudaStream_t st) {
     const int r = fa_rpt_for(a.Lmax);
-    if (a.ortho) return r == 1 ? fa_bwd<1, true>(a, st) : fa_bwd<2, true>(a, st);
-    return r == 1 ? fa_bwd<1, false>(a, st) : fa_bwd<2, false>(a, st);
+    if (a.ns == 0) return r == 1 ? fa_bwd<1, 0>(a, st) : fa_bwd<2, 0>(a, st);
+    if (a.ns == 2) return r == 1 ? fa_bwd<1, 2>(a, st) : fa_bwd<2, 2>(a, st);
+    return r == 1 ? fa_bwd<1, 1>(a, st) : fa_bwd<2, 1>(a, st);
 }
 
 }  // namespace tpl

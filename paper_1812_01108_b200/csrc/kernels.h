@@ -11,15 +11,21 @@ struct BondC {
     float ct, st, d;
 };
 
-constexpr int kBBThreads = 256;
+constexpr int kBBThreads = 128;
 constexpr int kFAThreads = 256;
 constexpr int kMaxGroups = 8;
 constexpr int kMaxAtomsPerRes = 16;
 constexpr int kMaxTypes = 32;
 constexpr int kFASlots = 8;
 
-// Backbone constants (cos theta, sin theta, d) for k = 0 (C-N, omega),
-// 1 (N-CA, phi), 2 (CA-C, psi): PAPER.md P:161-167, rounded from fp64.
+// Backbone transform constants: theta_k = pi - 2.1186,
+// pi - 1.9391, pi - 2.0610 and d_k = 1.330, 1.460, 1.525 for k = 0 (C-N,
+// omega), 1 (N-CA, phi), 2 (CA-C, psi).  cos/sin evaluated in fp64 and rounded
+// once to fp32 (reading Q20); tests/test_abi_cpu.py re-derives every literal.
+// Compile-time literals so the bond products issue as immediate-operand FFMAs.
+constexpr float kBBct[3] = {5.208135247e-01f, 3.600333929e-01f, 4.708055854e-01f};
+constexpr float kBBst[3] = {8.536704779e-01f, 9.329394102e-01f, 8.822369576e-01f};
+constexpr float kBBd[3] = {1.330000043e+00f, 1.460000038e+00f, 1.524999976e+00f};
 struct BBConst {
     BondC b[3];
 };
@@ -34,14 +40,14 @@ struct BBArgs {
     unsigned* err;
     float* ws_prefix;
     int max_tiles;
-    bool ortho;
+    int ns;  // Newton-Schulz policy: 0 none, 1 prefix/total, 2 every combine
     BBConst K;
 };
 
+bool pdl_enabled();  // capi.cu: programmatic dependent launch on (TPL_PDL != 0)
+
 int bb_rpt_for(int Lmax);
 int bb_tile_for(int Lmax);
-size_t bb_forward_smem(int rpt);
-size_t bb_backward_smem(int rpt);
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st);
 
@@ -80,7 +86,7 @@ struct FAArgs {
     unsigned* err;
     float* ws_prefix;  // per chain per tile: 12 floats prefix + 1 int atom offset (stride 16)
     int max_tiles;
-    bool ortho;
+    int ns;
     BBConst K;
 };
 

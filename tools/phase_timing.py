@@ -1,0 +1,61 @@
+#!/usr/bin/env python3
+"""Phase timeline of bb_forward_kernel CTAs (needs the phase-stamp build):
+
+    python -m paper_1812_01108_b200.build --phases
+    TPL_LIB=paper_1812_01108_b200/build/libtpl_phases.so python tools/phase_timing.py --B 256 --L 700
+
+Prints, over CTAs, the median / max time (ns, %globaltimer) of each phase
+relative to the earliest CTA start.
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_1812_01108_b200 import _abi  # noqa: E402
+
+NAMES = ["start", "lengths", "tma issued", "tma landed", "pass1 done", "scan done", "pass2 done", "synced",
+         "store issued", "store done"]
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--B", type=int, default=256)
+    p.add_argument("--L", type=int, default=700)
+    a = p.parse_args()
+    torch.cuda.set_device(0)
+    L = _abi.lib
+    L.tpl_debug_stamps.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    ang = synth.angles_uniform(a.B, a.L, 3, 1).cuda()
+    ln = torch.full((a.B,), a.L, dtype=torch.int32, device="cuda")
+    c = torch.empty(a.B, 3 * a.L, 3, device="cuda")
+    ws = torch.zeros(_abi.tpl_workspace_bytes(0, a.B, a.L), dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        _abi.tpl_backbone_forward(ang, ln, c, ws)
+    torch.cuda.synchronize()
+    L.tpl_debug_stamps_clear()
+    _abi.tpl_backbone_forward(ang, ln, c, ws)
+    torch.cuda.synchronize()
+    n = min(a.B, 4096)
+    buf = (ctypes.c_ulonglong * (n * 16))()
+    L.tpl_debug_stamps(buf, n * 16)
+    st = np.array(buf, dtype=np.int64).reshape(n, 16)[:, :10]
+    t0 = st[:, 0].min()
+    rel = st - t0
+    print(f"B={a.B} L={a.L}: kernel span {rel[:, 9].max() / 1e3:.2f} us (first CTA start -> last store done)")
+    for i, nm in enumerate(NAMES):
+        d = rel[:, i]
+        step = (st[:, i] - st[:, i - 1]) if i else rel[:, 0]
+        print(f"  {nm:13s} at median {np.median(d) / 1e3:6.2f} us, max {d.max() / 1e3:6.2f} us;"
+              f"  phase median {np.median(step) / 1e3:6.2f} us max {step.max() / 1e3:6.2f}")
+
+
+if __name__ == "__main__":
+    main()
