@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds of the cpu_baseline sample")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: every rank runs the config's batch; strong: the batch is split (LPT)")
     return p.parse_args()
 
 
@@ -163,12 +165,18 @@ def sum_over_ranks(x, dist):
 class BackboneWork:
     model = "backbone"
 
-    def __init__(self, c, rank):
+    def __init__(self, c, rank, world=1, strong=False):
         cfg = synth.CONFIGS[c]
         self.cfg = cfg
-        # weak scaling: rank r draws its own batch (seed offset by rank)
         ang, lengths, grad = synth.backbone_inputs(c)
-        if rank:
+        if strong and world > 1:
+            # strong scaling: the config's batch is split (LPT for ragged lengths)
+            from paper_1812_01108_b200 import dist as tdist
+
+            idx = torch.tensor(tdist.plan(lengths.tolist(), world)[rank], dtype=torch.long)
+            ang, lengths, grad = ang[idx].contiguous(), lengths[idx].contiguous(), grad[idx].contiguous()
+        elif rank:
+            # weak scaling: rank r draws its own batch (seed offset by rank)
             ang = synth.angles_uniform(ang.shape[0], ang.shape[1], 3, 1000 + synth.config_id(c) + 7919 * rank)
         self.host = dict(angles=ang, lengths=lengths, grad=grad)
         self.B, self.Lmax = ang.shape[0], ang.shape[1]
@@ -213,14 +221,20 @@ class BackboneWork:
 class FullAtomWork:
     model = "fullatom"
 
-    def __init__(self, c, rank):
+    def __init__(self, c, rank, world=1, strong=False):
         import paper_1812_01108_b200 as tpl
 
         cfg = synth.CONFIGS[c]
         self.cfg = cfg
         B = cfg["B"]
         ang, rt, lengths = synth.fullatom_inputs(c, B=B)
-        if rank:
+        if strong and world > 1:
+            from paper_1812_01108_b200 import dist as tdist
+
+            idx = torch.tensor(tdist.plan(lengths.tolist(), world)[rank], dtype=torch.long)
+            ang, rt, lengths = ang[idx].contiguous(), rt[idx].contiguous(), lengths[idx].contiguous()
+            B = len(idx)
+        elif rank:
             ang = synth.angles_uniform(B, cfg["L"], 8, 1000 + synth.config_id(c) + 7919 * rank)
             rt = synth.restype_uniform(B, cfg["L"], 20, 4000 + synth.config_id(c) + 7919 * rank)
         self.table = synth.load_residue_table()
@@ -273,8 +287,9 @@ class FullAtomWork:
                 "atoms_per_gpu": self.atoms}
 
 
-def make_work(c, rank):
-    return (BackboneWork if synth.CONFIGS[c]["model"] == "backbone" else FullAtomWork)(c, rank)
+def make_work(c, rank, world=1, strong=False):
+    cls = BackboneWork if synth.CONFIGS[c]["model"] == "backbone" else FullAtomWork
+    return cls(c, rank, world, strong)
 
 
 # --------------------------------------------------------------- graphs
@@ -316,7 +331,7 @@ def run_ours(args):
 
     world, rank, local, dist = dist_setup(args)
     c = cfg_key(args.config)
-    work = make_work(c, rank)
+    work = make_work(c, rank, world, args.scaling == "strong")
     props = torch.cuda.get_device_properties(local)
     l2 = getattr(props, "L2_cache_size", 126 * 2 ** 20)
     n_sets = max(2, math.ceil(4 * l2 / work.footprint()))
@@ -435,12 +450,13 @@ def run_ours(args):
 
     if rank == 0:
         cfgd = work.config()
-        cfgd.update({"global_batch": work.B * world, "parallelism": f"dp{world} (chains sharded, no collective)",
+        gb = work.cfg["B"] if args.scaling == "strong" else work.B * world
+        cfgd.update({"global_batch": gb, "parallelism": f"dp{world} (chains sharded, no collective)",
                      "l2_flush": f"rotating {n_sets} buffer sets ({n_sets * work.footprint() / 2**20:.0f} MiB > 4x L2)",
                      "timing": f"CUDA graphs of K steps, median of {len(t_step)} timed regions"})
         out = {"metric": f"residues/sec fwd+bwd ({work.model}, L={work.Lmax}, batch {work.B})",
                "value": value, "unit": "residues/s", "n_gpus": world, "steps": K, "warmup": W,
-               "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
                "dtype": "f32", "data": "synthetic (seeded uniform angles, N(0,1) dL/dr)", "config": cfgd,
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": 2 * K,
                "impl": "ours"}

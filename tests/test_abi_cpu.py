@@ -104,3 +104,24 @@ def test_cuda_tensors_required(abi):
     with pytest.raises(TypeError):
         abi.tpl_backbone_forward(a, torch.ones(1, dtype=torch.int32), torch.zeros(1, 12, 3),
                                  torch.zeros(4096, dtype=torch.uint8))
+
+
+def test_backbone_constant_literals():
+    """kernels.h compiles the §3 constants as fp32 literals: each must be
+    the fp64 cos/sin of pi - 2.1186 / pi - 1.9391 / pi - 2.0610 and d, rounded once."""
+    import math
+
+    import numpy as np
+
+    with open(os.path.join(ROOT, "paper_1812_01108_b200", "csrc", "kernels.h")) as f:
+        src = f.read()
+
+    def lits(name):
+        m = re.search(name + r"\[3\] = \{([^}]*)\}", src)
+        return [np.float32(float(x.strip().rstrip("f"))) for x in m.group(1).split(",")]
+
+    th = [math.pi - 2.1186, math.pi - 1.9391, math.pi - 2.0610]
+    d = [1.330, 1.460, 1.525]
+    assert lits("kBBct") == [np.float32(math.cos(t)) for t in th]
+    assert lits("kBBst") == [np.float32(math.sin(t)) for t in th]
+    assert lits("kBBd") == [np.float32(x) for x in d]

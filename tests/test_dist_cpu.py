@@ -1,0 +1,77 @@
+"""Multi-GPU host logic on the CPU: shard planning and the scalar reductions,
+exercised in a world-size-2 gloo process group (127.0.0.1)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1812_01108_b200 import dist as tdist
+
+
+def test_contiguous_cover_and_balance():
+    for n, w in ((256, 1), (256, 2), (256, 8), (10, 4), (3, 8)):
+        sh = tdist.contiguous_shards(n, w)
+        flat = [i for s in sh for i in s]
+        assert flat == list(range(n))
+        assert max(map(len, sh)) - min(map(len, sh)) <= 1
+
+
+def test_lpt_cover_order_and_balance():
+    rng = np.random.default_rng(0)
+    lengths = rng.integers(50, 2001, size=4096)
+    for w in (2, 4, 8):
+        sh = tdist.lpt_shards(lengths, w)
+        flat = sorted(i for s in sh for i in s)
+        assert flat == list(range(4096))
+        for s in sh:  # longest first inside a shard
+            ls = [lengths[i] for i in s]
+            assert ls == sorted(ls, reverse=True)
+        assert tdist.imbalance(lengths, sh) < 1.01
+    assert tdist.plan([700] * 10, 4) == tdist.contiguous_shards(10, 4)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lengths = [int(x) for x in np.random.default_rng(1).integers(50, 2001, size=64)]
+    shards = tdist.plan(lengths, world)
+    mine = shards[rank]
+    residues = sum(lengths[i] for i in mine)
+    tot = tdist.reduce_scalar(residues, "sum", dist)
+    mx = tdist.reduce_scalar(float(rank + 1) * 1.5, "max", dist)
+    # every rank sees the same global plan: gather the chain ids and check coverage
+    ids = [None] * world
+    dist.all_gather_object(ids, mine)
+    q.put((rank, tot, mx, sorted(i for s in ids for i in s), sum(lengths)))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_reductions_and_coverage():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, tot, mx, ids, total in res:
+        assert tot == total
+        assert mx == 3.0
+        assert ids == list(range(64))
