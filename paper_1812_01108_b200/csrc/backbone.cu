@@ -15,13 +15,15 @@
 // chunk start, gradients rotated into it): fewer flops than moving every
 // position and axis to the global frame, and smaller moments.
 //
-// Work decomposition: one CTA of NT threads per chain; a tile of NT*RPT
-// residues per CTA iteration; each thread owns RPT consecutive residues
-// (3*RPT transforms) and composes them sequentially, then one block-wide
-// affine scan combines the chunks.  Longer chains loop over tiles carrying
-// the prefix transform (forward) or, in backward, run a prefix pre-pass
-// (phase A, tile prefixes to the workspace) then walk tiles last-to-first
-// carrying the suffix sums.  Tiles move global<->shared with TMA bulk copies.
+// Work decomposition: a CTA of NT threads owns one chain at a time; a tile is
+// NT*RPT residues; each thread composes RPT consecutive residues (3*RPT
+// transforms) in registers, then one block-wide affine scan combines the
+// chunks.  CTAs are persistent over chains (grid <= resident CTAs) and run a
+// two-deep TMA pipeline: the next work item's tile is bulk-copied into the
+// other shared-memory buffer while the current one is computed.  Work items:
+//   forward : every tile of every chain, first to last (prefix carried);
+//   backward: phase A = tile prefixes of all but the last tile (to the
+//             workspace), then phase B = tiles last to first (suffix carried).
 #include <cstdlib>
 #include <type_traits>
 
@@ -33,7 +35,7 @@ namespace tpl {
 template <int NT>
 struct BBSmem {
     static constexpr int NW = NT / 32;
-    static constexpr int kBar = 0;                         // uint64 mbarrier (16 B slot)
+    static constexpr int kBar = 0;                         // 2 uint64 mbarriers (one per buffer)
     static constexpr int kScratch = 16;                    // NW*12 floats (affine scan)
     static constexpr int kSuf = kScratch + NW * 12 * 4;    // NW*6 floats (suffix scan)
     static constexpr int kTotal = kSuf + NW * 6 * 4;       // 12 floats
@@ -42,6 +44,9 @@ struct BBSmem {
 };
 
 __host__ __device__ constexpr int round16(int x) { return (x + 15) & ~15; }
+// __launch_bounds__ min-blocks so that ptxas keeps <= 128 registers/thread
+// (2 CTAs of 256, 4 of 128, 16 of 32 threads per SM).
+__host__ __device__ constexpr int kMinBlocks128Regs(int nt) { return 65536 / (nt * 128); }
 
 // The three transforms of residue j (local index rl in the staged tile):
 // k = 0: C_{j-1} -> N_j by omega_{j-1} (identity for j = 0, reading Q1),
@@ -56,55 +61,127 @@ __device__ __forceinline__ void bb_residue_trig(const float* s_ang, int rl, int 
     else tpl_sincos_hot<3>(x, s, c, maxabs);
 }
 
+// ---------------------------------------------------------------------------
+// Work-item iterator of one CTA (every thread computes the same sequence).
+// Chains b = blockIdx.x, blockIdx.x + gridDim.x, ...; the length of the next
+// chain is loaded one chain ahead so the prefetch never waits for it.
+struct BBIter {
+    const int* lengths;
+    int B, Lmax, tile, stride;
+    bool fwd;
+    unsigned* err;
+    int b, L, bn, Ln;  // current chain and the next one
+    int t, nt, phase;  // tile, tiles in chain, 0 = fwd/phase A, 1 = phase B
+    bool valid;
+
+    __device__ int load_len(int c) const { return c < B ? __ldg(lengths + c) : 0; }
+    __device__ void next_chain() {
+        b = bn;
+        L = Ln;
+        bn = b + stride;
+        Ln = load_len(bn);
+    }
+    __device__ void start_chain() {  // skips invalid chains (flagged), sets the first tile
+        while (b < B && (L < 1 || L > Lmax)) {
+            if (threadIdx.x == 0) atomicOr(err, ERR_LENGTH);
+            next_chain();
+        }
+        valid = b < B;
+        if (!valid) return;
+        nt = (L + tile - 1) / tile;
+        t = 0;
+        phase = (fwd || nt == 1) ? (fwd ? 0 : 1) : 0;
+    }
+    __device__ void init() {
+        b = blockIdx.x;
+        L = load_len(b);
+        bn = b + stride;
+        Ln = load_len(bn);
+        start_chain();
+    }
+    __device__ void advance() {
+        if (fwd) {
+            if (t + 1 < nt) { ++t; return; }
+        } else if (phase == 0) {
+            if (t + 1 < nt - 1) ++t;
+            else { phase = 1; t = nt - 1; }
+            return;
+        } else if (t > 0) {
+            --t;
+            return;
+        }
+        next_chain();
+        start_chain();
+    }
+    __device__ int r0() const { return t * tile; }
+    __device__ int n() const { return min(tile, L - t * tile); }
+};
+
+// Issue (thread 0) the bulk copies of one work item into buffer `buf`.
+__device__ __forceinline__ void bb_issue(const BBIter& it, const float* angles, const float* grad_coords,
+                                         char* s_ang, char* s_g, uint64_t* bar) {
+    const int r0 = it.r0(), n = it.n(), pre = r0 > 0 ? 1 : 0;
+    const Span sa = make_span(angles + ((size_t)it.b * it.Lmax + r0 - pre) * 3, (n + pre) * 12);
+    unsigned bytes = unsigned(sa.mid);
+    Span sg{};
+    const bool with_g = grad_coords && it.phase == 1;
+    if (with_g) {
+        sg = make_span(grad_coords + ((size_t)it.b * 3 * it.Lmax + 3 * (size_t)r0) * 3, n * 36);
+        bytes += unsigned(sg.mid);
+    }
+    mbar_arrive_expect_tx(bar, bytes);
+    span_load_bulk(sa, s_ang, bar);
+    if (with_g) span_load_bulk(sg, s_g, bar);
+}
+
 template <int NT, int RPT, int kNS>
-__global__ void __launch_bounds__(NT) bb_forward_kernel(const float* __restrict__ angles,
-                                                        const int* __restrict__ lengths, int Lmax,
+__global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(const float* __restrict__ angles,
+                                                        const int* __restrict__ lengths, int B, int Lmax,
                                                         float* __restrict__ coords, unsigned* __restrict__ err) {
     constexpr int TILE = NT * RPT;
+    constexpr int ANG = round16(16 + 12 * (TILE + 1));
     using S = BBSmem<NT>;
     extern __shared__ __align__(16) char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
     float* scratch = reinterpret_cast<float*>(smem + S::kScratch);
     float* s_total = reinterpret_cast<float*>(smem + S::kTotal);
-    char* s_ang_base = smem + S::kData;
-    char* s_out_base = s_ang_base + round16(16 + 12 * (TILE + 1));
+    char* s_ang_buf = smem + S::kData;  // 2 x ANG
+    char* s_out_base = s_ang_buf + 2 * ANG;
 
-    const int b = blockIdx.x;
     const int tid = threadIdx.x;
     TPL_STAMP(0);
     if (tid == 0) {
         mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
         fence_barrier_init();
     }
     pdl_wait();
     pdl_trigger();
-    const int L = lengths[b];
+    BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), true, err};
+    it.init();
     TPL_STAMP(1);
     __syncthreads();
-    if (L < 1 || L > Lmax) {
-        if (tid == 0) atomicOr(err, ERR_LENGTH);
-        return;
-    }
+    if (tid == 0 && it.valid) bb_issue(it, angles, nullptr, s_ang_buf, nullptr, bar);
 
     Aff carry = aff_identity();
-    unsigned phase = 0;
+    unsigned phases = 0;  // bit k = parity of buffer k
     const int rl0 = tid * RPT;
-    for (int r0 = 0; r0 < L; r0 += TILE) {
-        const int n = min(TILE, L - r0);
-        const int pre = r0 > 0 ? 1 : 0;
-        // ---- stage angles [r0-pre, r0+n) with one bulk copy (+ edges)
+    for (int k = 0; it.valid; ++k) {
+        const int buf = k & 1;
+        const int b = it.b, L = it.L, r0 = it.r0(), n = it.n(), pre = r0 > 0 ? 1 : 0;
+        if (r0 == 0) carry = aff_identity();
+        BBIter nx = it;
+        nx.advance();
+        if (tid == 0 && nx.valid) bb_issue(nx, angles, nullptr, s_ang_buf + (buf ^ 1) * ANG, nullptr, bar + (buf ^ 1));
+        // ---- angles [r0-pre, r0+n): bulk part by TMA, <16-byte edges by threads
+        char* s_ang_base = s_ang_buf + buf * ANG;
         const Span sa = make_span(angles + ((size_t)b * Lmax + r0 - pre) * 3, (n + pre) * 12);
-        if (tid == 0) {
-            bulk_wait_read_all();  // previous tile's output staging may still be read by TMA
-            mbar_arrive_expect_tx(bar, unsigned(sa.mid));
-            span_load_bulk(sa, s_ang_base, bar);
-        }
         span_load_edges_f32(sa, s_ang_base);
         const Span so = make_span(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3, n * 36);
         float* s_out = reinterpret_cast<float*>(s_out_base + so.mis());
         TPL_STAMP(2);
-        mbar_wait(bar, phase);
-        phase ^= 1u;
+        mbar_wait(bar + buf, (phases >> buf) & 1u);
+        phases ^= 1u << buf;
         __syncthreads();
         TPL_STAMP(3);
         const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 3 * pre;
@@ -137,6 +214,7 @@ __global__ void __launch_bounds__(NT) bb_forward_kernel(const float* __restrict_
         pass1(std::false_type{});
         if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
         if (kNS >= 1) aff_orthonormalize(M);
+        if (tid == 0) bulk_wait_read_all();  // the output staging is free again
         TPL_STAMP(4);
         const Aff P = block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
         carry = load_aff(s_total);
@@ -148,9 +226,9 @@ __global__ void __launch_bounds__(NT) bb_forward_kernel(const float* __restrict_
             if (q < nq) {
                 float* o = s_out + 9 * (rl0 + q);
 #pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    const int a = 3 * q + k;
-                    apply(P, px[a], py[a], pz[a], o[3 * k], o[3 * k + 1], o[3 * k + 2]);
+                for (int kk = 0; kk < 3; ++kk) {
+                    const int a = 3 * q + kk;
+                    apply(P, px[a], py[a], pz[a], o[3 * kk], o[3 * kk + 1], o[3 * kk + 2]);
                 }
             }
         }
@@ -163,6 +241,8 @@ __global__ void __launch_bounds__(NT) bb_forward_kernel(const float* __restrict_
             bulk_commit();
         }
         span_store_edges_f32(so, s_out_base);
+        (void)L;
+        it = nx;
     }
     TPL_STAMP(8);
     // Only the shared-memory source must outlive the CTA; grid completion (and the
@@ -172,12 +252,14 @@ __global__ void __launch_bounds__(NT) bb_forward_kernel(const float* __restrict_
 }
 
 template <int NT, int RPT, int kNS>
-__global__ void __launch_bounds__(NT) bb_backward_kernel(const float* __restrict__ angles,
-                                                         const int* __restrict__ lengths, int Lmax,
+__global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(const float* __restrict__ angles,
+                                                         const int* __restrict__ lengths, int B, int Lmax,
                                                          const float* __restrict__ grad_coords,
                                                          float* __restrict__ grad_angles, unsigned* __restrict__ err,
                                                          float* __restrict__ ws_prefix, int max_tiles) {
     constexpr int TILE = NT * RPT;
+    constexpr int ANG = round16(16 + 12 * (TILE + 1));
+    constexpr int GB = round16(16 + 36 * TILE);
     using S = BBSmem<NT>;
     extern __shared__ __align__(16) char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
@@ -185,45 +267,61 @@ __global__ void __launch_bounds__(NT) bb_backward_kernel(const float* __restrict
     float* s_suf = reinterpret_cast<float*>(smem + S::kSuf);
     float* s_total = reinterpret_cast<float*>(smem + S::kTotal);
     float* s_misc = reinterpret_cast<float*>(smem + S::kMisc);
-    char* s_ang_base = smem + S::kData;
-    char* s_g_base = s_ang_base + round16(16 + 12 * (TILE + 1));
-    char* s_go_base = s_g_base + round16(16 + 36 * TILE);
+    char* s_ang_buf = smem + S::kData;    // 2 x ANG
+    char* s_g_buf = s_ang_buf + 2 * ANG;  // 2 x GB
+    char* s_go_base = s_g_buf + 2 * GB;
 
-    const int b = blockIdx.x;
     const int tid = threadIdx.x;
     if (tid == 0) {
         mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
         fence_barrier_init();
     }
     pdl_wait();
     pdl_trigger();
-    const int L = lengths[b];
+    BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), false, err};
+    it.init();
     __syncthreads();
-    if (L < 1 || L > Lmax) {
-        if (tid == 0) atomicOr(err, ERR_LENGTH);
-        return;
-    }
-    const int n_tiles = (L + TILE - 1) / TILE;
-    unsigned phase = 0;
-    const int rl0 = tid * RPT;
-    float* pref = ws_prefix + (size_t)b * max_tiles * 12;
+    if (tid == 0 && it.valid) bb_issue(it, angles, grad_coords, s_ang_buf, s_g_buf, bar);
 
-    // ---- phase A: prefix transform at the start of every tile but the first
-    if (n_tiles > 1) {
-        Aff carry = aff_identity();
-        for (int t = 0; t + 1 < n_tiles; ++t) {
-            const int r0 = t * TILE;
-            const int pre = r0 > 0 ? 1 : 0;
-            const Span sa = make_span(angles + ((size_t)b * Lmax + r0 - pre) * 3, (TILE + pre) * 12);
-            if (tid == 0) {
-                mbar_arrive_expect_tx(bar, unsigned(sa.mid));
-                span_load_bulk(sa, s_ang_base, bar);
-            }
-            span_load_edges_f32(sa, s_ang_base);
-            mbar_wait(bar, phase);
-            phase ^= 1u;
-            __syncthreads();
-            const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 3 * pre;
+    unsigned phases = 0;
+    const int rl0 = tid * RPT;
+    Aff carryA = aff_identity();                        // phase A prefix carry
+    float carry6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // phase B suffix carry
+    float omega_next = 0.f;  // dL/d omega of the tile's last residue (from the later tile)
+    for (int k = 0; it.valid; ++k) {
+        const int buf = k & 1;
+        const int b = it.b, L = it.L, t = it.t, r0 = it.r0(), pre = r0 > 0 ? 1 : 0;
+        const int n = it.n();
+        const bool phaseB = it.phase == 1;
+        if (!phaseB && t == 0) carryA = aff_identity();
+        if (phaseB && t == it.nt - 1) {
+#pragma unroll
+            for (int q = 0; q < 6; ++q) carry6[q] = 0.f;
+            omega_next = 0.f;
+        }
+        float* pref = ws_prefix + (size_t)b * max_tiles * 12;
+        BBIter nx = it;
+        nx.advance();
+        if (tid == 0 && nx.valid)
+            bb_issue(nx, angles, grad_coords, s_ang_buf + (buf ^ 1) * ANG, s_g_buf + (buf ^ 1) * GB, bar + (buf ^ 1));
+        char* s_ang_base = s_ang_buf + buf * ANG;
+        char* s_g_base = s_g_buf + buf * GB;
+        const Span sa = make_span(angles + ((size_t)b * Lmax + r0 - pre) * 3, (n + pre) * 12);
+        span_load_edges_f32(sa, s_ang_base);
+        Span sg{};
+        if (phaseB) {
+            sg = make_span(grad_coords + ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3, n * 36);
+            span_load_edges_f32(sg, s_g_base);
+        }
+        mbar_wait(bar + buf, (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+        __syncthreads();
+        const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 3 * pre;
+        const int nq = max(0, min(RPT, n - rl0));
+
+        if (!phaseB) {
+            // ---- phase A: chunk aggregates only; the tile total becomes the prefix of tile t+1
             Aff M;
             float maxabs = 0.f;
             auto chunk = [&](auto slow) {
@@ -242,37 +340,17 @@ __global__ void __launch_bounds__(NT) bb_backward_kernel(const float* __restrict
             chunk(std::false_type{});
             if (__syncthreads_or(maxabs > kSinCosFastMax)) chunk(std::true_type{});
             if (kNS >= 1) aff_orthonormalize(M);
-            block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
-            carry = load_aff(s_total);
+            block_exclusive_scan<NT, kNS>(M, carryA, scratch, s_total);
+            carryA = load_aff(s_total);
             if (tid < 12) pref[(t + 1) * 12 + tid] = s_total[tid];
+            __syncthreads();  // the prefix is read by the tile's phase-B item
+            it = nx;
+            continue;
         }
-        __syncthreads();
-    }
 
-    // ---- phase B: tiles last to first
-    float carry6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    float omega_next = 0.f;  // dL/d omega of the tile's last residue (from the later tile)
-    for (int t = n_tiles - 1; t >= 0; --t) {
-        const int r0 = t * TILE;
-        const int n = min(TILE, L - r0);
-        const int pre = r0 > 0 ? 1 : 0;
+        // ---- phase B
         const Aff carry = (t == 0) ? aff_identity() : load_aff(pref + t * 12);
-        const Span sa = make_span(angles + ((size_t)b * Lmax + r0 - pre) * 3, (n + pre) * 12);
-        const Span sg = make_span(grad_coords + ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3, n * 36);
-        if (tid == 0) {
-            bulk_wait_read_all();
-            mbar_arrive_expect_tx(bar, unsigned(sa.mid + sg.mid));
-            span_load_bulk(sa, s_ang_base, bar);
-            span_load_bulk(sg, s_g_base, bar);
-        }
-        span_load_edges_f32(sa, s_ang_base);
-        span_load_edges_f32(sg, s_g_base);
-        mbar_wait(bar, phase);
-        phase ^= 1u;
-        __syncthreads();
-        const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 3 * pre;
         float* s_g = reinterpret_cast<float*>(s_g_base + sg.mis());
-        const int nq = max(0, min(RPT, n - rl0));
 
         // pass 1: local chunk; positions and rotation axes stay in registers
         constexpr int APT = 3 * RPT;
@@ -304,6 +382,7 @@ __global__ void __launch_bounds__(NT) bb_backward_kernel(const float* __restrict
         pass1(std::false_type{});
         if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
         if (kNS >= 1) aff_orthonormalize(M);
+        if (tid == 0) bulk_wait_read_all();  // the gradient staging is free again
         const Aff P = block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
 
         // pass 2: gradients rotated into the chunk frame (g_loc = R^T g)
@@ -358,13 +437,13 @@ __global__ void __launch_bounds__(NT) bb_backward_kernel(const float* __restrict
                 const int j = r0 + rl;
                 float ga[3];
 #pragma unroll
-                for (int k = 2; k >= 0; --k) {
-                    const int a = 3 * q + k;
+                for (int kk = 2; kk >= 0; --kk) {
+                    const int a = 3 * q + kk;
                     const float x = px[a], y = py[a], z = pz[a];
                     const float c0 = su[3] - fmaf(y, su[2], -z * su[1]);
                     const float c1 = su[4] - fmaf(z, su[0], -x * su[2]);
                     const float c2 = su[5] - fmaf(x, su[1], -y * su[0]);
-                    ga[k] = fmaf(ex[a], c0, fmaf(ey[a], c1, ez[a] * c2));
+                    ga[kk] = fmaf(ex[a], c0, fmaf(ey[a], c1, ez[a] * c2));
                     su[0] += gx[a]; su[1] += gy[a]; su[2] += gz[a];
                     su[3] += fmaf(y, gz[a], -z * gy[a]);
                     su[4] += fmaf(z, gx[a], -x * gz[a]);
@@ -389,8 +468,9 @@ __global__ void __launch_bounds__(NT) bb_backward_kernel(const float* __restrict
         span_store_edges_f32(so, s_go_base);
         omega_next = s_misc[0];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) carry6[k] = tot6[k];
+        for (int q = 0; q < 6; ++q) carry6[q] = tot6[q];
         __syncthreads();
+        it = nx;
     }
     // Only the shared-memory source must outlive the CTA; grid completion (and the
     // dependent's griddepcontrol.wait) covers visibility of the global writes.
@@ -401,30 +481,30 @@ __global__ void __launch_bounds__(NT) bb_backward_kernel(const float* __restrict
 // Host-side launch helpers (called from capi.cu).
 
 // Launch shape: NT threads per chain, RPT residues per thread (tile NT*RPT).
-// Default NT = 128; TPL_BB_NT=64|256 selects the other variants (tuning).
 // Chains longer than the largest tile loop over tiles.
 struct BBShape {
     int nt, rpt;
 };
-static int bb_nt_env() {  // TPL_BB_NT=128|256 forces the block size (tuning); 0 = default
+static int bb_nt_env() {  // TPL_BB_NT=32|128|256 forces the block size (tuning); 0 = default
     static int v = -1;
     if (v < 0) {
         const char* e = std::getenv("TPL_BB_NT");
         const int x = e ? std::atoi(e) : 0;
-        v = (x == 128 || x == 256) ? x : 0;
+        v = (x == 32 || x == 128 || x == 256) ? x : 0;
     }
     return v;
 }
 // Odd residues-per-thread only: the per-thread strides 3*RPT (angles) and
 // 9*RPT (coordinates) in shared memory are then bank-conflict free.
-// Forward: 128 threads, RPT in {1,3,5,7} (tile <= 896).  Backward keeps 6
+// Forward: 128 threads, RPT in {1,3,5,7} (tile <= 896).  Backward keeps 9
 // floats per atom in registers: 256 threads, RPT in {1,3} (tile <= 768).
 static BBShape bb_shape(bool fwd, int Lmax) {
     int nt = bb_nt_env();
     if (!nt) nt = (fwd || Lmax > 128) ? (fwd ? 128 : 256) : 128;
-    static const int f128[4] = {1, 3, 5, 7}, f256[3] = {1, 3, 5}, b128[2] = {1, 3}, b256[2] = {1, 3};
-    const int* opts = fwd ? (nt == 256 ? f256 : f128) : (nt == 256 ? b256 : b128);
-    const int n = fwd ? (nt == 256 ? 3 : 4) : 2;
+    static const int f128[4] = {1, 3, 5, 7}, f256[3] = {1, 3, 5}, b128[2] = {1, 3}, b256[2] = {1, 3},
+                     w32[4] = {1, 3, 5, 7};
+    const int* opts = nt == 32 ? w32 : fwd ? (nt == 256 ? f256 : f128) : (nt == 256 ? b256 : b128);
+    const int n = nt == 32 ? (fwd ? 4 : 3) : fwd ? (nt == 256 ? 3 : 4) : 2;
     for (int i = 0; i < n; ++i)
         if (nt * opts[i] >= Lmax) return {nt, opts[i]};
     return {nt, opts[n - 1]};
@@ -438,12 +518,30 @@ int bb_tile_for(int Lmax) {  // backward tile: sizes the workspace's per-tile pr
 template <int NT>
 static size_t fwd_smem(int rpt) {
     const int tile = NT * rpt;
-    return BBSmem<NT>::kData + round16(16 + 12 * (tile + 1)) + round16(16 + 36 * tile);
+    return BBSmem<NT>::kData + 2 * round16(16 + 12 * (tile + 1)) + round16(16 + 36 * tile);
 }
 template <int NT>
 static size_t bwd_smem(int rpt) {
     const int tile = NT * rpt;
-    return BBSmem<NT>::kData + round16(16 + 12 * (tile + 1)) + round16(16 + 36 * tile) + round16(16 + 12 * tile);
+    return BBSmem<NT>::kData + 2 * round16(16 + 12 * (tile + 1)) + 2 * round16(16 + 36 * tile) +
+           round16(16 + 12 * tile);
+}
+
+// Persistent grid: at most the resident CTAs, never more than the chains.
+template <typename K>
+static int persistent_grid(K kernel, int nt, size_t smem, int B) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const long cap = long(per_sm) * sms;
+    return int(B < cap ? B : cap);
 }
 
 template <int NT, int RPT, int NS>
@@ -451,24 +549,30 @@ static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
     auto k = bb_forward_kernel<NT, RPT, NS>;
     const size_t sm = fwd_smem<NT>(RPT);
     static size_t configured = 0;  // set the smem opt-in once per instance (not inside graph capture)
+    static int grid_cap = 0;
     if (configured < sm) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
         configured = sm;
+        grid_cap = persistent_grid(k, NT, sm, 1 << 30);
     }
-    return launch_pdl(k, a.B, NT, sm, st, a.angles, a.lengths, a.Lmax, a.coords, a.err);
+    const int grid = a.B < grid_cap ? a.B : grid_cap;
+    return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err);
 }
 template <int NT, int RPT, int NS>
 static cudaError_t launch_bwd(const BBArgs& a, cudaStream_t st) {
     auto k = bb_backward_kernel<NT, RPT, NS>;
     const size_t sm = bwd_smem<NT>(RPT);
     static size_t configured = 0;
+    static int grid_cap = 0;
     if (configured < sm) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
         configured = sm;
+        grid_cap = persistent_grid(k, NT, sm, 1 << 30);
     }
-    return launch_pdl(k, a.B, NT, sm, st, a.angles, a.lengths, a.Lmax, a.grad_coords, a.grad_angles, a.err,
+    const int grid = a.B < grid_cap ? a.B : grid_cap;
+    return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.grad_coords, a.grad_angles, a.err,
                       a.ws_prefix, a.max_tiles);
 }
 
@@ -478,12 +582,14 @@ static cudaError_t dispatch(const BBArgs& a, cudaStream_t st) {
     if (kFwd) {
 #define TPL_BB_FWD(NT_, R_) \
     if (s.nt == NT_ && s.rpt == R_) return launch_fwd<NT_, R_, NS>(a, st);
+        TPL_BB_FWD(32, 1) TPL_BB_FWD(32, 3) TPL_BB_FWD(32, 5) TPL_BB_FWD(32, 7)
         TPL_BB_FWD(128, 1) TPL_BB_FWD(128, 3) TPL_BB_FWD(128, 5) TPL_BB_FWD(128, 7)
         TPL_BB_FWD(256, 1) TPL_BB_FWD(256, 3) TPL_BB_FWD(256, 5)
 #undef TPL_BB_FWD
     } else {
 #define TPL_BB_BWD(NT_, R_) \
     if (s.nt == NT_ && s.rpt == R_) return launch_bwd<NT_, R_, NS>(a, st);
+        TPL_BB_BWD(32, 1) TPL_BB_BWD(32, 3) TPL_BB_BWD(32, 5)
         TPL_BB_BWD(128, 1) TPL_BB_BWD(128, 3) TPL_BB_BWD(256, 1) TPL_BB_BWD(256, 3)
 #undef TPL_BB_BWD
     }

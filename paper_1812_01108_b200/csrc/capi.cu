@@ -108,6 +108,7 @@ struct tpl_tables {
     FAType* dev = nullptr;
     int n_types = 0;
     int atoms[TPL_MAX_TYPES] = {0};
+    int max_atoms = 0;
     int device = 0;
 };
 
@@ -292,6 +293,7 @@ tpl_status tpl_tables_create(const tpl_residue_desc* types, int32_t n_types, tpl
             next = h.g[g].end_atom;
         }
         T->atoms[t] = d.n_atoms;
+        if (d.n_atoms > T->max_atoms) T->max_atoms = d.n_atoms;
     }
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -374,6 +376,7 @@ static FAArgs fa_args(const tpl_tables* T, const float* angles, const uint8_t* r
     a.ws_prefix = reinterpret_cast<float*>(static_cast<char*>(ws) + kWsHeader);
     a.max_tiles = max_tiles_for(TPL_MODEL_FULLATOM, Lmax);
     a.ns = ns_policy();
+    a.max_atoms = T->max_atoms > 0 ? T->max_atoms : 1;
     a.K = backbone_constants();
     return a;
 }

@@ -96,7 +96,7 @@ __device__ __forceinline__ void fa_chunk(const float* s_ang, int rl0, int r0, in
 }
 
 template <int NT, int RPT, int kNS>
-__global__ void __launch_bounds__(NT) fa_forward_kernel(FAArgs a, int stage_atoms_per_res) {
+__global__ void __launch_bounds__(NT, 2) fa_forward_kernel(FAArgs a, int stage_atoms_per_res) {
     constexpr int TILE = NT * RPT;
     using S = FASmem<NT>;
     using Lay = FALayout<NT, RPT>;
@@ -113,22 +113,26 @@ __global__ void __launch_bounds__(NT) fa_forward_kernel(FAArgs a, int stage_atom
 
     const int b = blockIdx.x;
     const int tid = threadIdx.x;
-    const int L = a.lengths[b];
-    if (L < 1 || L > a.Lmax) {
-        if (tid == 0) atomicOr(a.err, ERR_LENGTH);
-        return;
-    }
     unsigned phase = 0;
     if (tid == 0) {
         mbar_init(bar, 1);
         fence_barrier_init();
+        // the residue table is immutable after tpl_tables_create: it may be
+        // fetched before pdl_wait, overlapping the previous kernel's tail
         const unsigned tb = unsigned(a.n_types * sizeof(FAType));
         mbar_arrive_expect_tx(bar, tb);
         bulk_g2s(smem + S::kTable, a.types, tb, bar);
     }
+    pdl_wait();
+    pdl_trigger();
+    const int L = a.lengths[b];
     __syncthreads();
-    mbar_wait(bar, phase);
+    mbar_wait(bar, phase);  // also before any early exit: no bulk copy may outlive the CTA
     phase ^= 1u;
+    if (L < 1 || L > a.Lmax) {
+        if (tid == 0) atomicOr(a.err, ERR_LENGTH);
+        return;
+    }
 
     Aff carry = aff_identity();
     int carry_atoms = 0;
@@ -308,7 +312,7 @@ __device__ __forceinline__ void fa_residue_backward(const FAType& T, const float
 }
 
 template <int NT, int RPT, int kNS>
-__global__ void __launch_bounds__(NT) fa_backward_kernel(FAArgs a, int stage_atoms_per_res) {
+__global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_atoms_per_res) {
     constexpr int TILE = NT * RPT;
     using S = FASmem<NT>;
     using Lay = FALayout<NT, RPT>;
@@ -327,22 +331,26 @@ __global__ void __launch_bounds__(NT) fa_backward_kernel(FAArgs a, int stage_ato
 
     const int b = blockIdx.x;
     const int tid = threadIdx.x;
-    const int L = a.lengths[b];
-    if (L < 1 || L > a.Lmax) {
-        if (tid == 0) atomicOr(a.err, ERR_LENGTH);
-        return;
-    }
     unsigned phase = 0;
     if (tid == 0) {
         mbar_init(bar, 1);
         fence_barrier_init();
+        // the residue table is immutable after tpl_tables_create: it may be
+        // fetched before pdl_wait, overlapping the previous kernel's tail
         const unsigned tb = unsigned(a.n_types * sizeof(FAType));
         mbar_arrive_expect_tx(bar, tb);
         bulk_g2s(smem + S::kTable, a.types, tb, bar);
     }
+    pdl_wait();
+    pdl_trigger();
+    const int L = a.lengths[b];
     __syncthreads();
-    mbar_wait(bar, phase);
+    mbar_wait(bar, phase);  // also before any early exit: no bulk copy may outlive the CTA
     phase ^= 1u;
+    if (L < 1 || L > a.Lmax) {
+        if (tid == 0) atomicOr(a.err, ERR_LENGTH);
+        return;
+    }
 
     const int n_tiles = (L + TILE - 1) / TILE;
     const int rl0 = tid * RPT;
@@ -569,62 +577,58 @@ __global__ void __launch_bounds__(NT) fa_backward_kernel(FAArgs a, int stage_ato
 }
 
 // ---------------------------------------------------------------------------
-int fa_rpt_for(int Lmax) { return Lmax > kFAThreads ? 2 : 1; }
-int fa_tile_for(int Lmax) { return kFAThreads * fa_rpt_for(Lmax); }
+// One residue per thread; 256-thread forward CTAs, 128-thread backward CTAs
+// (the backward keeps more per-residue state: <= 170 registers, 3 CTAs/SM).
+// Chains longer than a tile loop over tiles.  The atom staging buffer is sized
+// by the table's largest residue type (FAArgs.max_atoms).
+constexpr int kFAFwdThreads = 256, kFAFwdRPT = 1;
+constexpr int kFABwdThreads = 128, kFABwdRPT = 1;
+int fa_rpt_for(int) { return kFABwdRPT; }
+int fa_tile_for(int) { return kFABwdThreads * kFABwdRPT; }  // backward tile: sizes the workspace prefixes
 
-static int max_atoms_per_res_host() { return kMaxAtomsPerRes; }
-
-template <int RPT>
-static size_t fa_fwd_smem(int n_types) {
-    using S = FASmem<kFAThreads>;
-    using Lay = FALayout<kFAThreads, RPT>;
+template <int NT, int RPT>
+static size_t fa_fwd_smem(int n_types, int max_atoms) {
+    using S = FASmem<NT>;
+    using Lay = FALayout<NT, RPT>;
     return S::kTable + r16(n_types * int(sizeof(FAType))) + Lay::ang_bytes + Lay::rt_bytes +
-           r16(16 + 12 * max_atoms_per_res_host() * Lay::TILE);
+           r16(16 + 12 * max_atoms * Lay::TILE);
 }
-template <int RPT>
-static size_t fa_bwd_smem(int n_types) {
-    using Lay = FALayout<kFAThreads, RPT>;
-    return fa_fwd_smem<RPT>(n_types) + Lay::go_bytes;
+template <int NT, int RPT>
+static size_t fa_bwd_smem(int n_types, int max_atoms) {
+    using Lay = FALayout<NT, RPT>;
+    return fa_fwd_smem<NT, RPT>(n_types, max_atoms) + Lay::go_bytes;
 }
 
-template <int RPT, int O>
+template <int NS>
 static cudaError_t fa_fwd(const FAArgs& a, cudaStream_t st) {
-    auto k = fa_forward_kernel<kFAThreads, RPT, O>;
-    const size_t sm = fa_fwd_smem<RPT>(a.n_types);
-    static size_t configured = 0;  // set the smem opt-in once per instance (not inside graph capture)
+    auto k = fa_forward_kernel<kFAFwdThreads, kFAFwdRPT, NS>;
+    const size_t sm = fa_fwd_smem<kFAFwdThreads, kFAFwdRPT>(a.n_types, a.max_atoms);
+    static size_t configured = 0;  // set the smem opt-in once per size (not inside graph capture)
     if (configured < sm) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
         configured = sm;
     }
-    k<<<a.B, kFAThreads, sm, st>>>(a, kMaxAtomsPerRes);
-    return cudaGetLastError();
+    return launch_pdl(k, a.B, kFAFwdThreads, sm, st, a, a.max_atoms);
 }
-template <int RPT, int O>
+template <int NS>
 static cudaError_t fa_bwd(const FAArgs& a, cudaStream_t st) {
-    auto k = fa_backward_kernel<kFAThreads, RPT, O>;
-    const size_t sm = fa_bwd_smem<RPT>(a.n_types);
-    static size_t configured = 0;  // set the smem opt-in once per instance (not inside graph capture)
+    auto k = fa_backward_kernel<kFABwdThreads, kFABwdRPT, NS>;
+    const size_t sm = fa_bwd_smem<kFABwdThreads, kFABwdRPT>(a.n_types, a.max_atoms);
+    static size_t configured = 0;
     if (configured < sm) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
         configured = sm;
     }
-    k<<<a.B, kFAThreads, sm, st>>>(a, kMaxAtomsPerRes);
-    return cudaGetLastError();
+    return launch_pdl(k, a.B, kFABwdThreads, sm, st, a, a.max_atoms);
 }
 
 cudaError_t fa_forward_launch(const FAArgs& a, cudaStream_t st) {
-    const int r = fa_rpt_for(a.Lmax);
-    if (a.ns == 0) return r == 1 ? fa_fwd<1, 0>(a, st) : fa_fwd<2, 0>(a, st);
-    if (a.ns == 2) return r == 1 ? fa_fwd<1, 2>(a, st) : fa_fwd<2, 2>(a, st);
-    return r == 1 ? fa_fwd<1, 1>(a, st) : fa_fwd<2, 1>(a, st);
+    return a.ns == 0 ? fa_fwd<0>(a, st) : fa_fwd<1>(a, st);
 }
 cudaError_t fa_backward_launch(const FAArgs& a, cudaStream_t st) {
-    const int r = fa_rpt_for(a.Lmax);
-    if (a.ns == 0) return r == 1 ? fa_bwd<1, 0>(a, st) : fa_bwd<2, 0>(a, st);
-    if (a.ns == 2) return r == 1 ? fa_bwd<1, 2>(a, st) : fa_bwd<2, 2>(a, st);
-    return r == 1 ? fa_bwd<1, 1>(a, st) : fa_bwd<2, 1>(a, st);
+    return a.ns == 0 ? fa_bwd<0>(a, st) : fa_bwd<1>(a, st);
 }
 
 }  // namespace tpl

@@ -12,7 +12,6 @@ struct BondC {
 };
 
 constexpr int kBBThreads = 128;
-constexpr int kFAThreads = 256;
 constexpr int kMaxGroups = 8;
 constexpr int kMaxAtomsPerRes = 16;
 constexpr int kMaxTypes = 32;
@@ -87,6 +86,7 @@ struct FAArgs {
     float* ws_prefix;  // per chain per tile: 12 floats prefix + 1 int atom offset (stride 16)
     int max_tiles;
     int ns;
+    int max_atoms;  // largest atom count of a residue type in the table
     BBConst K;
 };
 
