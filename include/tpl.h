@@ -180,6 +180,30 @@ TPL_API tpl_status tpl_fullatom_backward(const tpl_tables* tables, const float* 
                                  const float* grad_coords, float* grad_angles, void* workspace, size_t ws_bytes,
                                  void* stream);
 
+/* ======================================================================
+ * LRMSD loss (§4): Coutsias-Seok-Dill quaternion method
+ * ====================================================================== */
+
+/* Per chain b: barycentres, R = sum x~ y~^T, the 4x4 T as printed, its largest
+ * eigenpair (lambda, q), U(q) as printed, LRMSD = sqrt((sum|x~|^2+|y~|^2 - 2 lambda)/N).
+ * x is the structure that is differentiated, y the reference (reading Q19).
+ *   x, y     [B][stride][3] fp32 device (e.g. packed full-atom or backbone coords)
+ *   n_atoms  [B] int32 device, each in [1, stride]; atoms past n_atoms[b] are ignored
+ *   lrmsd    [B] fp32 output
+ *   state    [B][16] fp32 output for the backward: U row-major, centroid of x,
+ *            centroid of y, 1/(N LRMSD) (0 where LRMSD == 0)
+ *   workspace: any tpl workspace (its error word flags bad n_atoms). */
+TPL_API tpl_status tpl_lrmsd_forward(const float* x, const float* y, const int32_t* n_atoms, int32_t B,
+                                     int32_t stride, float* lrmsd, float* state, void* workspace, size_t ws_bytes,
+                                     void* stream);
+
+/* grad_x[b][i] = grad_lrmsd[b] * (x~_i - U^T y~_i) / (N LRMSD): the printed
+ * gradient with its normalisation; 0 where LRMSD == 0.  Atoms past
+ * n_atoms[b] are not written. */
+TPL_API tpl_status tpl_lrmsd_backward(const float* x, const float* y, const int32_t* n_atoms, int32_t B,
+                                      int32_t stride, const float* state, const float* grad_lrmsd, float* grad_x,
+                                      void* workspace, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

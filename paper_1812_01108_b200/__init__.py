@@ -8,7 +8,8 @@ marshalling, autograd glue, batch sharding for multi-GPU runs).
 """
 from . import _abi
 from ._abi import TplError, lib
-from .api import BackboneFunction, FullAtomFunction, Tables, Workspace, backbone, default_workspace, fullatom
+from .api import (BackboneFunction, FullAtomFunction, LRMSDFunction, Tables, Workspace, backbone,
+                  default_workspace, fullatom, lrmsd)
 
 __all__ = ["TplError", "lib", "Tables", "Workspace", "backbone", "fullatom", "BackboneFunction",
-           "FullAtomFunction", "default_workspace", "_abi"]
+           "FullAtomFunction", "LRMSDFunction", "lrmsd", "default_workspace", "_abi"]

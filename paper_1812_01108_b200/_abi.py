@@ -29,6 +29,7 @@ EXPORTS = [
     "tpl_last_error", "tpl_abi_version", "tpl_workspace_bytes", "tpl_sync_status", "tpl_backbone_atoms",
     "tpl_backbone_forward", "tpl_backbone_backward", "tpl_tables_create", "tpl_tables_destroy",
     "tpl_tables_n_types", "tpl_fullatom_atoms", "tpl_fullatom_forward", "tpl_fullatom_backward",
+    "tpl_lrmsd_forward", "tpl_lrmsd_backward",
 ]
 
 
@@ -86,6 +87,10 @@ def _load():
     L.tpl_fullatom_forward.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, sz, vp]
     L.tpl_fullatom_backward.restype = ctypes.c_int
     L.tpl_fullatom_backward.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]
+    L.tpl_lrmsd_forward.restype = ctypes.c_int
+    L.tpl_lrmsd_forward.argtypes = [vp, vp, vp, i32, i32, vp, vp, vp, sz, vp]
+    L.tpl_lrmsd_backward.restype = ctypes.c_int
+    L.tpl_lrmsd_backward.argtypes = [vp, vp, vp, i32, i32, vp, vp, vp, vp, sz, vp]
     return L
 
 
@@ -197,3 +202,23 @@ def tpl_fullatom_backward(handle, angles, restype, lengths, grad_coords, grad_an
                                      B, Lmax, grad_coords.shape[1], _dev(grad_coords, torch.float32, "grad_coords"),
                                      _dev(grad_angles, torch.float32, "grad_angles"),
                                      _dev(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream)))
+
+
+def tpl_lrmsd_forward(x, y, n_atoms, lrmsd, state, workspace, stream=None):
+    B, S, three = x.shape
+    if three != 3 or tuple(y.shape) != (B, S, 3) or tuple(lrmsd.shape) != (B,) or tuple(state.shape) != (B, 16):
+        raise ValueError("shapes: x, y [B,stride,3], n_atoms [B], lrmsd [B], state [B,16]")
+    _check(lib.tpl_lrmsd_forward(_dev(x, torch.float32, "x"), _dev(y, torch.float32, "y"),
+                                 _dev(n_atoms, torch.int32, "n_atoms"), B, S, _dev(lrmsd, torch.float32, "lrmsd"),
+                                 _dev(state, torch.float32, "state"), _dev(workspace, torch.uint8, "workspace"),
+                                 workspace.numel(), _stream(stream)))
+
+
+def tpl_lrmsd_backward(x, y, n_atoms, state, grad_lrmsd, grad_x, workspace, stream=None):
+    B, S, three = x.shape
+    if three != 3 or tuple(grad_x.shape) != (B, S, 3) or tuple(grad_lrmsd.shape) != (B,):
+        raise ValueError("shapes: x, y, grad_x [B,stride,3], grad_lrmsd [B], state [B,16]")
+    _check(lib.tpl_lrmsd_backward(_dev(x, torch.float32, "x"), _dev(y, torch.float32, "y"),
+                                  _dev(n_atoms, torch.int32, "n_atoms"), B, S, _dev(state, torch.float32, "state"),
+                                  _dev(grad_lrmsd, torch.float32, "grad_lrmsd"), _dev(grad_x, torch.float32, "grad_x"),
+                                  _dev(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream)))

@@ -158,3 +158,34 @@ def fullatom(angles, restype, lengths, tables, atom_stride=None):
     if atom_stride is None:
         _, atom_stride = tables.atoms(restype, lengths)
     return FullAtomFunction.apply(angles, restype, lengths, tables, int(atom_stride))
+
+
+class LRMSDFunction(torch.autograd.Function):
+    """LRMSD (PAPER §4) per chain between x (differentiated) and the reference y."""
+
+    @staticmethod
+    def forward(ctx, x, y, n_atoms):
+        x, y = x.contiguous(), y.contiguous()
+        B = x.shape[0]
+        out = torch.empty(B, dtype=torch.float32, device=x.device)
+        state = torch.empty(B, 16, dtype=torch.float32, device=x.device)
+        ws = default_workspace(x.device).buf
+        _abi.tpl_lrmsd_forward(x, y, n_atoms, out, state, ws)
+        ctx.save_for_backward(x, y, n_atoms, state)
+        ctx.mark_non_differentiable(n_atoms)
+        return out
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        x, y, n_atoms, state = ctx.saved_tensors
+        grad_x = torch.zeros_like(x)
+        ws = default_workspace(x.device).buf
+        _abi.tpl_lrmsd_backward(x, y, n_atoms, state, grad_out.contiguous(), grad_x, ws)
+        return grad_x, None, None
+
+
+def lrmsd(x, y, n_atoms=None):
+    """x, y [B, stride, 3] fp32 CUDA -> LRMSD [B]; differentiable in x."""
+    if n_atoms is None:
+        n_atoms = torch.full((x.shape[0],), x.shape[1], dtype=torch.int32, device=x.device)
+    return LRMSDFunction.apply(x, y.to(x.device), n_atoms.to(device=x.device, dtype=torch.int32).contiguous())

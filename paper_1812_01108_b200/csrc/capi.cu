@@ -411,4 +411,55 @@ tpl_status tpl_fullatom_backward(const tpl_tables* T, const float* angles, const
     return TPL_OK;
 }
 
+// ---------------------------------------------------------------- LRMSD
+static tpl_status lr_common(const float* x, const float* y, const int32_t* n_atoms, int32_t B, int32_t stride,
+                            void* ws, size_t ws_bytes) {
+    if (!x || !y || !n_atoms) return fail(TPL_ERR_NULL, "x/y/n_atoms is NULL");
+    if (B < 1 || stride < 1) return fail(TPL_ERR_SHAPE, "B=%d stride=%d must be >= 1", B, stride);
+    if (!aligned4(x) || !aligned4(y) || !aligned4(n_atoms)) return fail(TPL_ERR_ALIGN, "inputs not 4-byte aligned");
+    if (!ws) return fail(TPL_ERR_WORKSPACE, "workspace is NULL");
+    if (ws_bytes < kWsHeader) return fail(TPL_ERR_WORKSPACE, "workspace %zu bytes < %zu", ws_bytes, kWsHeader);
+    return TPL_OK;
+}
+
+tpl_status tpl_lrmsd_forward(const float* x, const float* y, const int32_t* n_atoms, int32_t B, int32_t stride,
+                             float* lrmsd, float* state, void* workspace, size_t ws_bytes, void* stream) {
+    tpl_status s = lr_common(x, y, n_atoms, B, stride, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!lrmsd || !state) return fail(TPL_ERR_NULL, "lrmsd/state is NULL");
+    LRArgs a{};
+    a.x = x;
+    a.y = y;
+    a.n_atoms = n_atoms;
+    a.B = B;
+    a.stride = stride;
+    a.out = lrmsd;
+    a.state = state;
+    a.err = static_cast<unsigned*>(workspace);
+    cudaError_t e = lrmsd_forward_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "lrmsd forward launch");
+    return TPL_OK;
+}
+
+tpl_status tpl_lrmsd_backward(const float* x, const float* y, const int32_t* n_atoms, int32_t B, int32_t stride,
+                              const float* state, const float* grad_lrmsd, float* grad_x, void* workspace,
+                              size_t ws_bytes, void* stream) {
+    tpl_status s = lr_common(x, y, n_atoms, B, stride, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!state || !grad_lrmsd || !grad_x) return fail(TPL_ERR_NULL, "state/grad_lrmsd/grad_x is NULL");
+    LRArgs a{};
+    a.x = x;
+    a.y = y;
+    a.n_atoms = n_atoms;
+    a.B = B;
+    a.stride = stride;
+    a.state = const_cast<float*>(state);
+    a.grad_out = grad_lrmsd;
+    a.grad_x = grad_x;
+    a.err = static_cast<unsigned*>(workspace);
+    cudaError_t e = lrmsd_backward_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "lrmsd backward launch");
+    return TPL_OK;
+}
+
 }  // extern "C"

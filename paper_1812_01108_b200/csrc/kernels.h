@@ -90,6 +90,21 @@ struct FAArgs {
     BBConst K;
 };
 
+// ---- LRMSD (PAPER §4) ------------------------------------------------------
+struct LRArgs {
+    const float* x;  // [B][stride][3], differentiated structure
+    const float* y;  // [B][stride][3], reference
+    const int* n_atoms;
+    int B, stride;
+    float* out;    // [B] LRMSD
+    float* state;  // [B][16]: U (9), centroid x (3), centroid y (3), 1/(N LRMSD)
+    const float* grad_out;  // [B] dL/dLRMSD
+    float* grad_x;          // [B][stride][3]
+    unsigned* err;
+};
+cudaError_t lrmsd_forward_launch(const LRArgs& a, cudaStream_t st);
+cudaError_t lrmsd_backward_launch(const LRArgs& a, cudaStream_t st);
+
 int fa_rpt_for(int Lmax);
 int fa_tile_for(int Lmax);
 cudaError_t fa_forward_launch(const FAArgs& a, cudaStream_t st);
