@@ -156,7 +156,6 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
         fence_barrier_init();
     }
     pdl_wait();
-    pdl_trigger();
     BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), true, err};
     it.init();
     TPL_STAMP(1);
@@ -218,6 +217,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
         TPL_STAMP(4);
         const Aff P = block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
         carry = load_aff(s_total);
+        // Let the next kernel launch only now: dependents launched earlier sit on
+        // SM resources while waiting and slowed alternating fwd/bwd by ~3 us.
+        if (!nx.valid) pdl_trigger();
         TPL_STAMP(5);
 
         // ---- pass 2: chunk prefix applied, positions to the output staging buffer
@@ -278,7 +280,6 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
         fence_barrier_init();
     }
     pdl_wait();
-    pdl_trigger();
     BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), false, err};
     it.init();
     __syncthreads();
@@ -413,6 +414,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
         sum6[5] = fmaf(P.r20, sl[3], fmaf(P.r21, sl[4], P.r22 * sl[5])) + fmaf(P.t0, sum6[1], -P.t1 * sum6[0]);
         float suf[6], tot6[6];
         block_exclusive_suffix6<NT>(sum6, carry6, s_suf, suf, tot6);
+        if (!nx.valid) pdl_trigger();  // late trigger (see the forward kernel)
         // later atoms into the chunk frame: S_l = R^T S, T_l = R^T (T - t x S)
         float su[6];
         {

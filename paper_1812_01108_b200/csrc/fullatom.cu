@@ -123,8 +123,7 @@ __global__ void __launch_bounds__(NT, 2) fa_forward_kernel(FAArgs a, int stage_a
         mbar_arrive_expect_tx(bar, tb);
         bulk_g2s(smem + S::kTable, a.types, tb, bar);
     }
-    pdl_wait();
-    pdl_trigger();
+    pdl_wait();  // the dependent launches when this grid exits (early triggers cost SM slots)
     const int L = a.lengths[b];
     __syncthreads();
     mbar_wait(bar, phase);  // also before any early exit: no bulk copy may outlive the CTA
@@ -341,8 +340,7 @@ __global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_
         mbar_arrive_expect_tx(bar, tb);
         bulk_g2s(smem + S::kTable, a.types, tb, bar);
     }
-    pdl_wait();
-    pdl_trigger();
+    pdl_wait();  // the dependent launches when this grid exits (early triggers cost SM slots)
     const int L = a.lengths[b];
     __syncthreads();
     mbar_wait(bar, phase);  // also before any early exit: no bulk copy may outlive the CTA

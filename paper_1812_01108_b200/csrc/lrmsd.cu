@@ -83,7 +83,6 @@ __global__ void __launch_bounds__(kLRThreads) lrmsd_forward_kernel(const float* 
                                                                    unsigned* __restrict__ err) {
     __shared__ double s_red[kLRThreads / 32][17];
     pdl_wait();
-    pdl_trigger();
     const int b = blockIdx.x;
     const int N = n_atoms[b];
     if (N < 1 || N > stride) {
@@ -158,7 +157,6 @@ __global__ void __launch_bounds__(kLRThreads) lrmsd_backward_kernel(const float*
                                                                     float* __restrict__ grad_x,
                                                                     unsigned* __restrict__ err) {
     pdl_wait();
-    pdl_trigger();
     const int b = blockIdx.y;
     const int N = n_atoms[b];
     if (N < 1 || N > stride) {
