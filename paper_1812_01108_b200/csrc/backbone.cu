@@ -70,6 +70,7 @@ struct BBIter {
     int B, Lmax, tile, stride;
     bool fwd;
     unsigned* err;
+    bool skipA;        // backward with forward checkpoints: no phase A
     int b, L, bn, Ln;  // current chain and the next one
     int t, nt, phase;  // tile, tiles in chain, 0 = fwd/phase A, 1 = phase B
     bool valid;
@@ -89,8 +90,8 @@ struct BBIter {
         valid = b < B;
         if (!valid) return;
         nt = (L + tile - 1) / tile;
-        t = 0;
-        phase = (fwd || nt == 1) ? (fwd ? 0 : 1) : 0;
+        phase = fwd ? 0 : ((nt == 1 || skipA) ? 1 : 0);
+        t = (!fwd && phase == 1) ? nt - 1 : 0;
     }
     __device__ void init() {
         b = blockIdx.x;
@@ -134,10 +135,19 @@ __device__ __forceinline__ void bb_issue(const BBIter& it, const float* angles, 
     if (with_g) span_load_bulk(sg, s_g, bar);
 }
 
-template <int NT, int RPT, int kNS>
+// Checkpoints (optional, kCk): the global prefix transform at every 3-residue
+// boundary, i.e. M_{3j-1} for j = 0, 3, 6, ... (identity for j = 0), 12 floats
+// each: [B][ceil(Lmax/3)][12].  With RPT = 3 a thread's chunk starts exactly at
+// such a boundary, so the checkpoint is the thread's scan result P.  The
+// backward reads them instead of re-running the prefix scan.
+constexpr int kCkptRes = 3;
+
+template <int NT, int RPT, int kNS, bool kCk>
 __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(const float* __restrict__ angles,
                                                         const int* __restrict__ lengths, int B, int Lmax,
-                                                        float* __restrict__ coords, unsigned* __restrict__ err) {
+                                                        float* __restrict__ coords, unsigned* __restrict__ err,
+                                                        float* __restrict__ ckpt) {
+    static_assert(!kCk || RPT == kCkptRes, "checkpoints need 3-residue chunks");
     constexpr int TILE = NT * RPT;
     constexpr int ANG = round16(16 + 12 * (TILE + 1));
     using S = BBSmem<NT>;
@@ -156,8 +166,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
         fence_barrier_init();
     }
     pdl_wait();
-    BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), true, err};
+    BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), true, err, false};
     it.init();
+    const int ck_stride = (Lmax + kCkptRes - 1) / kCkptRes;
     TPL_STAMP(1);
     __syncthreads();
     if (tid == 0 && it.valid) bb_issue(it, angles, nullptr, s_ang_buf, nullptr, bar);
@@ -220,6 +231,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
         // Let the next kernel launch only now: dependents launched earlier sit on
         // SM resources while waiting and slowed alternating fwd/bwd by ~3 us.
         if (!nx.valid) pdl_trigger();
+        if (kCk && rl0 < n) {
+            float4* d = reinterpret_cast<float4*>(ckpt + ((size_t)b * ck_stride + (r0 + rl0) / kCkptRes) * 12);
+            d[0] = make_float4(P.r00, P.r01, P.r02, P.t0);
+            d[1] = make_float4(P.r10, P.r11, P.r12, P.t1);
+            d[2] = make_float4(P.r20, P.r21, P.r22, P.t2);
+        }
         TPL_STAMP(5);
 
         // ---- pass 2: chunk prefix applied, positions to the output staging buffer
@@ -253,12 +270,17 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
     TPL_STAMP(9);
 }
 
-template <int NT, int RPT, int kNS>
+// kCk: the forward's checkpoints give every thread its chunk's global prefix,
+// so there is no phase A and no affine scan; pass 1 composes global positions
+// and axes directly and the sums stay in the global frame.
+template <int NT, int RPT, int kNS, bool kCk>
 __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(const float* __restrict__ angles,
                                                          const int* __restrict__ lengths, int B, int Lmax,
                                                          const float* __restrict__ grad_coords,
                                                          float* __restrict__ grad_angles, unsigned* __restrict__ err,
-                                                         float* __restrict__ ws_prefix, int max_tiles) {
+                                                         float* __restrict__ ws_prefix, int max_tiles,
+                                                         const float* __restrict__ ckpt) {
+    static_assert(!kCk || RPT == kCkptRes, "checkpoints need 3-residue chunks");
     constexpr int TILE = NT * RPT;
     constexpr int ANG = round16(16 + 12 * (TILE + 1));
     constexpr int GB = round16(16 + 36 * TILE);
@@ -280,8 +302,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
         fence_barrier_init();
     }
     pdl_wait();
-    BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), false, err};
+    BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), false, err, kCk};
     it.init();
+    const int ck_stride = (Lmax + kCkptRes - 1) / kCkptRes;
     __syncthreads();
     if (tid == 0 && it.valid) bb_issue(it, angles, grad_coords, s_ang_buf, s_g_buf, bar);
 
@@ -321,7 +344,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
         const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 3 * pre;
         const int nq = max(0, min(RPT, n - rl0));
 
-        if (!phaseB) {
+        if (!kCk && !phaseB) {
             // ---- phase A: chunk aggregates only; the tile total becomes the prefix of tile t+1
             Aff M;
             float maxabs = 0.f;
@@ -350,17 +373,22 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
         }
 
         // ---- phase B
-        const Aff carry = (t == 0) ? aff_identity() : load_aff(pref + t * 12);
         float* s_g = reinterpret_cast<float*>(s_g_base + sg.mis());
+        Aff M0 = aff_identity();  // start of the chunk: local frame, or the checkpointed global prefix
+        if (kCk && nq > 0) {
+            const float4* c4 = reinterpret_cast<const float4*>(ckpt + ((size_t)b * ck_stride + (r0 + rl0) / kCkptRes) * 12);
+            const float4 a0 = __ldg(c4), a1 = __ldg(c4 + 1), a2 = __ldg(c4 + 2);
+            M0 = Aff{a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+        }
 
-        // pass 1: local chunk; positions and rotation axes stay in registers
+        // pass 1: the chunk's positions and rotation axes stay in registers
         constexpr int APT = 3 * RPT;
         Aff M;
         float maxabs = 0.f;
         float px[APT], py[APT], pz[APT], ex[APT], ey[APT], ez[APT];
         auto pass1 = [&](auto slow) {
             constexpr bool kSlow = decltype(slow)::value;
-            M = aff_identity();
+            M = M0;
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
                 if (q < nq) {
@@ -382,11 +410,15 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
         };
         pass1(std::false_type{});
         if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
-        if (kNS >= 1) aff_orthonormalize(M);
         if (tid == 0) bulk_wait_read_all();  // the gradient staging is free again
-        const Aff P = block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
+        Aff P = aff_identity();
+        if (!kCk) {
+            const Aff carry = (t == 0) ? aff_identity() : load_aff(pref + t * 12);
+            if (kNS >= 1) aff_orthonormalize(M);
+            P = block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
+        }
 
-        // pass 2: gradients rotated into the chunk frame (g_loc = R^T g)
+        // pass 2: gradients into the chunk frame (g_loc = R^T g; the global frame under kCk)
         float sl[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         float gx[APT], gy[APT], gz[APT];
 #pragma unroll
@@ -395,9 +427,13 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
             if (a / 3 < nq) {
                 const float* g = s_g + 9 * rl0 + 3 * a;
                 const float g0 = g[0], g1 = g[1], g2 = g[2];
-                gx[a] = fmaf(P.r00, g0, fmaf(P.r10, g1, P.r20 * g2));
-                gy[a] = fmaf(P.r01, g0, fmaf(P.r11, g1, P.r21 * g2));
-                gz[a] = fmaf(P.r02, g0, fmaf(P.r12, g1, P.r22 * g2));
+                if (kCk) {
+                    gx[a] = g0; gy[a] = g1; gz[a] = g2;
+                } else {
+                    gx[a] = fmaf(P.r00, g0, fmaf(P.r10, g1, P.r20 * g2));
+                    gy[a] = fmaf(P.r01, g0, fmaf(P.r11, g1, P.r21 * g2));
+                    gz[a] = fmaf(P.r02, g0, fmaf(P.r12, g1, P.r22 * g2));
+                }
                 sl[0] += gx[a]; sl[1] += gy[a]; sl[2] += gz[a];
                 sl[3] += fmaf(py[a], gz[a], -pz[a] * gy[a]);
                 sl[4] += fmaf(pz[a], gx[a], -px[a] * gz[a]);
@@ -406,18 +442,26 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
         }
         // thread totals in the global frame: S = R S_l, T = R T_l + t x S
         float sum6[6];
-        sum6[0] = fmaf(P.r00, sl[0], fmaf(P.r01, sl[1], P.r02 * sl[2]));
-        sum6[1] = fmaf(P.r10, sl[0], fmaf(P.r11, sl[1], P.r12 * sl[2]));
-        sum6[2] = fmaf(P.r20, sl[0], fmaf(P.r21, sl[1], P.r22 * sl[2]));
-        sum6[3] = fmaf(P.r00, sl[3], fmaf(P.r01, sl[4], P.r02 * sl[5])) + fmaf(P.t1, sum6[2], -P.t2 * sum6[1]);
-        sum6[4] = fmaf(P.r10, sl[3], fmaf(P.r11, sl[4], P.r12 * sl[5])) + fmaf(P.t2, sum6[0], -P.t0 * sum6[2]);
-        sum6[5] = fmaf(P.r20, sl[3], fmaf(P.r21, sl[4], P.r22 * sl[5])) + fmaf(P.t0, sum6[1], -P.t1 * sum6[0]);
+        if (kCk) {
+#pragma unroll
+            for (int q = 0; q < 6; ++q) sum6[q] = sl[q];
+        } else {
+            sum6[0] = fmaf(P.r00, sl[0], fmaf(P.r01, sl[1], P.r02 * sl[2]));
+            sum6[1] = fmaf(P.r10, sl[0], fmaf(P.r11, sl[1], P.r12 * sl[2]));
+            sum6[2] = fmaf(P.r20, sl[0], fmaf(P.r21, sl[1], P.r22 * sl[2]));
+            sum6[3] = fmaf(P.r00, sl[3], fmaf(P.r01, sl[4], P.r02 * sl[5])) + fmaf(P.t1, sum6[2], -P.t2 * sum6[1]);
+            sum6[4] = fmaf(P.r10, sl[3], fmaf(P.r11, sl[4], P.r12 * sl[5])) + fmaf(P.t2, sum6[0], -P.t0 * sum6[2]);
+            sum6[5] = fmaf(P.r20, sl[3], fmaf(P.r21, sl[4], P.r22 * sl[5])) + fmaf(P.t0, sum6[1], -P.t1 * sum6[0]);
+        }
         float suf[6], tot6[6];
         block_exclusive_suffix6<NT>(sum6, carry6, s_suf, suf, tot6);
         if (!nx.valid) pdl_trigger();  // late trigger (see the forward kernel)
         // later atoms into the chunk frame: S_l = R^T S, T_l = R^T (T - t x S)
         float su[6];
-        {
+        if (kCk) {
+#pragma unroll
+            for (int q = 0; q < 6; ++q) su[q] = suf[q];
+        } else {
             const float w0 = suf[3] - fmaf(P.t1, suf[2], -P.t2 * suf[1]);
             const float w1 = suf[4] - fmaf(P.t2, suf[0], -P.t0 * suf[2]);
             const float w2 = suf[5] - fmaf(P.t0, suf[1], -P.t1 * suf[0]);
@@ -546,9 +590,9 @@ static int persistent_grid(K kernel, int nt, size_t smem, int B) {
     return int(B < cap ? B : cap);
 }
 
-template <int NT, int RPT, int NS>
+template <int NT, int RPT, int NS, bool CK>
 static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
-    auto k = bb_forward_kernel<NT, RPT, NS>;
+    auto k = bb_forward_kernel<NT, RPT, NS, CK>;
     const size_t sm = fwd_smem<NT>(RPT);
     static size_t configured = 0;  // set the smem opt-in once per instance (not inside graph capture)
     static int grid_cap = 0;
@@ -559,11 +603,11 @@ static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
         grid_cap = persistent_grid(k, NT, sm, 1 << 30);
     }
     const int grid = a.B < grid_cap ? a.B : grid_cap;
-    return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err);
+    return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err, a.ckpt);
 }
-template <int NT, int RPT, int NS>
+template <int NT, int RPT, int NS, bool CK>
 static cudaError_t launch_bwd(const BBArgs& a, cudaStream_t st) {
-    auto k = bb_backward_kernel<NT, RPT, NS>;
+    auto k = bb_backward_kernel<NT, RPT, NS, CK>;
     const size_t sm = bwd_smem<NT>(RPT);
     static size_t configured = 0;
     static int grid_cap = 0;
@@ -575,22 +619,34 @@ static cudaError_t launch_bwd(const BBArgs& a, cudaStream_t st) {
     }
     const int grid = a.B < grid_cap ? a.B : grid_cap;
     return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.grad_coords, a.grad_angles, a.err,
-                      a.ws_prefix, a.max_tiles);
+                      a.ws_prefix, a.max_tiles, static_cast<const float*>(a.ckpt));
+}
+
+// Checkpointed shape: 3 residues per thread (one checkpoint per thread chunk).
+static BBShape bb_ck_shape(int Lmax) {
+    int nt = bb_nt_env();
+    if (nt != 128 && nt != 256) nt = Lmax > 384 ? 256 : 128;
+    return {nt, kCkptRes};
 }
 
 template <bool kFwd, int NS>
 static cudaError_t dispatch(const BBArgs& a, cudaStream_t st) {
+    if (a.ckpt) {
+        const BBShape s = bb_ck_shape(a.Lmax);
+        if (kFwd) return s.nt == 256 ? launch_fwd<256, 3, NS, true>(a, st) : launch_fwd<128, 3, NS, true>(a, st);
+        return s.nt == 256 ? launch_bwd<256, 3, NS, true>(a, st) : launch_bwd<128, 3, NS, true>(a, st);
+    }
     const BBShape s = bb_shape(kFwd, a.Lmax);
     if (kFwd) {
 #define TPL_BB_FWD(NT_, R_) \
-    if (s.nt == NT_ && s.rpt == R_) return launch_fwd<NT_, R_, NS>(a, st);
+    if (s.nt == NT_ && s.rpt == R_) return launch_fwd<NT_, R_, NS, false>(a, st);
         TPL_BB_FWD(32, 1) TPL_BB_FWD(32, 3) TPL_BB_FWD(32, 5) TPL_BB_FWD(32, 7)
         TPL_BB_FWD(128, 1) TPL_BB_FWD(128, 3) TPL_BB_FWD(128, 5) TPL_BB_FWD(128, 7)
         TPL_BB_FWD(256, 1) TPL_BB_FWD(256, 3) TPL_BB_FWD(256, 5)
 #undef TPL_BB_FWD
     } else {
 #define TPL_BB_BWD(NT_, R_) \
-    if (s.nt == NT_ && s.rpt == R_) return launch_bwd<NT_, R_, NS>(a, st);
+    if (s.nt == NT_ && s.rpt == R_) return launch_bwd<NT_, R_, NS, false>(a, st);
         TPL_BB_BWD(32, 1) TPL_BB_BWD(32, 3) TPL_BB_BWD(32, 5)
         TPL_BB_BWD(128, 1) TPL_BB_BWD(128, 3) TPL_BB_BWD(256, 1) TPL_BB_BWD(256, 3)
 #undef TPL_BB_BWD

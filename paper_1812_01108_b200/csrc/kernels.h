@@ -41,6 +41,7 @@ struct BBArgs {
     int max_tiles;
     int ns;  // Newton-Schulz policy: 0 none, 1 prefix/total, 2 every combine
     BBConst K;
+    float* ckpt;  // optional per-3-residue prefix checkpoints [B][ceil(Lmax/3)][12] (nullptr: none)
 };
 
 bool pdl_enabled();  // capi.cu: programmatic dependent launch on (TPL_PDL != 0)

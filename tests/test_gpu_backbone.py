@@ -30,7 +30,7 @@ def tpl():
     return tpl
 
 
-def _run(tpl, ang, lengths, grad, sentinel=float("nan")):
+def _run(tpl, ang, lengths, grad, sentinel=float("nan"), ckpt=False):
     from paper_1812_01108_b200 import _abi
 
     B, Lmax, _ = ang.shape
@@ -40,8 +40,13 @@ def _run(tpl, ang, lengths, grad, sentinel=float("nan")):
     coords = torch.full((B, 3 * Lmax, 3), sentinel, device="cuda")
     gang = torch.full((B, Lmax, 3), sentinel, device="cuda")
     ws = torch.zeros(_abi.tpl_workspace_bytes(0, B, Lmax), dtype=torch.uint8, device="cuda")
-    _abi.tpl_backbone_forward(a, ln, coords, ws)
-    _abi.tpl_backbone_backward(a, ln, g, gang, ws)
+    if ckpt:
+        ck = torch.full((_abi.tpl_backbone_ckpt_floats(B, Lmax),), sentinel, device="cuda")
+        _abi.tpl_backbone_forward_ckpt(a, ln, coords, ck, ws)
+        _abi.tpl_backbone_backward_ckpt(a, ln, ck, g, gang, ws)
+    else:
+        _abi.tpl_backbone_forward(a, ln, coords, ws)
+        _abi.tpl_backbone_backward(a, ln, g, gang, ws)
     _abi.tpl_sync_status(ws)
     return coords.cpu().numpy(), gang.cpu().numpy()
 
@@ -114,6 +119,47 @@ def test_parity_ragged_tiles(tpl, oracle_lib, Lmax, lengths):
     # padding untouched (sentinel NaN survives)
     for b, L in enumerate(lengths):
         assert np.isnan(coords[b, 3 * L:]).all() and np.isnan(gang[b, L:]).all()
+
+
+@pytest.mark.parametrize("Lmax,lengths", [
+    (16, [16, 1, 2, 3, 4, 7]),                # chunk boundaries at 3 residues
+    (384, [384, 383, 129, 5]),                # 128-thread shape, one tile
+    (700, [700, 650, 512, 3]),                # 256-thread shape (metric config)
+    (2300, [2300, 2049, 769, 768, 767]),      # several tiles: suffix carry and omega across tiles
+])
+def test_ckpt_parity(tpl, oracle_lib, Lmax, lengths):
+    """Checkpointed pair (tpl_backbone_forward_ckpt / _backward_ckpt) against the oracle."""
+    B = len(lengths)
+    ang = synth.angles_uniform(B, Lmax, 3, 177 + Lmax)
+    grad = synth.grad_normal((B, 3 * Lmax, 3), 178 + Lmax)
+    ln = torch.tensor(lengths, dtype=torch.int32)
+    coords, gang = _run(tpl, ang, ln, grad, ckpt=True)
+    _check(oracle_lib, ang, ln, grad, coords, gang)
+    for b, L in enumerate(lengths):
+        assert np.isnan(coords[b, 3 * L:]).all() and np.isnan(gang[b, L:]).all()
+
+
+def test_ckpt_metric_sampled(tpl, oracle_lib):
+    ang, lengths, grad = synth.backbone_inputs("metric")
+    coords, gang = _run(tpl, ang, lengths, grad, ckpt=True)
+    sample = sorted(np.random.default_rng(3).choice(256, 16, replace=False).tolist())
+    _check(oracle_lib, ang, lengths, grad, coords, gang, chains=sample)
+
+
+def test_ckpt_errors(tpl):
+    from paper_1812_01108_b200 import TplError, _abi
+
+    ang = synth.angles_uniform(2, 10, 3, 5).cuda()
+    ln = torch.full((2,), 10, dtype=torch.int32, device="cuda")
+    coords = torch.zeros(2, 30, 3, device="cuda")
+    ws = torch.zeros(_abi.tpl_workspace_bytes(0, 2, 10), dtype=torch.uint8, device="cuda")
+    assert _abi.tpl_backbone_ckpt_floats(2, 10) == 2 * 4 * 12
+    ck = torch.zeros(2 * 4 * 12 + 4, device="cuda")
+    with pytest.raises(TplError) as e:  # misaligned by one float
+        _abi.tpl_backbone_forward_ckpt(ang, ln, coords, ck[1:97], ws)
+    assert e.value.status == 3
+    with pytest.raises(ValueError):
+        _abi.tpl_backbone_forward_ckpt(ang, ln, coords, ck, ws)
 
 
 def test_config2_full_parity(tpl, oracle_lib):
