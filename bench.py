@@ -36,6 +36,9 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 
 BYTES_PER_RES = {  # algorithmic bytes
+    # bwd: the operation's own bytes (angles + dL/dr in, dL/dangles out).  The kernel
+    # reads the forward's coordinates instead of the angles (36 B, not 12): moved
+    # bytes are 84/residue, but the roofline is charged the op's 60.
     "backbone": {"fwd": 12 + 36, "bwd": 12 + 36 + 12},
     "fullatom": {"fwd": None, "bwd": None},  # computed from the actual atom count
 }
@@ -203,7 +206,8 @@ class BackboneWork:
     def bwd(self, s, stream=None):
         from paper_1812_01108_b200 import _abi
 
-        _abi.tpl_backbone_backward(s["angles"], s["lengths"], s["grad"], s["gang"], s["ws"], stream)
+        # the autograd layer's backward: from the forward's coordinates
+        _abi.tpl_backbone_backward_from_coords(s["coords"], s["lengths"], s["grad"], s["gang"], s["ws"], stream)
 
     def algo_bytes(self):
         return {k: v * self.residues for k, v in BYTES_PER_RES["backbone"].items()}

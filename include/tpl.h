@@ -55,7 +55,7 @@ typedef enum {
     TPL_OK = 0,
     TPL_ERR_NULL = 1,         /* a required pointer is NULL */
     TPL_ERR_SHAPE = 2,        /* B < 1, Lmax < 1, atom_stride too small, ... */
-    TPL_ERR_ALIGN = 3,        /* a pointer is under-aligned (4 bytes; ckpt 16) */
+    TPL_ERR_ALIGN = 3,        /* a pointer is not 4-byte aligned */
     TPL_ERR_TABLE = 4,        /* residue-type table rejected */
     TPL_ERR_CUDA = 5,         /* a CUDA runtime call failed (see tpl_last_error) */
     TPL_ERR_DEVICE_INPUT = 6, /* a kernel flagged a bad length / restype */
@@ -123,20 +123,18 @@ TPL_API tpl_status tpl_backbone_backward(const float* angles, const int32_t* len
                                  const float* grad_coords, float* grad_angles, void* workspace, size_t ws_bytes,
                                  void* stream);
 
-/* Checkpointed pair.  The forward also stores the prefix transform
- * M_{3j-1} = R_0 ... R_{3j-1} (identity for j = 0) at every
- * residue j divisible by 3, which the backward reads instead of recomputing
- * the prefix of Eq. 2.  Same results as the plain pair up to fp32 rounding.
- *   ckpt  [B][ceil(Lmax/3)][12] fp32, row-major 3x4 [R | t], 16-byte aligned,
- *         caller-owned; written by the forward for j < lengths[b] only.  The
- *         backward must get the angles/lengths the forward saw.
- * tpl_backbone_ckpt_floats(B, Lmax) = B * ceil(Lmax/3) * 12 (0 for bad sizes). */
-TPL_API int64_t tpl_backbone_ckpt_floats(int32_t B, int32_t Lmax);
-TPL_API tpl_status tpl_backbone_forward_ckpt(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
-                                     float* coords, float* ckpt, void* workspace, size_t ws_bytes, void* stream);
-TPL_API tpl_status tpl_backbone_backward_ckpt(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
-                                      const float* ckpt, const float* grad_coords, float* grad_angles,
-                                      void* workspace, size_t ws_bytes, void* stream);
+/* Backward from the forward's output: the same dL/dangles computed from
+ * coords = tpl_backbone_forward(angles) instead of the angles.  Eq. 2's
+ * derivative dr_b/dalpha_a = e_a x (r_b - r_a) (b > a) needs only
+ * positions: the rotation axis e_a of transform a is the unit bond vector
+ * (r_a - r_{a-1}) / |r_a - r_{a-1}|.  No trig, no scan of
+ * transforms: one reverse suffix sum of (sum g, sum r x g) per chain.
+ *   coords      [B][3*Lmax][3] fp32, the forward's output for these lengths
+ *   grad_coords [B][3*Lmax][3] fp32
+ *   grad_angles [B][Lmax][3]   fp32 output; psi_{L-1} and omega_{L-1} are 0 */
+TPL_API tpl_status tpl_backbone_backward_from_coords(const float* coords, const int32_t* lengths, int32_t B,
+                                             int32_t Lmax, const float* grad_coords, float* grad_angles,
+                                             void* workspace, size_t ws_bytes, void* stream);
 
 /* ======================================================================
  * Full-atom model (§2)

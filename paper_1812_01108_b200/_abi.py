@@ -27,8 +27,7 @@ OWNER_N, OWNER_CA, OWNER_C = -3, -2, -1
 # Every symbol include/tpl.h declares (checked by tests/test_abi_cpu.py).
 EXPORTS = [
     "tpl_last_error", "tpl_abi_version", "tpl_workspace_bytes", "tpl_sync_status", "tpl_backbone_atoms",
-    "tpl_backbone_forward", "tpl_backbone_backward", "tpl_backbone_ckpt_floats", "tpl_backbone_forward_ckpt",
-    "tpl_backbone_backward_ckpt", "tpl_tables_create", "tpl_tables_destroy",
+    "tpl_backbone_forward", "tpl_backbone_backward", "tpl_backbone_backward_from_coords", "tpl_tables_create", "tpl_tables_destroy",
     "tpl_tables_n_types", "tpl_fullatom_atoms", "tpl_fullatom_forward", "tpl_fullatom_backward",
     "tpl_lrmsd_forward", "tpl_lrmsd_backward",
 ]
@@ -76,12 +75,8 @@ def _load():
     L.tpl_backbone_forward.argtypes = [vp, vp, i32, i32, vp, vp, sz, vp]
     L.tpl_backbone_backward.restype = ctypes.c_int
     L.tpl_backbone_backward.argtypes = [vp, vp, i32, i32, vp, vp, vp, sz, vp]
-    L.tpl_backbone_ckpt_floats.restype = i64
-    L.tpl_backbone_ckpt_floats.argtypes = [i32, i32]
-    L.tpl_backbone_forward_ckpt.restype = ctypes.c_int
-    L.tpl_backbone_forward_ckpt.argtypes = [vp, vp, i32, i32, vp, vp, vp, sz, vp]
-    L.tpl_backbone_backward_ckpt.restype = ctypes.c_int
-    L.tpl_backbone_backward_ckpt.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, sz, vp]
+    L.tpl_backbone_backward_from_coords.restype = ctypes.c_int
+    L.tpl_backbone_backward_from_coords.argtypes = [vp, vp, i32, i32, vp, vp, vp, sz, vp]
     L.tpl_tables_create.restype = ctypes.c_int
     L.tpl_tables_create.argtypes = [ctypes.POINTER(ResidueDesc), i32, ctypes.POINTER(vp)]
     L.tpl_tables_destroy.restype = None
@@ -162,39 +157,17 @@ def tpl_backbone_backward(angles, lengths, grad_coords, grad_angles, workspace, 
                                      _stream(stream)))
 
 
-def tpl_backbone_ckpt_floats(B, Lmax):
-    return int(lib.tpl_backbone_ckpt_floats(int(B), int(Lmax)))
-
-
-def _ckpt(ckpt, B, Lmax):
-    if ckpt.numel() != tpl_backbone_ckpt_floats(B, Lmax):
-        raise ValueError(f"ckpt must hold tpl_backbone_ckpt_floats(B, Lmax) = {tpl_backbone_ckpt_floats(B, Lmax)} "
-                         f"floats, got {ckpt.numel()}")
-    return _dev(ckpt, torch.float32, "ckpt")
-
-
-def tpl_backbone_forward_ckpt(angles, lengths, coords, ckpt, workspace, stream=None):
-    B, Lmax, three = angles.shape
-    if three != BB_SLOTS or tuple(coords.shape) != (B, 3 * Lmax, 3) or tuple(lengths.shape) != (B,):
-        raise ValueError("shapes: angles [B,Lmax,3], lengths [B], coords [B,3*Lmax,3]")
-    _check(lib.tpl_backbone_forward_ckpt(_dev(angles, torch.float32, "angles"),
-                                         _dev(lengths, torch.int32, "lengths"), B, Lmax,
-                                         _dev(coords, torch.float32, "coords"), _ckpt(ckpt, B, Lmax),
-                                         _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
-                                         _stream(stream)))
-
-
-def tpl_backbone_backward_ckpt(angles, lengths, ckpt, grad_coords, grad_angles, workspace, stream=None):
-    B, Lmax, three = angles.shape
-    if (three != BB_SLOTS or tuple(grad_coords.shape) != (B, 3 * Lmax, 3)
-            or tuple(grad_angles.shape) != (B, Lmax, 3) or tuple(lengths.shape) != (B,)):
-        raise ValueError("shapes: angles/grad_angles [B,Lmax,3], lengths [B], grad_coords [B,3*Lmax,3]")
-    _check(lib.tpl_backbone_backward_ckpt(_dev(angles, torch.float32, "angles"),
-                                          _dev(lengths, torch.int32, "lengths"), B, Lmax, _ckpt(ckpt, B, Lmax),
-                                          _dev(grad_coords, torch.float32, "grad_coords"),
-                                          _dev(grad_angles, torch.float32, "grad_angles"),
-                                          _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
-                                          _stream(stream)))
+def tpl_backbone_backward_from_coords(coords, lengths, grad_coords, grad_angles, workspace, stream=None):
+    B, Lmax, three = grad_angles.shape
+    if (three != BB_SLOTS or tuple(coords.shape) != (B, 3 * Lmax, 3) or tuple(grad_coords.shape) != (B, 3 * Lmax, 3)
+            or tuple(lengths.shape) != (B,)):
+        raise ValueError("shapes: coords/grad_coords [B,3*Lmax,3], lengths [B], grad_angles [B,Lmax,3]")
+    _check(lib.tpl_backbone_backward_from_coords(_dev(coords, torch.float32, "coords"),
+                                                 _dev(lengths, torch.int32, "lengths"), B, Lmax,
+                                                 _dev(grad_coords, torch.float32, "grad_coords"),
+                                                 _dev(grad_angles, torch.float32, "grad_angles"),
+                                                 _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                                 _stream(stream)))
 
 
 def tpl_tables_create(descs):

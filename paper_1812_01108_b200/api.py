@@ -108,17 +108,18 @@ class BackboneFunction(torch.autograd.Function):
         coords = torch.empty((B, 3 * Lmax, 3), dtype=torch.float32, device=angles.device)
         ws = default_workspace(angles.device).get(MODEL_BACKBONE, B, Lmax)
         _abi.tpl_backbone_forward(angles, lengths, coords, ws)
-        ctx.save_for_backward(angles, lengths)
+        # the backward needs only the output (rotation axes are bond vectors)
+        ctx.save_for_backward(coords, lengths)
         ctx.mark_non_differentiable(lengths)
         return coords
 
     @staticmethod
     def backward(ctx, grad_coords):
-        angles, lengths = ctx.saved_tensors
-        B, Lmax, _ = angles.shape
-        grad_angles = torch.zeros_like(angles)  # pads stay 0: the kernel never writes them
-        ws = default_workspace(angles.device).get(MODEL_BACKBONE, B, Lmax)
-        _abi.tpl_backbone_backward(angles, lengths, grad_coords.contiguous(), grad_angles, ws)
+        coords, lengths = ctx.saved_tensors
+        B, Lmax = coords.shape[0], coords.shape[1] // 3
+        grad_angles = torch.zeros((B, Lmax, 3), dtype=torch.float32, device=coords.device)  # pads stay 0
+        ws = default_workspace(coords.device).get(MODEL_BACKBONE, B, Lmax)
+        _abi.tpl_backbone_backward_from_coords(coords, lengths, grad_coords.contiguous(), grad_angles, ws)
         return grad_angles, None
 
 

@@ -24,6 +24,7 @@
 //   forward : every tile of every chain, first to last (prefix carried);
 //   backward: phase A = tile prefixes of all but the last tile (to the
 //             workspace), then phase B = tiles last to first (suffix carried).
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -70,7 +71,7 @@ struct BBIter {
     int B, Lmax, tile, stride;
     bool fwd;
     unsigned* err;
-    bool skipA;        // backward with forward checkpoints: no phase A
+    bool skipA;        // backward without phase A (the prefix is not needed)
     int b, L, bn, Ln;  // current chain and the next one
     int t, nt, phase;  // tile, tiles in chain, 0 = fwd/phase A, 1 = phase B
     bool valid;
@@ -135,19 +136,10 @@ __device__ __forceinline__ void bb_issue(const BBIter& it, const float* angles, 
     if (with_g) span_load_bulk(sg, s_g, bar);
 }
 
-// Checkpoints (optional, kCk): the global prefix transform at every 3-residue
-// boundary, i.e. M_{3j-1} for j = 0, 3, 6, ... (identity for j = 0), 12 floats
-// each: [B][ceil(Lmax/3)][12].  With RPT = 3 a thread's chunk starts exactly at
-// such a boundary, so the checkpoint is the thread's scan result P.  The
-// backward reads them instead of re-running the prefix scan.
-constexpr int kCkptRes = 3;
-
-template <int NT, int RPT, int kNS, bool kCk>
+template <int NT, int RPT, int kNS>
 __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(const float* __restrict__ angles,
                                                         const int* __restrict__ lengths, int B, int Lmax,
-                                                        float* __restrict__ coords, unsigned* __restrict__ err,
-                                                        float* __restrict__ ckpt) {
-    static_assert(!kCk || RPT == kCkptRes, "checkpoints need 3-residue chunks");
+                                                        float* __restrict__ coords, unsigned* __restrict__ err) {
     constexpr int TILE = NT * RPT;
     constexpr int ANG = round16(16 + 12 * (TILE + 1));
     using S = BBSmem<NT>;
@@ -168,7 +160,6 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
     pdl_wait();
     BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), true, err, false};
     it.init();
-    const int ck_stride = (Lmax + kCkptRes - 1) / kCkptRes;
     TPL_STAMP(1);
     __syncthreads();
     if (tid == 0 && it.valid) bb_issue(it, angles, nullptr, s_ang_buf, nullptr, bar);
@@ -231,12 +222,6 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
         // Let the next kernel launch only now: dependents launched earlier sit on
         // SM resources while waiting and slowed alternating fwd/bwd by ~3 us.
         if (!nx.valid) pdl_trigger();
-        if (kCk && rl0 < n) {
-            float4* d = reinterpret_cast<float4*>(ckpt + ((size_t)b * ck_stride + (r0 + rl0) / kCkptRes) * 12);
-            d[0] = make_float4(P.r00, P.r01, P.r02, P.t0);
-            d[1] = make_float4(P.r10, P.r11, P.r12, P.t1);
-            d[2] = make_float4(P.r20, P.r21, P.r22, P.t2);
-        }
         TPL_STAMP(5);
 
         // ---- pass 2: chunk prefix applied, positions to the output staging buffer
@@ -270,17 +255,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
     TPL_STAMP(9);
 }
 
-// kCk: the forward's checkpoints give every thread its chunk's global prefix,
-// so there is no phase A and no affine scan; pass 1 composes global positions
-// and axes directly and the sums stay in the global frame.
-template <int NT, int RPT, int kNS, bool kCk>
+template <int NT, int RPT, int kNS>
 __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(const float* __restrict__ angles,
                                                          const int* __restrict__ lengths, int B, int Lmax,
                                                          const float* __restrict__ grad_coords,
                                                          float* __restrict__ grad_angles, unsigned* __restrict__ err,
-                                                         float* __restrict__ ws_prefix, int max_tiles,
-                                                         const float* __restrict__ ckpt) {
-    static_assert(!kCk || RPT == kCkptRes, "checkpoints need 3-residue chunks");
+                                                         float* __restrict__ ws_prefix, int max_tiles) {
     constexpr int TILE = NT * RPT;
     constexpr int ANG = round16(16 + 12 * (TILE + 1));
     constexpr int GB = round16(16 + 36 * TILE);
@@ -302,9 +282,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
         fence_barrier_init();
     }
     pdl_wait();
-    BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), false, err, kCk};
+    BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), false, err, false};
     it.init();
-    const int ck_stride = (Lmax + kCkptRes - 1) / kCkptRes;
     __syncthreads();
     if (tid == 0 && it.valid) bb_issue(it, angles, grad_coords, s_ang_buf, s_g_buf, bar);
 
@@ -344,7 +323,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
         const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 3 * pre;
         const int nq = max(0, min(RPT, n - rl0));
 
-        if (!kCk && !phaseB) {
+        if (!phaseB) {
             // ---- phase A: chunk aggregates only; the tile total becomes the prefix of tile t+1
             Aff M;
             float maxabs = 0.f;
@@ -373,22 +352,17 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
         }
 
         // ---- phase B
+        const Aff carry = (t == 0) ? aff_identity() : load_aff(pref + t * 12);
         float* s_g = reinterpret_cast<float*>(s_g_base + sg.mis());
-        Aff M0 = aff_identity();  // start of the chunk: local frame, or the checkpointed global prefix
-        if (kCk && nq > 0) {
-            const float4* c4 = reinterpret_cast<const float4*>(ckpt + ((size_t)b * ck_stride + (r0 + rl0) / kCkptRes) * 12);
-            const float4 a0 = __ldg(c4), a1 = __ldg(c4 + 1), a2 = __ldg(c4 + 2);
-            M0 = Aff{a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
-        }
 
-        // pass 1: the chunk's positions and rotation axes stay in registers
+        // pass 1: local chunk; positions and rotation axes stay in registers
         constexpr int APT = 3 * RPT;
         Aff M;
         float maxabs = 0.f;
         float px[APT], py[APT], pz[APT], ex[APT], ey[APT], ez[APT];
         auto pass1 = [&](auto slow) {
             constexpr bool kSlow = decltype(slow)::value;
-            M = M0;
+            M = aff_identity();
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
                 if (q < nq) {
@@ -410,15 +384,11 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
         };
         pass1(std::false_type{});
         if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
+        if (kNS >= 1) aff_orthonormalize(M);
         if (tid == 0) bulk_wait_read_all();  // the gradient staging is free again
-        Aff P = aff_identity();
-        if (!kCk) {
-            const Aff carry = (t == 0) ? aff_identity() : load_aff(pref + t * 12);
-            if (kNS >= 1) aff_orthonormalize(M);
-            P = block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
-        }
+        const Aff P = block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
 
-        // pass 2: gradients into the chunk frame (g_loc = R^T g; the global frame under kCk)
+        // pass 2: gradients rotated into the chunk frame (g_loc = R^T g)
         float sl[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         float gx[APT], gy[APT], gz[APT];
 #pragma unroll
@@ -427,13 +397,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
             if (a / 3 < nq) {
                 const float* g = s_g + 9 * rl0 + 3 * a;
                 const float g0 = g[0], g1 = g[1], g2 = g[2];
-                if (kCk) {
-                    gx[a] = g0; gy[a] = g1; gz[a] = g2;
-                } else {
-                    gx[a] = fmaf(P.r00, g0, fmaf(P.r10, g1, P.r20 * g2));
-                    gy[a] = fmaf(P.r01, g0, fmaf(P.r11, g1, P.r21 * g2));
-                    gz[a] = fmaf(P.r02, g0, fmaf(P.r12, g1, P.r22 * g2));
-                }
+                gx[a] = fmaf(P.r00, g0, fmaf(P.r10, g1, P.r20 * g2));
+                gy[a] = fmaf(P.r01, g0, fmaf(P.r11, g1, P.r21 * g2));
+                gz[a] = fmaf(P.r02, g0, fmaf(P.r12, g1, P.r22 * g2));
                 sl[0] += gx[a]; sl[1] += gy[a]; sl[2] += gz[a];
                 sl[3] += fmaf(py[a], gz[a], -pz[a] * gy[a]);
                 sl[4] += fmaf(pz[a], gx[a], -px[a] * gz[a]);
@@ -442,26 +408,18 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
         }
         // thread totals in the global frame: S = R S_l, T = R T_l + t x S
         float sum6[6];
-        if (kCk) {
-#pragma unroll
-            for (int q = 0; q < 6; ++q) sum6[q] = sl[q];
-        } else {
-            sum6[0] = fmaf(P.r00, sl[0], fmaf(P.r01, sl[1], P.r02 * sl[2]));
-            sum6[1] = fmaf(P.r10, sl[0], fmaf(P.r11, sl[1], P.r12 * sl[2]));
-            sum6[2] = fmaf(P.r20, sl[0], fmaf(P.r21, sl[1], P.r22 * sl[2]));
-            sum6[3] = fmaf(P.r00, sl[3], fmaf(P.r01, sl[4], P.r02 * sl[5])) + fmaf(P.t1, sum6[2], -P.t2 * sum6[1]);
-            sum6[4] = fmaf(P.r10, sl[3], fmaf(P.r11, sl[4], P.r12 * sl[5])) + fmaf(P.t2, sum6[0], -P.t0 * sum6[2]);
-            sum6[5] = fmaf(P.r20, sl[3], fmaf(P.r21, sl[4], P.r22 * sl[5])) + fmaf(P.t0, sum6[1], -P.t1 * sum6[0]);
-        }
+        sum6[0] = fmaf(P.r00, sl[0], fmaf(P.r01, sl[1], P.r02 * sl[2]));
+        sum6[1] = fmaf(P.r10, sl[0], fmaf(P.r11, sl[1], P.r12 * sl[2]));
+        sum6[2] = fmaf(P.r20, sl[0], fmaf(P.r21, sl[1], P.r22 * sl[2]));
+        sum6[3] = fmaf(P.r00, sl[3], fmaf(P.r01, sl[4], P.r02 * sl[5])) + fmaf(P.t1, sum6[2], -P.t2 * sum6[1]);
+        sum6[4] = fmaf(P.r10, sl[3], fmaf(P.r11, sl[4], P.r12 * sl[5])) + fmaf(P.t2, sum6[0], -P.t0 * sum6[2]);
+        sum6[5] = fmaf(P.r20, sl[3], fmaf(P.r21, sl[4], P.r22 * sl[5])) + fmaf(P.t0, sum6[1], -P.t1 * sum6[0]);
         float suf[6], tot6[6];
         block_exclusive_suffix6<NT>(sum6, carry6, s_suf, suf, tot6);
         if (!nx.valid) pdl_trigger();  // late trigger (see the forward kernel)
         // later atoms into the chunk frame: S_l = R^T S, T_l = R^T (T - t x S)
         float su[6];
-        if (kCk) {
-#pragma unroll
-            for (int q = 0; q < 6; ++q) su[q] = suf[q];
-        } else {
+        {
             const float w0 = suf[3] - fmaf(P.t1, suf[2], -P.t2 * suf[1]);
             const float w1 = suf[4] - fmaf(P.t2, suf[0], -P.t0 * suf[2]);
             const float w2 = suf[5] - fmaf(P.t0, suf[1], -P.t1 * suf[0]);
@@ -524,6 +482,171 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// Backward from the forward's coordinates (no angles, no trig, no affine scan).
+// The rotation axis of alpha_a is the unit bond vector e_a = (r_a - r_{a-1}) /
+// |r_a - r_{a-1}| through r_a (M_a = M_{a-1} R_y(theta) T_x(d) R_x(alpha): the
+// x-axis of frame a is the bond direction and its origin is r_a), so with
+// S_a = sum_{b>a} g_b and T_a = sum_{b>a} (r_b - c) x g_b,
+//   dL/dalpha_a = e_a . (T_a - (r_a - c) x S_a)
+// for any reference point c (c = the tile's first atom, to keep moments small).
+// One reverse suffix sum of (S, T) per chain; tiles last to first.
+__device__ __forceinline__ void bbx_issue(const BBIter& it, const float* coords, const float* grad_coords,
+                                          char* s_x, char* s_g, uint64_t* bar) {
+    const int r0 = it.r0(), n = it.n(), pre = r0 > 0 ? 1 : 0;
+    const size_t base = ((size_t)it.b * 3 * it.Lmax + 3 * (size_t)r0) * 3;
+    const Span sx = make_span(coords + base - 3 * pre, (3 * n + pre) * 12);
+    const Span sg = make_span(grad_coords + base, n * 36);
+    mbar_arrive_expect_tx(bar, unsigned(sx.mid + sg.mid));
+    span_load_bulk(sx, s_x, bar);
+    span_load_bulk(sg, s_g, bar);
+}
+
+template <int NT, int RPT>
+__global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_kernel(const float* __restrict__ coords,
+                                                             const int* __restrict__ lengths, int B, int Lmax,
+                                                             const float* __restrict__ grad_coords,
+                                                             float* __restrict__ grad_angles,
+                                                             unsigned* __restrict__ err) {
+    constexpr int TILE = NT * RPT;
+    constexpr int XB = round16(16 + 36 * TILE + 12);  // tile atoms + the previous atom
+    constexpr int GB = round16(16 + 36 * TILE);
+    using S = BBSmem<NT>;
+    extern __shared__ __align__(16) char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
+    float* s_suf = reinterpret_cast<float*>(smem + S::kSuf);
+    float* s_misc = reinterpret_cast<float*>(smem + S::kMisc);
+    char* s_x_buf = smem + S::kData;   // 2 x XB
+    char* s_g_buf = s_x_buf + 2 * XB;  // 2 x GB
+    char* s_go_base = s_g_buf + 2 * GB;
+
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        fence_barrier_init();
+    }
+    pdl_wait();
+    BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), false, err, true};
+    it.init();
+    __syncthreads();
+    if (tid == 0 && it.valid) bbx_issue(it, coords, grad_coords, s_x_buf, s_g_buf, bar);
+
+    unsigned phases = 0;
+    const int rl0 = tid * RPT;
+    float carry6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // (S, T) of the later tiles, about c_prev
+    float cpx = 0.f, cpy = 0.f, cpz = 0.f;              // reference point of the later tile
+    float omega_next = 0.f;
+    for (int k = 0; it.valid; ++k) {
+        const int buf = k & 1;
+        const int b = it.b, L = it.L, r0 = it.r0(), n = it.n(), pre = r0 > 0 ? 1 : 0;
+        const bool last_tile = r0 + n == L;
+        BBIter nx = it;
+        nx.advance();
+        if (tid == 0 && nx.valid)
+            bbx_issue(nx, coords, grad_coords, s_x_buf + (buf ^ 1) * XB, s_g_buf + (buf ^ 1) * GB, bar + (buf ^ 1));
+        char* s_x_base = s_x_buf + buf * XB;
+        char* s_g_base = s_g_buf + buf * GB;
+        const size_t base = ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3;
+        const Span sx = make_span(coords + base - 3 * pre, (3 * n + pre) * 12);
+        const Span sg = make_span(grad_coords + base, n * 36);
+        span_load_edges_f32(sx, s_x_base);
+        span_load_edges_f32(sg, s_g_base);
+        mbar_wait(bar + buf, (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+        __syncthreads();
+        const float* s_x = reinterpret_cast<const float*>(s_x_base + sx.mis()) + 3 * pre;  // atom 0 of the tile
+        const float* s_g = reinterpret_cast<const float*>(s_g_base + sg.mis());
+        const int nq = max(0, min(RPT, n - rl0));
+        const float cx = s_x[0], cy = s_x[1], cz = s_x[2];
+        if (last_tile) {
+#pragma unroll
+            for (int q = 0; q < 6; ++q) carry6[q] = 0.f;
+            omega_next = 0.f;
+        } else {  // move the later tiles' moment to this tile's reference: T_c = T_c' + (c' - c) x S
+            const float dx = cpx - cx, dy = cpy - cy, dz = cpz - cz;
+            carry6[3] += fmaf(dy, carry6[2], -dz * carry6[1]);
+            carry6[4] += fmaf(dz, carry6[0], -dx * carry6[2]);
+            carry6[5] += fmaf(dx, carry6[1], -dy * carry6[0]);
+        }
+        cpx = cx; cpy = cy; cpz = cz;
+
+        // pass 1: this thread's (S, T) about c
+        float sum6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int a = 0; a < 3 * RPT; ++a) {
+            if (a / 3 < nq) {
+                const float* x = s_x + 9 * rl0 + 3 * a;
+                const float* g = s_g + 9 * rl0 + 3 * a;
+                const float px = x[0] - cx, py = x[1] - cy, pz = x[2] - cz, gx = g[0], gy = g[1], gz = g[2];
+                sum6[0] += gx; sum6[1] += gy; sum6[2] += gz;
+                sum6[3] += fmaf(py, gz, -pz * gy);
+                sum6[4] += fmaf(pz, gx, -px * gz);
+                sum6[5] += fmaf(px, gy, -py * gx);
+            }
+        }
+        if (tid == 0) bulk_wait_read_all();  // the output staging is free again
+        float su[6], tot6[6];
+        block_exclusive_suffix6<NT>(sum6, carry6, s_suf, su, tot6);
+        if (!nx.valid) pdl_trigger();
+
+        // pass 2: atoms last to first
+        const Span so = make_span(grad_angles + ((size_t)b * Lmax + r0) * 3, n * 12);
+        float* s_go = reinterpret_cast<float*>(s_go_base + so.mis());
+#pragma unroll
+        for (int q = RPT - 1; q >= 0; --q) {
+            if (q < nq) {
+                const int rl = rl0 + q;
+                const int j = r0 + rl;
+                float ga[3];
+#pragma unroll
+                for (int kk = 2; kk >= 0; --kk) {
+                    const int a = 3 * rl + kk;  // atom index within the tile
+                    const float* x = s_x + 3 * a;
+                    const float* g = s_g + 3 * a;
+                    const float x0 = x[0], x1 = x[1], x2 = x[2];
+                    const float px = x0 - cx, py = x1 - cy, pz = x2 - cz;
+                    const float gx = g[0], gy = g[1], gz = g[2];
+                    if (j > 0 || kk > 0) {  // atom 0 of the chain carries no angle
+                        const float ux = x0 - x[-3], uy = x1 - x[-2], uz = x2 - x[-1];
+                        const float inv = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
+                        const float c0 = su[3] - fmaf(py, su[2], -pz * su[1]);
+                        const float c1 = su[4] - fmaf(pz, su[0], -px * su[2]);
+                        const float c2 = su[5] - fmaf(px, su[1], -py * su[0]);
+                        ga[kk] = inv * fmaf(ux, c0, fmaf(uy, c1, uz * c2));
+                    } else {
+                        ga[kk] = 0.f;
+                    }
+                    su[0] += gx; su[1] += gy; su[2] += gz;
+                    su[3] += fmaf(py, gz, -pz * gy);
+                    su[4] += fmaf(pz, gx, -px * gz);
+                    su[5] += fmaf(px, gy, -py * gx);
+                }
+                s_go[3 * rl + 0] = ga[1];  // phi_j
+                s_go[3 * rl + 1] = ga[2];  // psi_j
+                if (j > 0) {               // omega_{j-1}
+                    if (rl > 0) s_go[3 * (rl - 1) + 2] = ga[0];
+                    else s_misc[0] = ga[0];  // belongs to the previous tile
+                }
+            }
+        }
+        if (tid == 0) s_go[3 * (n - 1) + 2] = last_tile ? 0.f : omega_next;
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            span_store_bulk(so, s_go_base);
+            bulk_commit();
+        }
+        span_store_edges_f32(so, s_go_base);
+        omega_next = s_misc[0];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) carry6[q] = tot6[q];
+        __syncthreads();
+        it = nx;
+    }
+    if (tid == 0) bulk_wait_read_all();
+}
+
+// ---------------------------------------------------------------------------
 // Host-side launch helpers (called from capi.cu).
 
 // Launch shape: NT threads per chain, RPT residues per thread (tile NT*RPT).
@@ -574,8 +697,7 @@ static size_t bwd_smem(int rpt) {
 }
 
 // Persistent grid: at most the resident CTAs, never more than the chains.
-template <typename K>
-static int persistent_grid(K kernel, int nt, size_t smem, int B) {
+static int sm_count() {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -583,6 +705,12 @@ static int persistent_grid(K kernel, int nt, size_t smem, int B) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms <= 0) sms = 148;
     }
+    return sms;
+}
+
+template <typename K>
+static int persistent_grid(K kernel, int nt, size_t smem, int B) {
+    const int sms = sm_count();
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
@@ -590,9 +718,9 @@ static int persistent_grid(K kernel, int nt, size_t smem, int B) {
     return int(B < cap ? B : cap);
 }
 
-template <int NT, int RPT, int NS, bool CK>
+template <int NT, int RPT, int NS>
 static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
-    auto k = bb_forward_kernel<NT, RPT, NS, CK>;
+    auto k = bb_forward_kernel<NT, RPT, NS>;
     const size_t sm = fwd_smem<NT>(RPT);
     static size_t configured = 0;  // set the smem opt-in once per instance (not inside graph capture)
     static int grid_cap = 0;
@@ -603,11 +731,11 @@ static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
         grid_cap = persistent_grid(k, NT, sm, 1 << 30);
     }
     const int grid = a.B < grid_cap ? a.B : grid_cap;
-    return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err, a.ckpt);
+    return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err);
 }
-template <int NT, int RPT, int NS, bool CK>
+template <int NT, int RPT, int NS>
 static cudaError_t launch_bwd(const BBArgs& a, cudaStream_t st) {
-    auto k = bb_backward_kernel<NT, RPT, NS, CK>;
+    auto k = bb_backward_kernel<NT, RPT, NS>;
     const size_t sm = bwd_smem<NT>(RPT);
     static size_t configured = 0;
     static int grid_cap = 0;
@@ -619,38 +747,78 @@ static cudaError_t launch_bwd(const BBArgs& a, cudaStream_t st) {
     }
     const int grid = a.B < grid_cap ? a.B : grid_cap;
     return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.grad_coords, a.grad_angles, a.err,
-                      a.ws_prefix, a.max_tiles, static_cast<const float*>(a.ckpt));
-}
-
-// Checkpointed shape: 3 residues per thread (one checkpoint per thread chunk).
-static BBShape bb_ck_shape(int Lmax) {
-    int nt = bb_nt_env();
-    if (nt != 128 && nt != 256) nt = Lmax > 384 ? 256 : 128;
-    return {nt, kCkptRes};
+                      a.ws_prefix, a.max_tiles);
 }
 
 template <bool kFwd, int NS>
 static cudaError_t dispatch(const BBArgs& a, cudaStream_t st) {
-    if (a.ckpt) {
-        const BBShape s = bb_ck_shape(a.Lmax);
-        if (kFwd) return s.nt == 256 ? launch_fwd<256, 3, NS, true>(a, st) : launch_fwd<128, 3, NS, true>(a, st);
-        return s.nt == 256 ? launch_bwd<256, 3, NS, true>(a, st) : launch_bwd<128, 3, NS, true>(a, st);
-    }
     const BBShape s = bb_shape(kFwd, a.Lmax);
     if (kFwd) {
 #define TPL_BB_FWD(NT_, R_) \
-    if (s.nt == NT_ && s.rpt == R_) return launch_fwd<NT_, R_, NS, false>(a, st);
+    if (s.nt == NT_ && s.rpt == R_) return launch_fwd<NT_, R_, NS>(a, st);
         TPL_BB_FWD(32, 1) TPL_BB_FWD(32, 3) TPL_BB_FWD(32, 5) TPL_BB_FWD(32, 7)
         TPL_BB_FWD(128, 1) TPL_BB_FWD(128, 3) TPL_BB_FWD(128, 5) TPL_BB_FWD(128, 7)
         TPL_BB_FWD(256, 1) TPL_BB_FWD(256, 3) TPL_BB_FWD(256, 5)
 #undef TPL_BB_FWD
     } else {
 #define TPL_BB_BWD(NT_, R_) \
-    if (s.nt == NT_ && s.rpt == R_) return launch_bwd<NT_, R_, NS, false>(a, st);
+    if (s.nt == NT_ && s.rpt == R_) return launch_bwd<NT_, R_, NS>(a, st);
         TPL_BB_BWD(32, 1) TPL_BB_BWD(32, 3) TPL_BB_BWD(32, 5)
         TPL_BB_BWD(128, 1) TPL_BB_BWD(128, 3) TPL_BB_BWD(256, 1) TPL_BB_BWD(256, 3)
 #undef TPL_BB_BWD
     }
+    return cudaErrorInvalidConfiguration;
+}
+
+template <int NT, int RPT>
+static cudaError_t launch_bwd_xyz(const BBArgs& a, cudaStream_t st) {
+    auto k = bb_backward_xyz_kernel<NT, RPT>;
+    const int tile = NT * RPT;
+    const size_t sm = BBSmem<NT>::kData + 2 * round16(16 + 36 * tile + 12) + 2 * round16(16 + 36 * tile) +
+                      round16(16 + 12 * tile);
+    static size_t configured = 0;
+    static int grid_cap = 0;
+    if (configured < sm) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+        configured = sm;
+        grid_cap = persistent_grid(k, NT, sm, 1 << 30);
+    }
+    const int grid = a.B < grid_cap ? a.B : grid_cap;
+    return launch_pdl(k, grid, NT, sm, st, static_cast<const float*>(a.coords), a.lengths, a.B, a.Lmax,
+                      a.grad_coords, a.grad_angles, a.err);
+}
+
+// Shape of the coordinate backward: TPL_BBX=NTxRPT (tuning) or the default.
+// Measured (tools/gpu_bbx.sh): with at most one chain per SM the serial tile
+// chain dominates -> the largest tile (256 threads, RPT up to 5); with more
+// chains than SMs the kernel streams HBM and small tiles win (more resident
+// CTAs: 128 x 3 takes 60 KB of shared memory, 3 CTAs per SM).
+static BBShape bbx_shape(int B, int Lmax) {
+    static int env_nt = -1, env_rpt = 0;
+    if (env_nt < 0) {
+        env_nt = 0;
+        if (const char* e = std::getenv("TPL_BBX")) {
+            int nt = 0, r = 0;
+            if (std::sscanf(e, "%dx%d", &nt, &r) == 2) { env_nt = nt; env_rpt = r; }
+        }
+    }
+    if (env_nt) return {env_nt, env_rpt};
+    if (B > sm_count()) return {128, Lmax > 128 ? 3 : 1};
+    static const int opts[3] = {1, 3, 5};  // 256 x 7 would not fit in shared memory
+    const int nt = Lmax > 128 ? 256 : 128;
+    for (int i = 0; i < 3; ++i)
+        if (nt * opts[i] >= Lmax) return {nt, opts[i]};
+    return {nt, 5};
+}
+
+cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
+    const BBShape s = bbx_shape(a.B, a.Lmax);
+#define TPL_BBX(NT_, R_) \
+    if (s.nt == NT_ && s.rpt == R_) return launch_bwd_xyz<NT_, R_>(a, st);
+    TPL_BBX(128, 1) TPL_BBX(128, 3) TPL_BBX(128, 5) TPL_BBX(128, 7)
+    TPL_BBX(256, 1) TPL_BBX(256, 3) TPL_BBX(256, 5)
+#undef TPL_BBX
     return cudaErrorInvalidConfiguration;
 }
 

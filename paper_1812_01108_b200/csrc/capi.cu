@@ -153,8 +153,8 @@ static tpl_status bb_common(const float* angles, const int32_t* lengths, int32_t
     return check_ws(TPL_MODEL_BACKBONE, B, Lmax, ws, ws_bytes);
 }
 
-static tpl_status bb_forward_impl(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
-                                  float* coords, float* ckpt, void* workspace, size_t ws_bytes, void* stream) {
+tpl_status tpl_backbone_forward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                float* coords, void* workspace, size_t ws_bytes, void* stream) {
     tpl_status s = bb_common(angles, lengths, B, Lmax, workspace, ws_bytes);
     if (s != TPL_OK) return s;
     if (!coords) return fail(TPL_ERR_NULL, "coords is NULL");
@@ -170,15 +170,14 @@ static tpl_status bb_forward_impl(const float* angles, const int32_t* lengths, i
     a.max_tiles = max_tiles_for(TPL_MODEL_BACKBONE, Lmax);
     a.ns = ns_policy();
     a.K = backbone_constants();
-    a.ckpt = ckpt;
     cudaError_t e = bb_forward_launch(a, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "backbone forward launch");
     return TPL_OK;
 }
 
-static tpl_status bb_backward_impl(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
-                                   const float* ckpt, const float* grad_coords, float* grad_angles, void* workspace,
-                                   size_t ws_bytes, void* stream) {
+tpl_status tpl_backbone_backward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                 const float* grad_coords, float* grad_angles, void* workspace, size_t ws_bytes,
+                                 void* stream) {
     tpl_status s = bb_common(angles, lengths, B, Lmax, workspace, ws_bytes);
     if (s != TPL_OK) return s;
     if (!grad_coords || !grad_angles) return fail(TPL_ERR_NULL, "grad_coords/grad_angles is NULL");
@@ -195,43 +194,31 @@ static tpl_status bb_backward_impl(const float* angles, const int32_t* lengths, 
     a.max_tiles = max_tiles_for(TPL_MODEL_BACKBONE, Lmax);
     a.ns = ns_policy();
     a.K = backbone_constants();
-    a.ckpt = const_cast<float*>(ckpt);
     cudaError_t e = bb_backward_launch(a, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "backbone backward launch");
     return TPL_OK;
 }
 
-tpl_status tpl_backbone_forward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
-                                float* coords, void* workspace, size_t ws_bytes, void* stream) {
-    return bb_forward_impl(angles, lengths, B, Lmax, coords, nullptr, workspace, ws_bytes, stream);
-}
-
-tpl_status tpl_backbone_backward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
-                                 const float* grad_coords, float* grad_angles, void* workspace, size_t ws_bytes,
-                                 void* stream) {
-    return bb_backward_impl(angles, lengths, B, Lmax, nullptr, grad_coords, grad_angles, workspace, ws_bytes, stream);
-}
-
-int64_t tpl_backbone_ckpt_floats(int32_t B, int32_t Lmax) {
-    if (B < 1 || Lmax < 1) return 0;
-    return static_cast<int64_t>(B) * ((Lmax + 2) / 3) * 12;
-}
-
-static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
-tpl_status tpl_backbone_forward_ckpt(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
-                                     float* coords, float* ckpt, void* workspace, size_t ws_bytes, void* stream) {
-    if (!ckpt) return fail(TPL_ERR_NULL, "ckpt is NULL");
-    if (!aligned16(ckpt)) return fail(TPL_ERR_ALIGN, "ckpt not 16-byte aligned");
-    return bb_forward_impl(angles, lengths, B, Lmax, coords, ckpt, workspace, ws_bytes, stream);
-}
-
-tpl_status tpl_backbone_backward_ckpt(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
-                                      const float* ckpt, const float* grad_coords, float* grad_angles,
-                                      void* workspace, size_t ws_bytes, void* stream) {
-    if (!ckpt) return fail(TPL_ERR_NULL, "ckpt is NULL");
-    if (!aligned16(ckpt)) return fail(TPL_ERR_ALIGN, "ckpt not 16-byte aligned");
-    return bb_backward_impl(angles, lengths, B, Lmax, ckpt, grad_coords, grad_angles, workspace, ws_bytes, stream);
+tpl_status tpl_backbone_backward_from_coords(const float* coords, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                             const float* grad_coords, float* grad_angles, void* workspace,
+                                             size_t ws_bytes, void* stream) {
+    if (!coords) return fail(TPL_ERR_NULL, "coords is NULL");
+    // bb_common checks lengths/B/Lmax/workspace; coords stands in for the (unused) angles
+    tpl_status s = bb_common(coords, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!grad_coords || !grad_angles) return fail(TPL_ERR_NULL, "grad_coords/grad_angles is NULL");
+    if (!aligned4(grad_coords) || !aligned4(grad_angles)) return fail(TPL_ERR_ALIGN, "grads not 4-byte aligned");
+    BBArgs a{};
+    a.lengths = lengths;
+    a.B = B;
+    a.Lmax = Lmax;
+    a.coords = const_cast<float*>(coords);
+    a.grad_coords = grad_coords;
+    a.grad_angles = grad_angles;
+    a.err = static_cast<unsigned*>(workspace);
+    cudaError_t e = bb_backward_xyz_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "backbone backward (from coords) launch");
+    return TPL_OK;
 }
 
 // ---------------------------------------------------------------- tables

@@ -41,7 +41,6 @@ struct BBArgs {
     int max_tiles;
     int ns;  // Newton-Schulz policy: 0 none, 1 prefix/total, 2 every combine
     BBConst K;
-    float* ckpt;  // optional per-3-residue prefix checkpoints [B][ceil(Lmax/3)][12] (nullptr: none)
 };
 
 bool pdl_enabled();  // capi.cu: programmatic dependent launch on (TPL_PDL != 0)
@@ -50,6 +49,7 @@ int bb_rpt_for(int Lmax);
 int bb_tile_for(int Lmax);
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st);
+cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st);  // a.coords is the input
 
 // ---- full atom -------------------------------------------------------------
 // Device residue-type table (fp32, uploaded once by tpl_tables_create).

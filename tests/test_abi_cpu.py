@@ -66,6 +66,10 @@ def test_null_and_shape_rejected_before_launch(abi):
     # bad shape
     assert L.tpl_backbone_forward(p, p, 0, 4, p, p, 4096, None) == 2
     assert L.tpl_backbone_backward(p, p, 1, 0, p, p, p, 4096, None) == 2
+    assert L.tpl_backbone_backward_from_coords(None, p, 1, 4, p, p, p, 4096, None) == 1
+    assert L.tpl_backbone_backward_from_coords(p, p, 1, 0, p, p, p, 4096, None) == 2
+    assert L.tpl_backbone_backward_from_coords(p, p, 1, 4, None, p, p, 4096, None) == 1
+    assert L.tpl_backbone_backward_from_coords(p, p, 1, 4, p, p, p, 8, None) == 7
     # workspace too small / NULL
     assert L.tpl_backbone_forward(p, p, 1, 4, p, p, 8, None) == 7
     assert L.tpl_backbone_forward(p, p, 1, 4, p, None, 4096, None) == 7
