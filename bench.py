@@ -273,10 +273,12 @@ class FullAtomWork:
     def bwd(self, s, stream=None):
         from paper_1812_01108_b200 import _abi
 
-        _abi.tpl_fullatom_backward(self.tables.handle, s["angles"], s["restype"], s["lengths"], s["grad"],
-                                   s["gang"], s["ws"], stream)
+        # the autograd layer's backward: from the forward's coordinates
+        _abi.tpl_fullatom_backward_from_coords(self.tables.handle, s["coords"], s["restype"], s["lengths"],
+                                               s["grad"], s["gang"], s["ws"], stream)
 
     def algo_bytes(self):
+        # the op's bytes; the coordinate backward moves r * 33 + a * 24 (reads coords, not angles)
         r, a = self.residues, self.atoms
         return {"fwd": r * (32 + 1) + a * 12, "bwd": r * (32 + 1 + 32) + a * 12}
 

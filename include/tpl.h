@@ -193,6 +193,20 @@ TPL_API tpl_status tpl_fullatom_backward(const tpl_tables* tables, const float* 
                                  const float* grad_coords, float* grad_angles, void* workspace, size_t ws_bytes,
                                  void* stream);
 
+/* Backward from the forward's output: the same grad_angles computed from
+ * coords = tpl_fullatom_forward(angles) instead of the angles.  Each angle of
+ * Eq. 1 rotates a frame about the bond from its parent frame's
+ * origin to its own: the axis is the unit vector between those two
+ * origin atoms and the rotated subtree is fixed by the atom order.  Needs a
+ * table in which every such origin is an atom (r° = 0): N, CA, C and each
+ * chi group's first atom -- tpl_tables_backward_from_coords_ok() tells; else
+ * TPL_ERR_TABLE.  The bundled table (synth/residue_table.json) qualifies. */
+TPL_API tpl_status tpl_fullatom_backward_from_coords(const tpl_tables* tables, const float* coords,
+                                             const uint8_t* restype, const int32_t* lengths, int32_t B,
+                                             int32_t Lmax, int32_t atom_stride, const float* grad_coords,
+                                             float* grad_angles, void* workspace, size_t ws_bytes, void* stream);
+TPL_API int32_t tpl_tables_backward_from_coords_ok(const tpl_tables* tables);
+
 /* ======================================================================
  * LRMSD loss (§4): Coutsias-Seok-Dill quaternion method
  * ====================================================================== */

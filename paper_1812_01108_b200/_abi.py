@@ -29,6 +29,7 @@ EXPORTS = [
     "tpl_last_error", "tpl_abi_version", "tpl_workspace_bytes", "tpl_sync_status", "tpl_backbone_atoms",
     "tpl_backbone_forward", "tpl_backbone_backward", "tpl_backbone_backward_from_coords", "tpl_tables_create", "tpl_tables_destroy",
     "tpl_tables_n_types", "tpl_fullatom_atoms", "tpl_fullatom_forward", "tpl_fullatom_backward",
+    "tpl_fullatom_backward_from_coords", "tpl_tables_backward_from_coords_ok",
     "tpl_lrmsd_forward", "tpl_lrmsd_backward",
 ]
 
@@ -89,6 +90,10 @@ def _load():
     L.tpl_fullatom_forward.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, sz, vp]
     L.tpl_fullatom_backward.restype = ctypes.c_int
     L.tpl_fullatom_backward.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]
+    L.tpl_fullatom_backward_from_coords.restype = ctypes.c_int
+    L.tpl_fullatom_backward_from_coords.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]
+    L.tpl_tables_backward_from_coords_ok.restype = i32
+    L.tpl_tables_backward_from_coords_ok.argtypes = [vp]
     L.tpl_lrmsd_forward.restype = ctypes.c_int
     L.tpl_lrmsd_forward.argtypes = [vp, vp, vp, i32, i32, vp, vp, vp, sz, vp]
     L.tpl_lrmsd_backward.restype = ctypes.c_int
@@ -217,6 +222,25 @@ def tpl_fullatom_backward(handle, angles, restype, lengths, grad_coords, grad_an
                                      B, Lmax, grad_coords.shape[1], _dev(grad_coords, torch.float32, "grad_coords"),
                                      _dev(grad_angles, torch.float32, "grad_angles"),
                                      _dev(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream)))
+
+
+def tpl_fullatom_backward_from_coords(handle, coords, restype, lengths, grad_coords, grad_angles, workspace,
+                                      stream=None):
+    B, Lmax, slots = grad_angles.shape
+    if (slots != FA_SLOTS or tuple(restype.shape) != (B, Lmax) or coords.dim() != 3 or coords.shape[0] != B
+            or tuple(grad_coords.shape) != tuple(coords.shape)):
+        raise ValueError("shapes: coords/grad_coords [B,atom_stride,3], restype [B,Lmax], grad_angles [B,Lmax,8]")
+    _check(lib.tpl_fullatom_backward_from_coords(ctypes.c_void_p(handle), _dev(coords, torch.float32, "coords"),
+                                                 _dev(restype, torch.uint8, "restype"),
+                                                 _dev(lengths, torch.int32, "lengths"), B, Lmax, coords.shape[1],
+                                                 _dev(grad_coords, torch.float32, "grad_coords"),
+                                                 _dev(grad_angles, torch.float32, "grad_angles"),
+                                                 _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                                 _stream(stream)))
+
+
+def tpl_tables_backward_from_coords_ok(handle):
+    return bool(lib.tpl_tables_backward_from_coords_ok(ctypes.c_void_p(handle)))
 
 
 def tpl_lrmsd_forward(x, y, n_atoms, lrmsd, state, workspace, stream=None):

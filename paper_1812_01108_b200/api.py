@@ -75,6 +75,7 @@ class Tables:
         self.names = [ty.get("name", str(i)) for i, ty in enumerate(types)]
         self.atoms_per_type = torch.tensor([len(ty["atoms"]) for ty in types], dtype=torch.int64)
         self.handle = _abi.tpl_tables_create(descs)
+        self.backward_from_coords = _abi.tpl_tables_backward_from_coords_ok(self.handle)
 
     @property
     def n_types(self):
@@ -131,18 +132,25 @@ class FullAtomFunction(torch.autograd.Function):
         coords = torch.zeros((B, atom_stride, 3), dtype=torch.float32, device=angles.device)
         ws = default_workspace(angles.device).get(MODEL_FULLATOM, B, Lmax)
         _abi.tpl_fullatom_forward(tables.handle, angles, restype, lengths, coords, ws)
-        ctx.save_for_backward(angles, restype, lengths)
+        # tables with an atom at every frame origin back-propagate from the output
+        ctx.from_coords = tables.backward_from_coords
+        ctx.save_for_backward(coords if ctx.from_coords else angles, restype, lengths)
         ctx.tables = tables
+        ctx.Lmax = Lmax
         return coords
 
     @staticmethod
     def backward(ctx, grad_coords):
-        angles, restype, lengths = ctx.saved_tensors
-        B, Lmax, _ = angles.shape
-        grad_angles = torch.zeros_like(angles)
-        ws = default_workspace(angles.device).get(MODEL_FULLATOM, B, Lmax)
-        _abi.tpl_fullatom_backward(ctx.tables.handle, angles, restype, lengths, grad_coords.contiguous(),
-                                   grad_angles, ws)
+        saved, restype, lengths = ctx.saved_tensors
+        B, Lmax = restype.shape[0], ctx.Lmax
+        grad_angles = torch.zeros((B, Lmax, _abi.FA_SLOTS), dtype=torch.float32, device=saved.device)
+        ws = default_workspace(saved.device).get(MODEL_FULLATOM, B, Lmax)
+        if ctx.from_coords:
+            _abi.tpl_fullatom_backward_from_coords(ctx.tables.handle, saved, restype, lengths,
+                                                   grad_coords.contiguous(), grad_angles, ws)
+        else:
+            _abi.tpl_fullatom_backward(ctx.tables.handle, saved, restype, lengths, grad_coords.contiguous(),
+                                       grad_angles, ws)
         return grad_angles, None, None, None, None
 
 

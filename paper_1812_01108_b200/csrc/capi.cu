@@ -113,6 +113,10 @@ struct tpl_tables {
     int atoms[TPL_MAX_TYPES] = {0};
     int max_atoms = 0;
     int device = 0;
+    // every frame an angle rotates has an atom at its origin and at its parent's
+    // origin: the from-coordinates backward can read the rotation axes
+    bool xyz_ok = false;
+    std::string xyz_why;
 };
 
 extern "C" {
@@ -277,7 +281,10 @@ tpl_status tpl_tables_create(const tpl_residue_desc* types, int32_t n_types, tpl
             G.slot = sl;
             G.first_atom = -1;
             G.end_atom = -1;
+            G.origin = -1;
+            G.porigin = -1;
         }
+        h.iN = h.iCA = h.iC = -1;
         int prev_rank = -1;
         h.n_N = h.n_CA = 0;
         h.first_C = d.n_atoms;
@@ -307,6 +314,22 @@ tpl_status tpl_tables_create(const tpl_residue_desc* types, int32_t n_types, tpl
                 if (h.g[o].first_atom < 0) h.g[o].first_atom = k;
                 h.g[o].end_atom = k + 1;
             }
+            if (d.atom_r[k][0] == 0.0 && d.atom_r[k][1] == 0.0 && d.atom_r[k][2] == 0.0) {
+                int* slot = o == TPL_OWNER_N ? &h.iN : o == TPL_OWNER_CA ? &h.iCA : o == TPL_OWNER_C ? &h.iC
+                                                                                     : &h.g[o].origin;
+                if (*slot < 0) *slot = k;
+            }
+        }
+        for (int g = 0; g < d.n_groups; ++g) h.g[g].porigin = h.g[g].parent < 0 ? h.iCA : h.g[g - 1].origin;
+        if (T->xyz_why.empty()) {
+            char why[160] = {0};
+            if (h.iN < 0 || h.iCA < 0 || h.iC < 0)
+                std::snprintf(why, sizeof(why), "type %d: no atom at the N, CA or C frame origin", t);
+            for (int g = 0; g < d.n_groups && !why[0]; ++g)
+                if (h.g[g].slot >= 0 && (h.g[g].origin < 0 || h.g[g].porigin < 0))
+                    std::snprintf(why, sizeof(why), "type %d group %d: no atom at its frame's or parent's origin", t,
+                                  g);
+            if (why[0]) T->xyz_why = why;
         }
         // empty groups: give them an empty range at the right position
         int next = h.n_N + h.n_CA;
@@ -339,6 +362,7 @@ tpl_status tpl_tables_create(const tpl_residue_desc* types, int32_t n_types, tpl
     }
     T->n_types = n_types;
     T->device = dev;
+    T->xyz_ok = T->xyz_why.empty();
     *out = T;
     return TPL_OK;
 }
@@ -435,6 +459,28 @@ tpl_status tpl_fullatom_backward(const tpl_tables* T, const float* angles, const
     if (e != cudaSuccess) return cuda_fail(e, "full-atom backward launch");
     return TPL_OK;
 }
+
+tpl_status tpl_fullatom_backward_from_coords(const tpl_tables* T, const float* coords, const uint8_t* restype,
+                                             const int32_t* lengths, int32_t B, int32_t Lmax, int32_t atom_stride,
+                                             const float* grad_coords, float* grad_angles, void* workspace,
+                                             size_t ws_bytes, void* stream) {
+    if (!coords) return fail(TPL_ERR_NULL, "coords is NULL");
+    // fa_common's angle checks apply to coords (same pointer rules)
+    tpl_status s = fa_common(T, coords, restype, lengths, B, Lmax, atom_stride, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!T->xyz_ok) return fail(TPL_ERR_TABLE, "table cannot back-propagate from coordinates: %s", T->xyz_why.c_str());
+    if (!grad_coords || !grad_angles) return fail(TPL_ERR_NULL, "grad_coords/grad_angles is NULL");
+    if (!aligned4(grad_coords) || !aligned4(grad_angles)) return fail(TPL_ERR_ALIGN, "grads not 4-byte aligned");
+    FAArgs a = fa_args(T, nullptr, restype, lengths, B, Lmax, atom_stride, workspace);
+    a.coords = const_cast<float*>(coords);
+    a.grad_coords = grad_coords;
+    a.grad_angles = grad_angles;
+    cudaError_t e = fa_backward_xyz_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "full-atom backward (from coords) launch");
+    return TPL_OK;
+}
+
+int32_t tpl_tables_backward_from_coords_ok(const tpl_tables* T) { return T && T->xyz_ok ? 1 : 0; }
 
 // ---------------------------------------------------------------- LRMSD
 static tpl_status lr_common(const float* x, const float* y, const int32_t* n_atoms, int32_t B, int32_t stride,

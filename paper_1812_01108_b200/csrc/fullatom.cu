@@ -18,6 +18,9 @@
 // Chi subtrees are residue-local: a side-chain branch is walked from its tip
 // back to the CA frame (frames undone with the rigid inverse of each bond)
 // accumulating the local sums.  One reverse suffix scan per chain: O(L).
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -575,6 +578,300 @@ __global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_
 }
 
 // ---------------------------------------------------------------------------
+// Backward from the forward's coordinates.  Every angle rotates a frame whose
+// origin is an atom (table check xyz_ok), about the bond from the parent
+// frame's origin atom: e = unit(r_origin - r_parent_origin), o = r_origin.
+//   phi_j: N_j -> CA_j through CA_j, subtree {residue j minus N-owned} + later
+//   psi_j: CA_j -> C_j through C_j, subtree {C-owned atoms of j} + later
+//   omega_j: C_j -> N_{j+1} through N_{j+1}, subtree {residues > j}
+//   chi_g: parent origin -> group origin, subtree = groups g..(branch end)
+// No angles and no transforms are read.  Residue-local sums are taken about
+// CA_j, the chain suffix about the tile's first atom (moments stay small).
+// Tile atom offsets come from a pre-pass over the chain's residue types.
+template <int NT>
+struct FAXSmem {
+    static constexpr int NW = NT / 32;
+    static constexpr int kBar = 0;                   // 3 mbarriers: 2 tile buffers + table
+    static constexpr int kSuf = 32;                  // NW*6 floats
+    static constexpr int kInt = kSuf + NW * 6 * 4;   // NW ints
+    static constexpr int kTable = r16(kInt + NW * 4);
+};
+
+struct FAXTile {  // byte layout of one tile buffer
+    int rt, x, g, total;
+};
+__host__ __device__ inline FAXTile fax_tile_layout(int tile, int max_atoms) {
+    FAXTile l;
+    l.rt = 0;
+    l.x = r16(16 + tile);
+    l.g = l.x + r16(16 + 12 * max_atoms * tile);
+    l.total = l.g + r16(16 + 12 * max_atoms * tile);
+    return l;
+}
+
+template <int NT, int RPT>
+__global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_tiles) {
+    constexpr int TILE = NT * RPT;
+    using S = FAXSmem<NT>;
+    extern __shared__ __align__(16) char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
+    float* s_suf = reinterpret_cast<float*>(smem + S::kSuf);
+    int* s_int = reinterpret_cast<int*>(smem + S::kInt);
+    const FAType* s_types = reinterpret_cast<const FAType*>(smem + S::kTable);
+    int* s_off = reinterpret_cast<int*>(smem + S::kTable + r16(a.n_types * int(sizeof(FAType))));
+    char* s_buf = reinterpret_cast<char*>(s_off) + r16(4 * (max_tiles + 1));
+    const FAXTile lay = fax_tile_layout(TILE, a.max_atoms);
+    char* s_go_base = s_buf + 2 * lay.total;
+
+    const int b = blockIdx.x;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        mbar_init(bar + 2, 1);
+        fence_barrier_init();
+        const unsigned tb = unsigned(a.n_types * sizeof(FAType));
+        mbar_arrive_expect_tx(bar + 2, tb);
+        bulk_g2s(smem + S::kTable, a.types, tb, bar + 2);
+    }
+    pdl_wait();
+    const int L = a.lengths[b];
+    __syncthreads();
+    mbar_wait(bar + 2, 0);
+    if (L < 1 || L > a.Lmax) {
+        if (tid == 0) atomicOr(a.err, ERR_LENGTH);
+        return;
+    }
+    const unsigned char* rtb = a.restype + (size_t)b * a.Lmax;
+    const int n_tiles = (L + TILE - 1) / TILE;
+    const int rl0 = tid * RPT;
+
+    // pre-pass: atom offset of every tile start (and validity of the types)
+    {
+        int carry = 0;
+        bool bad = false;
+        for (int t = 0; t < n_tiles; ++t) {
+            int cnt = 0;
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                const int j = t * TILE + rl0 + q;
+                if (j < L) {
+                    const int ty = __ldg(rtb + j);
+                    if (ty >= a.n_types) bad = true;
+                    else cnt += s_types[ty].n_atoms;
+                }
+            }
+            int end;
+            block_exclusive_sum_int<NT>(cnt, carry, s_int, &end);
+            if (tid == 0) s_off[t] = carry;
+            carry = end;
+        }
+        if (tid == 0) s_off[n_tiles] = carry;
+        if (__syncthreads_or(bad)) {
+            if (tid == 0) atomicOr(a.err, ERR_RESTYPE);
+            return;
+        }
+    }
+
+    const float* xb = a.coords + (size_t)b * a.atom_stride * 3;
+    const float* gb = a.grad_coords + (size_t)b * a.atom_stride * 3;
+    auto spans = [&](int t, Span& sr, Span& sx, Span& sg) {
+        const int r0 = t * TILE, n = min(TILE, L - r0);
+        const int a0 = s_off[t], a1 = s_off[t + 1];
+        sr = make_span(rtb + r0, n);
+        sx = make_span(xb + (size_t)a0 * 3, (a1 - a0) * 12);
+        sg = make_span(gb + (size_t)a0 * 3, (a1 - a0) * 12);
+    };
+    auto issue = [&](int t, int buf) {
+        Span sr, sx, sg;
+        spans(t, sr, sx, sg);
+        char* base = s_buf + buf * lay.total;
+        mbar_arrive_expect_tx(bar + buf, unsigned(sr.mid + sx.mid + sg.mid));
+        span_load_bulk(sr, base + lay.rt, bar + buf);
+        span_load_bulk(sx, base + lay.x, bar + buf);
+        span_load_bulk(sg, base + lay.g, bar + buf);
+    };
+    if (tid == 0) issue(n_tiles - 1, 0);
+
+    float carry6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float cpx = 0.f, cpy = 0.f, cpz = 0.f;
+    unsigned phases = 0;
+    for (int k = 0; k < n_tiles; ++k) {
+        const int t = n_tiles - 1 - k, buf = k & 1;
+        const int r0 = t * TILE, n = min(TILE, L - r0);
+        if (tid == 0 && t > 0) issue(t - 1, buf ^ 1);
+        Span sr, sx, sg;
+        spans(t, sr, sx, sg);
+        char* base = s_buf + buf * lay.total;
+        span_load_edges_u8(sr, base + lay.rt);
+        span_load_edges_f32(sx, base + lay.x);
+        span_load_edges_f32(sg, base + lay.g);
+        mbar_wait(bar + buf, (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+        __syncthreads();
+        const unsigned char* s_rt = reinterpret_cast<const unsigned char*>(base + lay.rt + sr.mis());
+        const float* X = reinterpret_cast<const float*>(base + lay.x + sx.mis());
+        const float* G = reinterpret_cast<const float*>(base + lay.g + sg.mis());
+
+        if (tid == 0) bulk_wait_read_all();  // grad staging free (read by the previous store)
+        int typ[RPT];
+        int cnt = 0;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            typ[q] = rl0 + q < n ? s_rt[rl0 + q] : 0;
+            cnt += rl0 + q < n ? s_types[typ[q]].n_atoms : 0;
+        }
+        int tile_atoms;
+        const int off0 = block_exclusive_sum_int<NT>(cnt, 0, s_int, &tile_atoms);
+        const float rx = X[0], ry = X[1], rz = X[2];  // tile reference point
+        if (k > 0) {  // later tiles' moment about this tile's reference
+            const float dx = cpx - rx, dy = cpy - ry, dz = cpz - rz;
+            carry6[3] += fmaf(dy, carry6[2], -dz * carry6[1]);
+            carry6[4] += fmaf(dz, carry6[0], -dx * carry6[2]);
+            carry6[5] += fmaf(dx, carry6[1], -dy * carry6[0]);
+        }
+        cpx = rx; cpy = ry; cpz = rz;
+        float* s_go = reinterpret_cast<float*>(s_go_base);  // [n][8], 16-B aligned rows when dst is
+
+        // residue pass: chi gradients and residue sums about CA
+        float RA[RPT][6], RN[RPT][6], RC[RPT][6];
+        float thr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        int off = off0;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+#pragma unroll
+            for (int c = 0; c < 6; ++c) RA[q][c] = RN[q][c] = RC[q][c] = 0.f;
+            const int rl = rl0 + q;
+            if (rl < n) {
+                const FAType& T = s_types[typ[q]];
+                const float* x = X + 3 * off;
+                const float* g = G + 3 * off;
+                float* go = s_go + 8 * rl;
+#pragma unroll
+                for (int c = 3; c < 8; ++c) go[c] = 0.f;
+                const float cx = x[3 * T.iCA], cy = x[3 * T.iCA + 1], cz = x[3 * T.iCA + 2];
+                auto acc = [&](float* s6, int i) {
+                    cross_acc(s6, x[3 * i] - cx, x[3 * i + 1] - cy, x[3 * i + 2] - cz, g[3 * i], g[3 * i + 1],
+                              g[3 * i + 2]);
+                };
+                for (int i = 0; i < T.n_N; ++i) acc(RN[q], i);
+                for (int i = T.n_N; i < T.n_N + T.n_CA; ++i) acc(RA[q], i);
+                for (int i = T.first_C; i < T.n_atoms; ++i) acc(RC[q], i);
+                float br[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                for (int gi = T.n_groups - 1; gi >= 0; --gi) {
+                    const FAGroup& gr = T.g[gi];
+                    for (int i = gr.first_atom; i < gr.end_atom; ++i) acc(br, i);
+                    if (gr.slot >= 0) {
+                        const int o = gr.origin, p = gr.porigin;
+                        const float ox = x[3 * o] - cx, oy = x[3 * o + 1] - cy, oz = x[3 * o + 2] - cz;
+                        const float ux = x[3 * o] - x[3 * p], uy = x[3 * o + 1] - x[3 * p + 1],
+                                    uz = x[3 * o + 2] - x[3 * p + 2];
+                        const float inv = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
+                        go[gr.slot] = inv * axis_moment(ux, uy, uz, ox, oy, oz, br);
+                    }
+                    if (gr.parent < 0) {
+#pragma unroll
+                        for (int c = 0; c < 6; ++c) { RA[q][c] += br[c]; br[c] = 0.f; }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 6; ++c) RA[q][c] += RN[q][c] + RC[q][c];
+                // residue moment about the tile reference: T_r = T_CA + (CA - r) x S
+                const float dx = cx - rx, dy = cy - ry, dz = cz - rz;
+                const float* s6 = RA[q];
+                thr[0] += s6[0]; thr[1] += s6[1]; thr[2] += s6[2];
+                thr[3] += s6[3] + fmaf(dy, s6[2], -dz * s6[1]);
+                thr[4] += s6[4] + fmaf(dz, s6[0], -dx * s6[2]);
+                thr[5] += s6[5] + fmaf(dx, s6[1], -dy * s6[0]);
+                off += T.n_atoms;
+            }
+        }
+        float suf[6], tot6[6];
+        block_exclusive_suffix6<NT>(thr, carry6, s_suf, suf, tot6);
+
+        // backbone gradients, residues last to first
+#pragma unroll
+        for (int q = RPT - 1; q >= 0; --q) {
+            const int rl = rl0 + q;
+            const int j = r0 + rl;
+            if (rl < n) {
+                const FAType& T = s_types[typ[q]];
+                off -= T.n_atoms;
+                const float* x = X + 3 * off;
+                float* go = s_go + 8 * rl;
+                const float cx = x[3 * T.iCA], cy = x[3 * T.iCA + 1], cz = x[3 * T.iCA + 2];
+                const float dx = cx - rx, dy = cy - ry, dz = cz - rz;
+                float aft[6];  // later residues, moment about CA_j
+                aft[0] = suf[0]; aft[1] = suf[1]; aft[2] = suf[2];
+                aft[3] = suf[3] - fmaf(dy, suf[2], -dz * suf[1]);
+                aft[4] = suf[4] - fmaf(dz, suf[0], -dx * suf[2]);
+                aft[5] = suf[5] - fmaf(dx, suf[1], -dy * suf[0]);
+                const float nx = x[3 * T.iN], ny = x[3 * T.iN + 1], nz = x[3 * T.iN + 2];
+                const float kx = x[3 * T.iC], ky = x[3 * T.iC + 1], kz = x[3 * T.iC + 2];
+                float s6[6];
+                // psi_j
+#pragma unroll
+                for (int c = 0; c < 6; ++c) s6[c] = RC[q][c] + aft[c];
+                {
+                    const float ux = kx - cx, uy = ky - cy, uz = kz - cz;
+                    go[1] = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * axis_moment(ux, uy, uz, ux, uy, uz, s6);
+                }
+                // phi_j
+#pragma unroll
+                for (int c = 0; c < 6; ++c) s6[c] = RA[q][c] - RN[q][c] + aft[c];
+                {
+                    const float ux = cx - nx, uy = cy - ny, uz = cz - nz;
+                    go[0] = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * axis_moment(ux, uy, uz, 0.f, 0.f, 0.f, s6);
+                }
+                // omega_j: C_j -> N_{j+1}, later residues
+                float gw = 0.f;
+                if (j + 1 < L) {
+                    const float* xn;
+                    int tn;
+                    if (rl + 1 < n) {
+                        tn = s_rt[rl + 1];
+                        xn = x + 3 * T.n_atoms;
+                    } else {  // first residue of the later tile
+                        tn = __ldg(rtb + j + 1);
+                        xn = xb + (size_t)s_off[t + 1] * 3;
+                    }
+                    const int iN = s_types[tn].iN;
+                    const float px = xn[3 * iN], py = xn[3 * iN + 1], pz = xn[3 * iN + 2];
+                    const float ux = px - kx, uy = py - ky, uz = pz - kz;
+                    gw = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) *
+                         axis_moment(ux, uy, uz, px - cx, py - cy, pz - cz, aft);
+                }
+                go[2] = gw;
+                // fold this residue into the suffix (about the tile reference)
+                const float* r6 = RA[q];
+                suf[0] += r6[0]; suf[1] += r6[1]; suf[2] += r6[2];
+                suf[3] += r6[3] + fmaf(dy, r6[2], -dz * r6[1]);
+                suf[4] += r6[4] + fmaf(dz, r6[0], -dx * r6[2]);
+                suf[5] += r6[5] + fmaf(dx, r6[1], -dy * r6[0]);
+            }
+        }
+        __syncthreads();
+        {
+            float* dst = a.grad_angles + ((size_t)b * a.Lmax + r0) * kFASlots;
+            if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                fence_proxy_async_smem();
+                __syncthreads();
+                if (tid == 0) {
+                    bulk_s2g(dst, s_go, unsigned(n * 32));
+                    bulk_commit();
+                }
+            } else {
+                for (int i = tid; i < n * 8; i += NT) dst[i] = s_go[i];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) carry6[c] = tot6[c];
+        __syncthreads();
+    }
+    if (tid == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
 // One residue per thread; 256-thread forward CTAs, 128-thread backward CTAs
 // (the backward keeps more per-residue state: <= 170 registers, 3 CTAs/SM).
 // Chains longer than a tile loop over tiles.  The atom staging buffer is sized
@@ -620,6 +917,48 @@ static cudaError_t fa_bwd(const FAArgs& a, cudaStream_t st) {
         configured = sm;
     }
     return launch_pdl(k, a.B, kFABwdThreads, sm, st, a, a.max_atoms);
+}
+
+// TPL_FAX=NTxRPT (tuning) or 128 x 1.
+static void fax_shape(int* nt, int* rpt) {
+    static int env_nt = -1, env_rpt = 0;
+    if (env_nt < 0) {
+        env_nt = 0;
+        if (const char* e = std::getenv("TPL_FAX")) {
+            int x = 0, r = 0;
+            if (std::sscanf(e, "%dx%d", &x, &r) == 2) { env_nt = x; env_rpt = r; }
+        }
+    }
+    *nt = env_nt ? env_nt : 128;
+    *rpt = env_nt ? env_rpt : 1;
+}
+
+template <int NT, int RPT>
+static cudaError_t fa_bwd_xyz(const FAArgs& a, cudaStream_t st) {
+    auto k = fa_backward_xyz_kernel<NT, RPT>;
+    constexpr int TILE = NT * RPT;
+    const int max_tiles = (a.Lmax + TILE - 1) / TILE;
+    const size_t sm = FAXSmem<NT>::kTable + r16(a.n_types * int(sizeof(FAType))) + r16(4 * (max_tiles + 1)) +
+                      2 * fax_tile_layout(TILE, a.max_atoms).total + r16(32 * TILE);
+    static size_t configured = 0;
+    if (configured < sm) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+        configured = sm;
+    }
+    return launch_pdl(k, a.B, NT, sm, st, a, max_tiles);
+}
+
+cudaError_t fa_backward_xyz_launch(const FAArgs& a, cudaStream_t st) {
+    int nt, rpt;
+    fax_shape(&nt, &rpt);
+    if (nt == 64 && rpt == 1) return fa_bwd_xyz<64, 1>(a, st);
+    if (nt == 64 && rpt == 2) return fa_bwd_xyz<64, 2>(a, st);
+    if (nt == 128 && rpt == 1) return fa_bwd_xyz<128, 1>(a, st);
+    if (nt == 128 && rpt == 2) return fa_bwd_xyz<128, 2>(a, st);
+    if (nt == 256 && rpt == 1) return fa_bwd_xyz<256, 1>(a, st);
+    if (nt == 256 && rpt == 2) return fa_bwd_xyz<256, 2>(a, st);
+    return cudaErrorInvalidConfiguration;
 }
 
 cudaError_t fa_forward_launch(const FAArgs& a, cudaStream_t st) {

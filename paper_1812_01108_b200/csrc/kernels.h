@@ -63,12 +63,14 @@ struct FAGroup {
     int has_pre;       // pre_rx != 0
     int first_atom;    // index of the group's first atom in the type's atom list
     int end_atom;      // one past the group's last atom
+    int origin;        // atom at the group frame's origin (owned by g, r° = 0), -1 if none
+    int porigin;       // atom at the parent frame's origin (CA for parent -1), -1 if none
 };
 struct alignas(16) FAType {
     int n_groups, n_atoms;
     int n_N, n_CA;            // atoms owned by the N / CA frames (first n_N, then n_CA)
     int first_C;              // first atom owned by the C frame; C-owned atoms run to n_atoms
-    int pad[3];
+    int iN, iCA, iC;          // atoms at the N / CA / C frame origins (r° = 0), -1 if none
     FAGroup g[kMaxGroups];
     float r[kMaxAtomsPerRes][4];  // r° xyz (w unused)
 };
@@ -110,5 +112,6 @@ int fa_rpt_for(int Lmax);
 int fa_tile_for(int Lmax);
 cudaError_t fa_forward_launch(const FAArgs& a, cudaStream_t st);
 cudaError_t fa_backward_launch(const FAArgs& a, cudaStream_t st);
+cudaError_t fa_backward_xyz_launch(const FAArgs& a, cudaStream_t st);  // a.coords is the input
 
 }  // namespace tpl

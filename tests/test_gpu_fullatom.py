@@ -23,7 +23,7 @@ def tpl():
     return tpl
 
 
-def _run(tpl, tables, ang, rt, lengths, grad_fn, sentinel=float("nan")):
+def _run(tpl, tables, ang, rt, lengths, grad_fn, sentinel=float("nan"), xyz=False):
     from paper_1812_01108_b200 import _abi
 
     B, Lmax, _ = ang.shape
@@ -34,7 +34,10 @@ def _run(tpl, tables, ang, rt, lengths, grad_fn, sentinel=float("nan")):
     ws = torch.zeros(_abi.tpl_workspace_bytes(1, B, Lmax), dtype=torch.uint8, device="cuda")
     _abi.tpl_fullatom_forward(tables.handle, a, r, ln, coords, ws)
     grad = grad_fn(B, stride)
-    _abi.tpl_fullatom_backward(tables.handle, a, r, ln, grad.cuda(), gang, ws)
+    if xyz:  # backward from the forward's coordinates
+        _abi.tpl_fullatom_backward_from_coords(tables.handle, coords, r, ln, grad.cuda(), gang, ws)
+    else:
+        _abi.tpl_fullatom_backward(tables.handle, a, r, ln, grad.cuda(), gang, ws)
     _abi.tpl_sync_status(ws)
     return coords.cpu().numpy(), gang.cpu().numpy(), grad, apc.numpy()
 
@@ -69,12 +72,16 @@ def _check(oracle_lib, table, ang, rt, lengths, grad, coords, gang, apc, chains=
     return wc, wg
 
 
-def test_config3_all_types(tpl, oracle_lib, table):
+XYZ = pytest.mark.parametrize("xyz", [False, True], ids=["from_angles", "from_coords"])
+
+
+@XYZ
+def test_config3_all_types(tpl, oracle_lib, table, xyz):
     tables = tpl.Tables(table)
     ang, rt, lengths = synth.fullatom_inputs(3)
-    coords, gang, grad, apc = _run(tpl, tables, ang, rt, lengths, lambda B, S: synth.fullatom_grad(B, S, 3))
+    coords, gang, grad, apc = _run(tpl, tables, ang, rt, lengths, lambda B, S: synth.fullatom_grad(B, S, 3), xyz=xyz)
     c, g = _check(oracle_lib, table, ang, rt, lengths, grad, coords, gang, apc)
-    print(f"config3 64x300: max coord err {c:.3e} A, grad rel err {g:.3e}")
+    print(f"config3 64x300 ({'from coords' if xyz else 'from angles'}): max coord err {c:.3e} A, grad rel err {g:.3e}")
 
 
 @pytest.mark.parametrize("Lmax,lengths", [
@@ -82,34 +89,40 @@ def test_config3_all_types(tpl, oracle_lib, table):
     (256, [256, 255, 1]),
     (300, [300, 257, 129]),       # RPT 2, one tile
     (700, [700, 513, 512, 40]),   # two tiles (phase A: prefix + atom offset carries)
+    (1100, [1100, 897, 385, 384, 383]),  # several tiles of the coordinate backward
 ])
-def test_parity_ragged(tpl, oracle_lib, table, Lmax, lengths):
+@XYZ
+def test_parity_ragged(tpl, oracle_lib, table, Lmax, lengths, xyz):
     tables = tpl.Tables(table)
     B = len(lengths)
     ang = synth.angles_uniform(B, Lmax, 8, 11 + Lmax)
     rt = synth.restype_uniform(B, Lmax, 20, 12 + Lmax)
     ln = torch.tensor(lengths, dtype=torch.int32)
-    coords, gang, grad, apc = _run(tpl, tables, ang, rt, ln, lambda B_, S: synth.grad_normal((B_, S, 3), 13))
+    coords, gang, grad, apc = _run(tpl, tables, ang, rt, ln, lambda B_, S: synth.grad_normal((B_, S, 3), 13),
+                                   xyz=xyz)
     _check(oracle_lib, table, ang, rt, ln, grad, coords, gang, apc)
 
 
-def test_chi5_table(tpl, oracle_lib, table_chi5):
+@XYZ
+def test_chi5_table(tpl, oracle_lib, table_chi5, xyz):
     tables = tpl.Tables(table_chi5)
     B, L = 4, 64
     ang = synth.angles_uniform(B, L, 8, 21)
     rt = torch.full((B, L), 1, dtype=torch.uint8)  # ARG: chi1..chi5 variable
     rt[1] = synth.restype_uniform(1, L, 20, 22)[0]
     ln = torch.full((B,), L, dtype=torch.int32)
-    coords, gang, grad, apc = _run(tpl, tables, ang, rt, ln, lambda B_, S: synth.grad_normal((B_, S, 3), 23))
+    coords, gang, grad, apc = _run(tpl, tables, ang, rt, ln, lambda B_, S: synth.grad_normal((B_, S, 3), 23),
+                                   xyz=xyz)
     _check(oracle_lib, table_chi5, ang, rt, ln, grad, coords, gang, apc)
     assert np.abs(gang[0, :, 7]).max() > 0  # chi5 gradient is live
 
 
-def test_config5_shape_sampled(tpl, oracle_lib, table):
+@XYZ
+def test_config5_shape_sampled(tpl, oracle_lib, table, xyz):
     """Config 5 per-GPU shape (8192/8 = 1024 chains x L=500); parity on 8 sampled chains."""
     tables = tpl.Tables(table)
     ang, rt, lengths = synth.fullatom_inputs(5, B=1024)
-    coords, gang, grad, apc = _run(tpl, tables, ang, rt, lengths, lambda B, S: synth.fullatom_grad(B, S, 5))
+    coords, gang, grad, apc = _run(tpl, tables, ang, rt, lengths, lambda B, S: synth.fullatom_grad(B, S, 5), xyz=xyz)
     sample = sorted(np.random.default_rng(2).choice(1024, 8, replace=False).tolist())
     _check(oracle_lib, table, ang, rt, lengths, grad, coords, gang, apc, chains=sample)
 
@@ -158,3 +171,32 @@ def test_autograd_layer(tpl, oracle_lib, table):
     g = a.grad.cpu().numpy()
     for b in range(3):
         assert np.abs(g[b] - G[b]).max() / np.abs(G[b]).max() <= GRAD_TOL
+
+
+def test_from_coords_needs_origin_atoms(tpl, table):
+    """A table whose chi group has no atom at its frame origin cannot back-propagate
+    from coordinates: the call is refused before any launch (TPL_ERR_TABLE)."""
+    import copy
+
+    from paper_1812_01108_b200 import TplError, _abi
+
+    assert tpl.Tables(table).backward_from_coords
+    bad = copy.deepcopy(table)
+    ser = next(t for t in bad["types"] if t["name"] == "SER")
+    cb = next(a for a in ser["atoms"] if a["name"] == "CB")
+    cb["r"] = [0.1, 0.0, 0.0]  # CB no longer at the chi1 frame origin
+    tables = tpl.Tables(bad)
+    assert not tables.backward_from_coords
+    B, L = 1, 4
+    ws = torch.zeros(_abi.tpl_workspace_bytes(1, B, L), dtype=torch.uint8, device="cuda")
+    rt = torch.zeros(B, L, dtype=torch.uint8, device="cuda")
+    ln = torch.full((B,), L, dtype=torch.int32, device="cuda")
+    x = torch.zeros(B, 64, 3, device="cuda")
+    with pytest.raises(TplError) as e:
+        _abi.tpl_fullatom_backward_from_coords(tables.handle, x, rt, ln, x.clone(), torch.zeros(B, L, 8, device="cuda"),
+                                               ws)
+    assert e.value.status == 4
+    # the autograd layer falls back to the from-angles backward for such tables
+    a = synth.angles_uniform(B, L, 8, 3).cuda().requires_grad_(True)
+    tpl.fullatom(a, rt, ln, tables).sum().backward()
+    assert torch.isfinite(a.grad).all()

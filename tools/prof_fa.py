@@ -12,6 +12,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--B", type=int, default=1024)
 p.add_argument("--L", type=int, default=500)
 p.add_argument("--iters", type=int, default=3)
+p.add_argument("--angles-bwd", action="store_true", help="backward from the angles (default: from coords)")
 a = p.parse_args()
 torch.cuda.set_device(0)
 tables = tpl.Tables(synth.load_residue_table())
@@ -26,6 +27,9 @@ ga = torch.empty(a.B, a.L, 8, device="cuda")
 ws = torch.zeros(_abi.tpl_workspace_bytes(1, a.B, a.L), dtype=torch.uint8, device="cuda")
 for _ in range(a.iters):
     _abi.tpl_fullatom_forward(tables.handle, ang, rt, ln, c, ws)
-    _abi.tpl_fullatom_backward(tables.handle, ang, rt, ln, g, ga, ws)
+    if a.angles_bwd:
+        _abi.tpl_fullatom_backward(tables.handle, ang, rt, ln, g, ga, ws)
+    else:
+        _abi.tpl_fullatom_backward_from_coords(tables.handle, c, rt, ln, g, ga, ws)
 torch.cuda.synchronize()
 print("ok")
