@@ -469,6 +469,7 @@ tpl_status tpl_fullatom_backward_from_coords(const tpl_tables* T, const float* c
     tpl_status s = fa_common(T, coords, restype, lengths, B, Lmax, atom_stride, workspace, ws_bytes);
     if (s != TPL_OK) return s;
     if (!T->xyz_ok) return fail(TPL_ERR_TABLE, "table cannot back-propagate from coordinates: %s", T->xyz_why.c_str());
+    if (Lmax > kFAXMaxL) return fail(TPL_ERR_SHAPE, "Lmax=%d > %d (the chain's types are staged on chip)", Lmax, kFAXMaxL);
     if (!grad_coords || !grad_angles) return fail(TPL_ERR_NULL, "grad_coords/grad_angles is NULL");
     if (!aligned4(grad_coords) || !aligned4(grad_angles)) return fail(TPL_ERR_ALIGN, "grads not 4-byte aligned");
     FAArgs a = fa_args(T, nullptr, restype, lengths, B, Lmax, atom_stride, workspace);

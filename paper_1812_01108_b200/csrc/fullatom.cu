@@ -591,25 +591,31 @@ __global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_
 template <int NT>
 struct FAXSmem {
     static constexpr int NW = NT / 32;
-    static constexpr int kBar = 0;                   // 3 mbarriers: 2 tile buffers + table
+    static constexpr int kBar = 0;                   // 4 mbarriers: 2 tile buffers, table, chain restype
     static constexpr int kSuf = 32;                  // NW*6 floats
     static constexpr int kInt = kSuf + NW * 6 * 4;   // NW ints
     static constexpr int kTable = r16(kInt + NW * 4);
 };
 
 struct FAXTile {  // byte layout of one tile buffer
-    int rt, x, g, total;
+    int x, g, total;
 };
 __host__ __device__ inline FAXTile fax_tile_layout(int tile, int max_atoms) {
     FAXTile l;
-    l.rt = 0;
-    l.x = r16(16 + tile);
+    l.x = 0;
     l.g = l.x + r16(16 + 12 * max_atoms * tile);
     l.total = l.g + r16(16 + 12 * max_atoms * tile);
     return l;
 }
 
-template <int NT, int RPT>
+// kDB: double-buffered tiles (prefetch tile t-1 during t); kTabSmem: the
+// residue table staged in shared memory (else read through L1).  Both cost
+// shared memory, i.e. resident CTAs; tools/gpu_fax.sh measures the variants.
+__host__ __device__ constexpr int fax_table_bytes(bool tab_smem, int n_types) {
+    return tab_smem ? r16(n_types * int(sizeof(FAType))) : 0;
+}
+
+template <int NT, int RPT, bool kDB, bool kTabSmem>
 __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_tiles) {
     constexpr int TILE = NT * RPT;
     using S = FAXSmem<NT>;
@@ -617,11 +623,13 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
     float* s_suf = reinterpret_cast<float*>(smem + S::kSuf);
     int* s_int = reinterpret_cast<int*>(smem + S::kInt);
-    const FAType* s_types = reinterpret_cast<const FAType*>(smem + S::kTable);
-    int* s_off = reinterpret_cast<int*>(smem + S::kTable + r16(a.n_types * int(sizeof(FAType))));
-    char* s_buf = reinterpret_cast<char*>(s_off) + r16(4 * (max_tiles + 1));
+    const FAType* __restrict__ s_types =
+        kTabSmem ? reinterpret_cast<const FAType*>(smem + S::kTable) : a.types;
+    int* s_off = reinterpret_cast<int*>(smem + S::kTable + fax_table_bytes(kTabSmem, a.n_types));
+    char* s_rt_base = reinterpret_cast<char*>(s_off) + r16(4 * (max_tiles + 1));  // the chain's restype
+    char* s_buf = s_rt_base + r16(16 + a.Lmax);
     const FAXTile lay = fax_tile_layout(TILE, a.max_atoms);
-    char* s_go_base = s_buf + 2 * lay.total;
+    char* s_go_base = s_buf + (kDB ? 2 : 1) * lay.total;
 
     const int b = blockIdx.x;
     const int tid = threadIdx.x;
@@ -629,15 +637,18 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
         mbar_init(bar, 1);
         mbar_init(bar + 1, 1);
         mbar_init(bar + 2, 1);
+        mbar_init(bar + 3, 1);
         fence_barrier_init();
-        const unsigned tb = unsigned(a.n_types * sizeof(FAType));
-        mbar_arrive_expect_tx(bar + 2, tb);
-        bulk_g2s(smem + S::kTable, a.types, tb, bar + 2);
+        if (kTabSmem) {
+            const unsigned tb = unsigned(a.n_types * sizeof(FAType));
+            mbar_arrive_expect_tx(bar + 2, tb);
+            bulk_g2s(smem + S::kTable, a.types, tb, bar + 2);
+        }
     }
     pdl_wait();
     const int L = a.lengths[b];
     __syncthreads();
-    mbar_wait(bar + 2, 0);
+    if (kTabSmem) mbar_wait(bar + 2, 0);
     if (L < 1 || L > a.Lmax) {
         if (tid == 0) atomicOr(a.err, ERR_LENGTH);
         return;
@@ -645,6 +656,19 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
     const unsigned char* rtb = a.restype + (size_t)b * a.Lmax;
     const int n_tiles = (L + TILE - 1) / TILE;
     const int rl0 = tid * RPT;
+    // the chain's residue types, once (bar 3)
+    const unsigned char* s_rtc;
+    {
+        const Span sr = make_span(rtb, L);
+        if (tid == 0) {
+            mbar_arrive_expect_tx(bar + 3, unsigned(sr.mid));
+            span_load_bulk(sr, s_rt_base, bar + 3);
+        }
+        span_load_edges_u8(sr, s_rt_base);
+        mbar_wait(bar + 3, 0);
+        __syncthreads();
+        s_rtc = reinterpret_cast<const unsigned char*>(s_rt_base + sr.mis());
+    }
 
     // pre-pass: atom offset of every tile start (and validity of the types)
     {
@@ -656,7 +680,7 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
             for (int q = 0; q < RPT; ++q) {
                 const int j = t * TILE + rl0 + q;
                 if (j < L) {
-                    const int ty = __ldg(rtb + j);
+                    const int ty = s_rtc[j];
                     if (ty >= a.n_types) bad = true;
                     else cnt += s_types[ty].n_atoms;
                 }
@@ -675,19 +699,16 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
 
     const float* xb = a.coords + (size_t)b * a.atom_stride * 3;
     const float* gb = a.grad_coords + (size_t)b * a.atom_stride * 3;
-    auto spans = [&](int t, Span& sr, Span& sx, Span& sg) {
-        const int r0 = t * TILE, n = min(TILE, L - r0);
+    auto spans = [&](int t, Span& sx, Span& sg) {
         const int a0 = s_off[t], a1 = s_off[t + 1];
-        sr = make_span(rtb + r0, n);
         sx = make_span(xb + (size_t)a0 * 3, (a1 - a0) * 12);
         sg = make_span(gb + (size_t)a0 * 3, (a1 - a0) * 12);
     };
     auto issue = [&](int t, int buf) {
-        Span sr, sx, sg;
-        spans(t, sr, sx, sg);
+        Span sx, sg;
+        spans(t, sx, sg);
         char* base = s_buf + buf * lay.total;
-        mbar_arrive_expect_tx(bar + buf, unsigned(sr.mid + sx.mid + sg.mid));
-        span_load_bulk(sr, base + lay.rt, bar + buf);
+        mbar_arrive_expect_tx(bar + buf, unsigned(sx.mid + sg.mid));
         span_load_bulk(sx, base + lay.x, bar + buf);
         span_load_bulk(sg, base + lay.g, bar + buf);
     };
@@ -697,19 +718,18 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
     float cpx = 0.f, cpy = 0.f, cpz = 0.f;
     unsigned phases = 0;
     for (int k = 0; k < n_tiles; ++k) {
-        const int t = n_tiles - 1 - k, buf = k & 1;
+        const int t = n_tiles - 1 - k, buf = kDB ? (k & 1) : 0;
         const int r0 = t * TILE, n = min(TILE, L - r0);
-        if (tid == 0 && t > 0) issue(t - 1, buf ^ 1);
-        Span sr, sx, sg;
-        spans(t, sr, sx, sg);
+        if (kDB && tid == 0 && t > 0) issue(t - 1, buf ^ 1);
+        Span sx, sg;
+        spans(t, sx, sg);
         char* base = s_buf + buf * lay.total;
-        span_load_edges_u8(sr, base + lay.rt);
         span_load_edges_f32(sx, base + lay.x);
         span_load_edges_f32(sg, base + lay.g);
         mbar_wait(bar + buf, (phases >> buf) & 1u);
         phases ^= 1u << buf;
         __syncthreads();
-        const unsigned char* s_rt = reinterpret_cast<const unsigned char*>(base + lay.rt + sr.mis());
+        const unsigned char* s_rt = s_rtc + r0;
         const float* X = reinterpret_cast<const float*>(base + lay.x + sx.mis());
         const float* G = reinterpret_cast<const float*>(base + lay.g + sg.mis());
 
@@ -733,14 +753,18 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
         cpx = rx; cpy = ry; cpz = rz;
         float* s_go = reinterpret_cast<float*>(s_go_base);  // [n][8], 16-B aligned rows when dst is
 
-        // residue pass: chi gradients and residue sums about CA
+        // residue pass: chi gradients, residue sums about CA, and the backbone
+        // positions the gradient pass needs (the staging is released after it)
         float RA[RPT][6], RN[RPT][6], RC[RPT][6];
+        float PN[RPT][3], PCA[RPT][3], PC[RPT][3], PNX[RPT][3];  // N, CA, C, next residue's N
         float thr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         int off = off0;
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
 #pragma unroll
             for (int c = 0; c < 6; ++c) RA[q][c] = RN[q][c] = RC[q][c] = 0.f;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) PN[q][c] = PCA[q][c] = PC[q][c] = PNX[q][c] = 0.f;
             const int rl = rl0 + q;
             if (rl < n) {
                 const FAType& T = s_types[typ[q]];
@@ -750,6 +774,19 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
 #pragma unroll
                 for (int c = 3; c < 8; ++c) go[c] = 0.f;
                 const float cx = x[3 * T.iCA], cy = x[3 * T.iCA + 1], cz = x[3 * T.iCA + 2];
+                PCA[q][0] = cx; PCA[q][1] = cy; PCA[q][2] = cz;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    PN[q][c] = x[3 * T.iN + c];
+                    PC[q][c] = x[3 * T.iC + c];
+                }
+                const int j = r0 + rl;
+                if (j + 1 < L) {  // N of the next residue: in this tile, or the first of the later tile
+                    const int iN = s_types[s_rtc[j + 1]].iN;
+                    const float* xn = rl + 1 < n ? x + 3 * T.n_atoms : xb + (size_t)s_off[t + 1] * 3;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) PNX[q][c] = xn[3 * iN + c];
+                }
                 auto acc = [&](float* s6, int i) {
                     cross_acc(s6, x[3 * i] - cx, x[3 * i + 1] - cy, x[3 * i + 2] - cz, g[3 * i], g[3 * i + 1],
                               g[3 * i + 2]);
@@ -788,26 +825,25 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
         }
         float suf[6], tot6[6];
         block_exclusive_suffix6<NT>(thr, carry6, s_suf, suf, tot6);
+        // every thread is past the residue pass: the single buffer may refill
+        if (!kDB && tid == 0 && t > 0) issue(t - 1, 0);
 
-        // backbone gradients, residues last to first
+        // backbone gradients, residues last to first (registers only)
 #pragma unroll
         for (int q = RPT - 1; q >= 0; --q) {
             const int rl = rl0 + q;
             const int j = r0 + rl;
             if (rl < n) {
-                const FAType& T = s_types[typ[q]];
-                off -= T.n_atoms;
-                const float* x = X + 3 * off;
                 float* go = s_go + 8 * rl;
-                const float cx = x[3 * T.iCA], cy = x[3 * T.iCA + 1], cz = x[3 * T.iCA + 2];
+                const float cx = PCA[q][0], cy = PCA[q][1], cz = PCA[q][2];
                 const float dx = cx - rx, dy = cy - ry, dz = cz - rz;
                 float aft[6];  // later residues, moment about CA_j
                 aft[0] = suf[0]; aft[1] = suf[1]; aft[2] = suf[2];
                 aft[3] = suf[3] - fmaf(dy, suf[2], -dz * suf[1]);
                 aft[4] = suf[4] - fmaf(dz, suf[0], -dx * suf[2]);
                 aft[5] = suf[5] - fmaf(dx, suf[1], -dy * suf[0]);
-                const float nx = x[3 * T.iN], ny = x[3 * T.iN + 1], nz = x[3 * T.iN + 2];
-                const float kx = x[3 * T.iC], ky = x[3 * T.iC + 1], kz = x[3 * T.iC + 2];
+                const float nx = PN[q][0], ny = PN[q][1], nz = PN[q][2];
+                const float kx = PC[q][0], ky = PC[q][1], kz = PC[q][2];
                 float s6[6];
                 // psi_j
 #pragma unroll
@@ -826,17 +862,7 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
                 // omega_j: C_j -> N_{j+1}, later residues
                 float gw = 0.f;
                 if (j + 1 < L) {
-                    const float* xn;
-                    int tn;
-                    if (rl + 1 < n) {
-                        tn = s_rt[rl + 1];
-                        xn = x + 3 * T.n_atoms;
-                    } else {  // first residue of the later tile
-                        tn = __ldg(rtb + j + 1);
-                        xn = xb + (size_t)s_off[t + 1] * 3;
-                    }
-                    const int iN = s_types[tn].iN;
-                    const float px = xn[3 * iN], py = xn[3 * iN + 1], pz = xn[3 * iN + 2];
+                    const float px = PNX[q][0], py = PNX[q][1], pz = PNX[q][2];
                     const float ux = px - kx, uy = py - ky, uz = pz - kz;
                     gw = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) *
                          axis_moment(ux, uy, uz, px - cx, py - cy, pz - cz, aft);
@@ -919,27 +945,32 @@ static cudaError_t fa_bwd(const FAArgs& a, cudaStream_t st) {
     return launch_pdl(k, a.B, kFABwdThreads, sm, st, a, a.max_atoms);
 }
 
-// TPL_FAX=NTxRPT (tuning) or 128 x 1.
-static void fax_shape(int* nt, int* rpt) {
-    static int env_nt = -1, env_rpt = 0;
-    if (env_nt < 0) {
-        env_nt = 0;
+// TPL_FAX=NTxRPTxDBxTS (tuning) or the default.
+struct FAXShape {
+    int nt, rpt, db, ts;
+};
+static FAXShape fax_shape(int B) {
+    static FAXShape env{-1, 0, 0, 0};
+    if (env.nt < 0) {
+        env = {0, 0, 0, 0};
         if (const char* e = std::getenv("TPL_FAX")) {
-            int x = 0, r = 0;
-            if (std::sscanf(e, "%dx%d", &x, &r) == 2) { env_nt = x; env_rpt = r; }
+            FAXShape s{0, 1, 0, 0};
+            if (std::sscanf(e, "%dx%dx%dx%d", &s.nt, &s.rpt, &s.db, &s.ts) >= 2) env = s;
         }
     }
-    *nt = env_nt ? env_nt : 128;
-    *rpt = env_nt ? env_rpt : 1;
+    if (env.nt) return env;
+    // measured (tools/gpu_fax.sh): single buffer + table through L1 (more resident
+    // CTAs) wins; few chains -> long tiles (latency), many chains -> 64 threads
+    return B <= 2 * 148 ? FAXShape{256, 1, 0, 0} : FAXShape{64, 1, 0, 0};
 }
 
-template <int NT, int RPT>
+template <int NT, int RPT, bool DB, bool TS>
 static cudaError_t fa_bwd_xyz(const FAArgs& a, cudaStream_t st) {
-    auto k = fa_backward_xyz_kernel<NT, RPT>;
+    auto k = fa_backward_xyz_kernel<NT, RPT, DB, TS>;
     constexpr int TILE = NT * RPT;
     const int max_tiles = (a.Lmax + TILE - 1) / TILE;
-    const size_t sm = FAXSmem<NT>::kTable + r16(a.n_types * int(sizeof(FAType))) + r16(4 * (max_tiles + 1)) +
-                      2 * fax_tile_layout(TILE, a.max_atoms).total + r16(32 * TILE);
+    const size_t sm = FAXSmem<NT>::kTable + fax_table_bytes(TS, a.n_types) + r16(4 * (max_tiles + 1)) +
+                      r16(16 + a.Lmax) + (DB ? 2 : 1) * fax_tile_layout(TILE, a.max_atoms).total + r16(32 * TILE);
     static size_t configured = 0;
     if (configured < sm) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
@@ -950,14 +981,12 @@ static cudaError_t fa_bwd_xyz(const FAArgs& a, cudaStream_t st) {
 }
 
 cudaError_t fa_backward_xyz_launch(const FAArgs& a, cudaStream_t st) {
-    int nt, rpt;
-    fax_shape(&nt, &rpt);
-    if (nt == 64 && rpt == 1) return fa_bwd_xyz<64, 1>(a, st);
-    if (nt == 64 && rpt == 2) return fa_bwd_xyz<64, 2>(a, st);
-    if (nt == 128 && rpt == 1) return fa_bwd_xyz<128, 1>(a, st);
-    if (nt == 128 && rpt == 2) return fa_bwd_xyz<128, 2>(a, st);
-    if (nt == 256 && rpt == 1) return fa_bwd_xyz<256, 1>(a, st);
-    if (nt == 256 && rpt == 2) return fa_bwd_xyz<256, 2>(a, st);
+    const FAXShape s = fax_shape(a.B);
+#define TPL_FAX(NT_, R_, DB_, TS_) \
+    if (s.nt == NT_ && s.rpt == R_ && s.db == DB_ && s.ts == TS_) return fa_bwd_xyz<NT_, R_, DB_, TS_>(a, st);
+    TPL_FAX(64, 1, 0, 0) TPL_FAX(128, 1, 0, 0) TPL_FAX(256, 1, 0, 0)
+    TPL_FAX(64, 1, 1, 1) TPL_FAX(128, 1, 1, 1) TPL_FAX(256, 1, 1, 1)
+#undef TPL_FAX
     return cudaErrorInvalidConfiguration;
 }
 

@@ -113,5 +113,6 @@ int fa_tile_for(int Lmax);
 cudaError_t fa_forward_launch(const FAArgs& a, cudaStream_t st);
 cudaError_t fa_backward_launch(const FAArgs& a, cudaStream_t st);
 cudaError_t fa_backward_xyz_launch(const FAArgs& a, cudaStream_t st);  // a.coords is the input
+constexpr int kFAXMaxL = 65536;  // longest chain of the coordinate backward (restype staged on chip)
 
 }  // namespace tpl

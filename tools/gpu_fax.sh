@@ -8,8 +8,8 @@ grep -E "config3|passed|failed|Error|error" gpurun_out/pytest_fa.log | tail -12
 for c in 3 5; do
   for sh in ${SHAPES:-128x1}; do
     echo "config $c TPL_FAX=$sh"
-    TPL_FAX=$sh timeout 600 python bench.py --no-cpu-baseline --no-e2e --config $c --steps ${STEPS:-20} --repeats 3 > gpurun_out/fax_$c_$sh.log 2>&1
-    python - gpurun_out/fax_$c_$sh.log <<'PY'
+    TPL_FAX=$sh timeout 600 python bench.py --no-cpu-baseline --no-e2e --config $c --steps ${STEPS:-20} --repeats 3 > gpurun_out/fax_${c}_$sh.log 2>&1
+    python - gpurun_out/fax_${c}_$sh.log <<'PY'
 import json, sys
 for ln in open(sys.argv[1]):
     if ln.startswith("{"):
