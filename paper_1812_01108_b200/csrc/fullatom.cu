@@ -98,8 +98,10 @@ __device__ __forceinline__ void fa_chunk(const float* s_ang, int rl0, int r0, in
     }
 }
 
-template <int NT, int RPT, int kNS>
-__global__ void __launch_bounds__(NT, 2) fa_forward_kernel(FAArgs a, int stage_atoms_per_res) {
+// kTS: residue table staged in shared memory (else read through L1);
+// kMinB: __launch_bounds__ min blocks (register budget).  TPL_FAF tunes them.
+template <int NT, int RPT, int kNS, bool kTS = true, int kMinB = 2>
+__global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int stage_atoms_per_res) {
     constexpr int TILE = NT * RPT;
     using S = FASmem<NT>;
     using Lay = FALayout<NT, RPT>;
@@ -109,8 +111,8 @@ __global__ void __launch_bounds__(NT, 2) fa_forward_kernel(FAArgs a, int stage_a
     int* s_int = reinterpret_cast<int*>(smem + S::kInt);
     float* s_total = reinterpret_cast<float*>(smem + S::kTotal);
     int* s_misc = reinterpret_cast<int*>(smem + S::kMisc);
-    const FAType* s_types = reinterpret_cast<const FAType*>(smem + S::kTable);
-    char* s_ang_base = smem + S::kTable + r16(a.n_types * int(sizeof(FAType)));
+    const FAType* __restrict__ s_types = kTS ? reinterpret_cast<const FAType*>(smem + S::kTable) : a.types;
+    char* s_ang_base = smem + S::kTable + (kTS ? r16(a.n_types * int(sizeof(FAType))) : 0);
     char* s_rt_base = s_ang_base + Lay::ang_bytes;
     char* s_out_base = s_rt_base + Lay::rt_bytes;
 
@@ -122,15 +124,19 @@ __global__ void __launch_bounds__(NT, 2) fa_forward_kernel(FAArgs a, int stage_a
         fence_barrier_init();
         // the residue table is immutable after tpl_tables_create: it may be
         // fetched before pdl_wait, overlapping the previous kernel's tail
-        const unsigned tb = unsigned(a.n_types * sizeof(FAType));
-        mbar_arrive_expect_tx(bar, tb);
-        bulk_g2s(smem + S::kTable, a.types, tb, bar);
+        if (kTS) {
+            const unsigned tb = unsigned(a.n_types * sizeof(FAType));
+            mbar_arrive_expect_tx(bar, tb);
+            bulk_g2s(smem + S::kTable, a.types, tb, bar);
+        }
     }
     pdl_wait();  // the dependent launches when this grid exits (early triggers cost SM slots)
     const int L = a.lengths[b];
     __syncthreads();
-    mbar_wait(bar, phase);  // also before any early exit: no bulk copy may outlive the CTA
-    phase ^= 1u;
+    if (kTS) {
+        mbar_wait(bar, phase);  // also before any early exit: no bulk copy may outlive the CTA
+        phase ^= 1u;
+    }
     if (L < 1 || L > a.Lmax) {
         if (tid == 0) atomicOr(a.err, ERR_LENGTH);
         return;
@@ -908,10 +914,10 @@ int fa_rpt_for(int) { return kFABwdRPT; }
 int fa_tile_for(int) { return kFABwdThreads * kFABwdRPT; }  // backward tile: sizes the workspace prefixes
 
 template <int NT, int RPT>
-static size_t fa_fwd_smem(int n_types, int max_atoms) {
+static size_t fa_fwd_smem(int n_types, int max_atoms, bool ts = true) {
     using S = FASmem<NT>;
     using Lay = FALayout<NT, RPT>;
-    return S::kTable + r16(n_types * int(sizeof(FAType))) + Lay::ang_bytes + Lay::rt_bytes +
+    return S::kTable + (ts ? r16(n_types * int(sizeof(FAType))) : 0) + Lay::ang_bytes + Lay::rt_bytes +
            r16(16 + 12 * max_atoms * Lay::TILE);
 }
 template <int NT, int RPT>
@@ -920,17 +926,45 @@ static size_t fa_bwd_smem(int n_types, int max_atoms) {
     return fa_fwd_smem<NT, RPT>(n_types, max_atoms) + Lay::go_bytes;
 }
 
-template <int NS>
-static cudaError_t fa_fwd(const FAArgs& a, cudaStream_t st) {
-    auto k = fa_forward_kernel<kFAFwdThreads, kFAFwdRPT, NS>;
-    const size_t sm = fa_fwd_smem<kFAFwdThreads, kFAFwdRPT>(a.n_types, a.max_atoms);
+template <int NT, int NS, bool TS, int MINB>
+static cudaError_t fa_fwd_v(const FAArgs& a, cudaStream_t st) {
+    auto k = fa_forward_kernel<NT, 1, NS, TS, MINB>;
+    const size_t sm = fa_fwd_smem<NT, 1>(a.n_types, a.max_atoms, TS);
     static size_t configured = 0;  // set the smem opt-in once per size (not inside graph capture)
     if (configured < sm) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
         configured = sm;
     }
-    return launch_pdl(k, a.B, kFAFwdThreads, sm, st, a, a.max_atoms);
+    return launch_pdl(k, a.B, NT, sm, st, a, a.max_atoms);
+}
+// TPL_FAF=NTxTSxMINB (tuning) or the default.
+struct FAFShape {
+    int nt, ts, minb;
+};
+static FAFShape faf_shape(int B) {
+    static FAFShape env{-1, 0, 0};
+    if (env.nt < 0) {
+        env = {0, 0, 0};
+        if (const char* e = std::getenv("TPL_FAF")) {
+            FAFShape s{0, 1, 2};
+            if (std::sscanf(e, "%dx%dx%d", &s.nt, &s.ts, &s.minb) == 3) env = s;
+        }
+    }
+    if (env.nt) return env;
+    // measured (tools/gpu_faf.sh): few chains -> 256 threads, table in shared
+    // memory; many chains -> 128 threads, table through L1, 6 CTAs/SM
+    return B <= 2 * 148 ? FAFShape{256, 1, 2} : FAFShape{128, 0, 6};
+}
+template <int NS>
+static cudaError_t fa_fwd(const FAArgs& a, cudaStream_t st) {
+    const FAFShape s = faf_shape(a.B);
+#define TPL_FAF(NT_, TS_, MB_) \
+    if (s.nt == NT_ && s.ts == TS_ && s.minb == MB_) return fa_fwd_v<NT_, NS, TS_, MB_>(a, st);
+    TPL_FAF(256, 1, 2) TPL_FAF(256, 0, 2) TPL_FAF(256, 0, 3) TPL_FAF(256, 1, 3)
+    TPL_FAF(128, 1, 4) TPL_FAF(128, 0, 4) TPL_FAF(128, 0, 6) TPL_FAF(128, 1, 6)
+#undef TPL_FAF
+    return cudaErrorInvalidConfiguration;
 }
 template <int NS>
 static cudaError_t fa_bwd(const FAArgs& a, cudaStream_t st) {
