@@ -49,7 +49,8 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=10)
-    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference", "paper"],
+                   help="paper: the paper's own GPU design (SURVEY f3; saved M_i + O(L^2) backward), backbone only")
     p.add_argument("--config", default="metric")
     p.add_argument("--repeats", type=int, default=7, help="timed regions of K steps; the median is reported")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -222,6 +223,31 @@ class BackboneWork:
                 "L": self.Lmax, "batch_per_gpu": self.B}
 
 
+class PaperBackboneWork(BackboneWork):
+    """the paper's GPU design on the same workload -- forward saves M_i
+    (64 B/atom), backward sums Eq. 2 per angle without a reduction."""
+
+    def alloc_set(self, ws_bytes):
+        from paper_1812_01108_b200 import _abi
+
+        s = super().alloc_set(ws_bytes)
+        s["M"] = torch.empty(_abi.tpl_paper_backbone_saved_floats(self.B, self.Lmax), device="cuda")
+        return s
+
+    def footprint(self):
+        return super().footprint() + self.B * self.Lmax * 3 * 64
+
+    def fwd(self, s, stream=None):
+        from paper_1812_01108_b200 import _abi
+
+        _abi.tpl_paper_backbone_forward(s["angles"], s["lengths"], s["coords"], s["M"], s["ws"], stream)
+
+    def bwd(self, s, stream=None):
+        from paper_1812_01108_b200 import _abi
+
+        _abi.tpl_paper_backbone_backward(s["angles"], s["lengths"], s["M"], s["grad"], s["gang"], s["ws"], stream)
+
+
 class FullAtomWork:
     model = "fullatom"
 
@@ -293,7 +319,11 @@ class FullAtomWork:
                 "atoms_per_gpu": self.atoms}
 
 
-def make_work(c, rank, world=1, strong=False):
+def make_work(c, rank, world=1, strong=False, paper=False):
+    if paper:
+        if synth.CONFIGS[c]["model"] != "backbone":
+            raise SystemExit("--impl paper: the paper's GPU design is the backbone model (its full atom ran on CPU)")
+        return PaperBackboneWork(c, rank, world, strong)
     cls = BackboneWork if synth.CONFIGS[c]["model"] == "backbone" else FullAtomWork
     return cls(c, rank, world, strong)
 
@@ -337,7 +367,7 @@ def run_ours(args):
 
     world, rank, local, dist = dist_setup(args)
     c = cfg_key(args.config)
-    work = make_work(c, rank, world, args.scaling == "strong")
+    work = make_work(c, rank, world, args.scaling == "strong", paper=args.impl == "paper")
     props = torch.cuda.get_device_properties(local)
     l2 = getattr(props, "L2_cache_size", 126 * 2 ** 20)
     n_sets = max(2, math.ceil(4 * l2 / work.footprint()))
@@ -451,7 +481,7 @@ def run_ours(args):
             "step_frac": (ab["fwd"] + ab["bwd"]) / (ms_step * 1e-3) / 1e9 / peak}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.impl != "paper":
         cpu = cpu_baseline(work, args.cpu_seconds)
 
     if rank == 0:
@@ -465,7 +495,7 @@ def run_ours(args):
                "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
                "dtype": "f32", "data": "synthetic (seeded uniform angles, N(0,1) dL/dr)", "config": cfgd,
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": 2 * K,
-               "impl": "ours"}
+               "impl": "paper_gpu_design" if args.impl == "paper" else "ours"}
         print(json.dumps(out))
     if dist is not None:
         dist.destroy_process_group()

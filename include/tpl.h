@@ -136,6 +136,23 @@ TPL_API tpl_status tpl_backbone_backward_from_coords(const float* coords, const 
                                              int32_t Lmax, const float* grad_coords, float* grad_angles,
                                              void* workspace, size_t ws_bytes, void* stream);
 
+/* the paper's own GPU design, built as a measured comparison
+ * point (not the product path).  Forward: one thread per chain saves every
+ * cumulative transform M_i = R_0...R_i as a row-major 4x4 fp32
+ * (64 B/atom) plus r_i.  Backward: one thread per (chain, angle) evaluates
+ * sum_{i>=a} g_i . (M_{a-1} dR_a M_a^{-1} M_i 0) (Eq. 2) without a
+ * reduction: O(L^2) per chain.  Same readings (Q1, Q2) and outputs as
+ * the product pair.
+ *   saved_M [B][3*Lmax][16] fp32, 16-byte aligned, written by the forward and
+ *           read by the backward; tpl_paper_backbone_saved_floats(B, Lmax) floats */
+TPL_API int64_t tpl_paper_backbone_saved_floats(int32_t B, int32_t Lmax);
+TPL_API tpl_status tpl_paper_backbone_forward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                      float* coords, float* saved_M, void* workspace, size_t ws_bytes,
+                                      void* stream);
+TPL_API tpl_status tpl_paper_backbone_backward(const float* angles, const int32_t* lengths, int32_t B,
+                                       int32_t Lmax, const float* saved_M, const float* grad_coords,
+                                       float* grad_angles, void* workspace, size_t ws_bytes, void* stream);
+
 /* ======================================================================
  * Full-atom model (§2)
  * ====================================================================== */

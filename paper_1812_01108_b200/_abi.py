@@ -31,6 +31,7 @@ EXPORTS = [
     "tpl_tables_n_types", "tpl_fullatom_atoms", "tpl_fullatom_forward", "tpl_fullatom_backward",
     "tpl_fullatom_backward_from_coords", "tpl_tables_backward_from_coords_ok",
     "tpl_lrmsd_forward", "tpl_lrmsd_backward",
+    "tpl_paper_backbone_saved_floats", "tpl_paper_backbone_forward", "tpl_paper_backbone_backward",
 ]
 
 
@@ -94,6 +95,12 @@ def _load():
     L.tpl_fullatom_backward_from_coords.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]
     L.tpl_tables_backward_from_coords_ok.restype = i32
     L.tpl_tables_backward_from_coords_ok.argtypes = [vp]
+    L.tpl_paper_backbone_saved_floats.restype = i64
+    L.tpl_paper_backbone_saved_floats.argtypes = [i32, i32]
+    L.tpl_paper_backbone_forward.restype = ctypes.c_int
+    L.tpl_paper_backbone_forward.argtypes = [vp, vp, i32, i32, vp, vp, vp, sz, vp]
+    L.tpl_paper_backbone_backward.restype = ctypes.c_int
+    L.tpl_paper_backbone_backward.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, sz, vp]
     L.tpl_lrmsd_forward.restype = ctypes.c_int
     L.tpl_lrmsd_forward.argtypes = [vp, vp, vp, i32, i32, vp, vp, vp, sz, vp]
     L.tpl_lrmsd_backward.restype = ctypes.c_int
@@ -241,6 +248,38 @@ def tpl_fullatom_backward_from_coords(handle, coords, restype, lengths, grad_coo
 
 def tpl_tables_backward_from_coords_ok(handle):
     return bool(lib.tpl_tables_backward_from_coords_ok(ctypes.c_void_p(handle)))
+
+
+def tpl_paper_backbone_saved_floats(B, Lmax):
+    return int(lib.tpl_paper_backbone_saved_floats(int(B), int(Lmax)))
+
+
+def tpl_paper_backbone_forward(angles, lengths, coords, saved_M, workspace, stream=None):
+    """the paper's GPU design (saves M_i, 64 B/atom) -- a comparison point."""
+    B, Lmax, three = angles.shape
+    if three != BB_SLOTS or tuple(coords.shape) != (B, 3 * Lmax, 3) or saved_M.numel() != 48 * B * Lmax:
+        raise ValueError("shapes: angles [B,Lmax,3], coords [B,3*Lmax,3], saved_M [B,3*Lmax,16]")
+    _check(lib.tpl_paper_backbone_forward(_dev(angles, torch.float32, "angles"),
+                                          _dev(lengths, torch.int32, "lengths"), B, Lmax,
+                                          _dev(coords, torch.float32, "coords"),
+                                          _dev(saved_M, torch.float32, "saved_M"),
+                                          _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                          _stream(stream)))
+
+
+def tpl_paper_backbone_backward(angles, lengths, saved_M, grad_coords, grad_angles, workspace, stream=None):
+    """O(L^2) per-angle sums without a reduction."""
+    B, Lmax, three = angles.shape
+    if (three != BB_SLOTS or tuple(grad_coords.shape) != (B, 3 * Lmax, 3)
+            or tuple(grad_angles.shape) != (B, Lmax, 3) or saved_M.numel() != 48 * B * Lmax):
+        raise ValueError("shapes: angles/grad_angles [B,Lmax,3], grad_coords [B,3*Lmax,3], saved_M [B,3*Lmax,16]")
+    _check(lib.tpl_paper_backbone_backward(_dev(angles, torch.float32, "angles"),
+                                           _dev(lengths, torch.int32, "lengths"), B, Lmax,
+                                           _dev(saved_M, torch.float32, "saved_M"),
+                                           _dev(grad_coords, torch.float32, "grad_coords"),
+                                           _dev(grad_angles, torch.float32, "grad_angles"),
+                                           _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                           _stream(stream)))
 
 
 def tpl_lrmsd_forward(x, y, n_atoms, lrmsd, state, workspace, stream=None):

@@ -225,6 +225,51 @@ tpl_status tpl_backbone_backward_from_coords(const float* coords, const int32_t*
     return TPL_OK;
 }
 
+// ---------------------------------------------------------------- f3: the paper's GPU design
+int64_t tpl_paper_backbone_saved_floats(int32_t B, int32_t Lmax) {
+    return (B < 1 || Lmax < 1) ? 0 : static_cast<int64_t>(B) * 3 * Lmax * 16;
+}
+
+tpl_status tpl_paper_backbone_forward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                      float* coords, float* saved_M, void* workspace, size_t ws_bytes, void* stream) {
+    tpl_status s = bb_common(angles, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!coords || !saved_M) return fail(TPL_ERR_NULL, "coords/saved_M is NULL");
+    if (!aligned4(coords) || (reinterpret_cast<uintptr_t>(saved_M) & 15u))
+        return fail(TPL_ERR_ALIGN, "coords not 4-byte or saved_M not 16-byte aligned");
+    BBArgs a{};
+    a.angles = angles;
+    a.lengths = lengths;
+    a.B = B;
+    a.Lmax = Lmax;
+    a.coords = coords;
+    a.err = static_cast<unsigned*>(workspace);
+    cudaError_t e = paper_bb_forward_launch(a, saved_M, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "paper-design backbone forward launch");
+    return TPL_OK;
+}
+
+tpl_status tpl_paper_backbone_backward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                       const float* saved_M, const float* grad_coords, float* grad_angles,
+                                       void* workspace, size_t ws_bytes, void* stream) {
+    tpl_status s = bb_common(angles, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!saved_M || !grad_coords || !grad_angles) return fail(TPL_ERR_NULL, "saved_M/grad_coords/grad_angles is NULL");
+    if (!aligned4(grad_coords) || !aligned4(grad_angles) || !aligned4(saved_M))
+        return fail(TPL_ERR_ALIGN, "pointers not 4-byte aligned");
+    BBArgs a{};
+    a.angles = angles;
+    a.lengths = lengths;
+    a.B = B;
+    a.Lmax = Lmax;
+    a.grad_coords = grad_coords;
+    a.grad_angles = grad_angles;
+    a.err = static_cast<unsigned*>(workspace);
+    cudaError_t e = paper_bb_backward_launch(a, saved_M, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "paper-design backbone backward launch");
+    return TPL_OK;
+}
+
 // ---------------------------------------------------------------- tables
 static int owner_rank(int owner, int n_groups) {
     if (owner == TPL_OWNER_N) return 0;

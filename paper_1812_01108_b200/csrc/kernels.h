@@ -50,6 +50,9 @@ int bb_tile_for(int Lmax);
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st);  // a.coords is the input
+// the paper's own GPU design (paper_baseline.cu), a comparison point
+cudaError_t paper_bb_forward_launch(const BBArgs& a, float* Msave, cudaStream_t st);
+cudaError_t paper_bb_backward_launch(const BBArgs& a, const float* Msave, cudaStream_t st);
 
 // ---- full atom -------------------------------------------------------------
 // Device residue-type table (fp32, uploaded once by tpl_tables_create).
