@@ -119,8 +119,63 @@ struct BBIter {
     __device__ int n() const { return min(tile, L - t * tile); }
 };
 
+// ---------------------------------------------------------------------------
+// Work items of the decoupled ("DL") kernels: every (chain, tile) pair is an
+// item, i = b * max_tiles + (fwd ? t : max_tiles - 1 - t), dealt round-robin
+// to a co-resident persistent grid.  An item only waits for items with a
+// smaller index (earlier tiles in the forward, later tiles in the backward),
+// so the smallest unfinished item can always proceed: tiles of one chain run
+// on different SMs at the same time and exchange only their aggregates.
+struct DLIter {
+    const int* lengths;
+    int B, Lmax, tile, max_tiles, stride;
+    bool fwd;
+    unsigned* err;
+    int i, b, L, t, nt;
+    bool valid;
+    static constexpr int phase = 1;  // for bb_issue: a backward item always loads dL/dr
+
+    __device__ void settle() {
+        const int n_items = B * max_tiles;
+        int cb = -1, cL = 0;
+        for (; i < n_items; i += stride) {
+            const int bb = i / max_tiles, tr = i - bb * max_tiles;
+            if (bb != cb) {
+                cb = bb;
+                cL = __ldg(lengths + bb);
+            }
+            if (cL < 1 || cL > Lmax) {
+                if (tr == 0 && threadIdx.x == 0) atomicOr(err, ERR_LENGTH);
+                continue;
+            }
+            const int ntt = (cL + tile - 1) / tile;
+            const int tt = fwd ? tr : max_tiles - 1 - tr;
+            if (tt < ntt) {
+                b = bb;
+                L = cL;
+                t = tt;
+                nt = ntt;
+                valid = true;
+                return;
+            }
+        }
+        valid = false;
+    }
+    __device__ void init() {
+        i = blockIdx.x;
+        settle();
+    }
+    __device__ void advance() {
+        i += stride;
+        settle();
+    }
+    __device__ int r0() const { return t * tile; }
+    __device__ int n() const { return min(tile, L - t * tile); }
+};
+
 // Issue (thread 0) the bulk copies of one work item into buffer `buf`.
-__device__ __forceinline__ void bb_issue(const BBIter& it, const float* angles, const float* grad_coords,
+template <typename It>
+__device__ __forceinline__ void bb_issue(const It& it, const float* angles, const float* grad_coords,
                                          char* s_ang, char* s_g, uint64_t* bar) {
     const int r0 = it.r0(), n = it.n(), pre = r0 > 0 ? 1 : 0;
     const Span sa = make_span(angles + ((size_t)it.b * it.Lmax + r0 - pre) * 3, (n + pre) * 12);
@@ -253,6 +308,143 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
     // dependent's griddepcontrol.wait) covers visibility of the global writes.
     if (tid == 0) bulk_wait_read_all();
     TPL_STAMP(9);
+}
+
+// Decoupled forward: each (chain, tile) item scans its tile from the identity,
+// publishes the tile aggregate A_t (unless it is the chain's last tile) and
+// takes its prefix C_t = N(...N(N(A_0) A_1)... A_{t-1}) from the published
+// aggregates in a fixed order (bitwise deterministic; N = Newton-Schulz).
+// Slots: [B][max_tiles] x 16 floats (12 payload + flag) after the header.
+template <int NT, int RPT, int kNS>
+__global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_dl_kernel(const float* __restrict__ angles,
+                                                           const int* __restrict__ lengths, int B, int Lmax,
+                                                           float* __restrict__ coords, unsigned* __restrict__ hdr,
+                                                           float* __restrict__ slots, int max_tiles) {
+    constexpr int TILE = NT * RPT;
+    constexpr int ANG = round16(16 + 12 * (TILE + 1));
+    using S = BBSmem<NT>;
+    extern __shared__ __align__(16) char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
+    float* scratch = reinterpret_cast<float*>(smem + S::kScratch);
+    float* s_total = reinterpret_cast<float*>(smem + S::kTotal);
+    float* s_pre = reinterpret_cast<float*>(smem + S::kMisc);  // the tile's prefix C_t
+    char* s_ang_buf = smem + S::kData;  // 2 x ANG
+    char* s_out_base = s_ang_buf + 2 * ANG;
+
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        fence_barrier_init();
+    }
+    pdl_wait();
+    const unsigned fv = launch_epoch(hdr) + 1u;
+    DLIter it{lengths, B, Lmax, TILE, max_tiles, int(gridDim.x), true, hdr};
+    it.init();
+    __syncthreads();
+    if (tid == 0 && it.valid) bb_issue(it, angles, nullptr, s_ang_buf, nullptr, bar);
+
+    unsigned phases = 0;
+    const int rl0 = tid * RPT;
+    for (int k = 0; it.valid; ++k) {
+        const int buf = k & 1;
+        const int b = it.b, r0 = it.r0(), n = it.n(), t = it.t, pre = r0 > 0 ? 1 : 0;
+        DLIter nx = it;
+        nx.advance();
+        if (tid == 0 && nx.valid) bb_issue(nx, angles, nullptr, s_ang_buf + (buf ^ 1) * ANG, nullptr, bar + (buf ^ 1));
+        char* s_ang_base = s_ang_buf + buf * ANG;
+        const Span sa = make_span(angles + ((size_t)b * Lmax + r0 - pre) * 3, (n + pre) * 12);
+        span_load_edges_f32(sa, s_ang_base);
+        const Span so = make_span(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3, n * 36);
+        float* s_out = reinterpret_cast<float*>(s_out_base + so.mis());
+        mbar_wait(bar + buf, (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+        __syncthreads();
+        const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 3 * pre;
+
+        Aff M;
+        const int nq = max(0, min(RPT, n - rl0));
+        float px[3 * RPT], py[3 * RPT], pz[3 * RPT];
+        float maxabs = 0.f;
+        auto pass1 = [&](auto slow) {
+            constexpr bool kSlow = decltype(slow)::value;
+            M = aff_identity();
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                if (q < nq) {
+                    const int rl = rl0 + q;
+                    float c[3], s[3];
+                    bb_residue_trig<kSlow>(s_ang, rl, r0 + rl, c, s, &maxabs);
+                    if (r0 + rl > 0) aff_bond_bb<0>(M, c[0], s[0]);
+                    px[3 * q] = M.t0; py[3 * q] = M.t1; pz[3 * q] = M.t2;
+                    aff_bond_bb<1>(M, c[1], s[1]);
+                    px[3 * q + 1] = M.t0; py[3 * q + 1] = M.t1; pz[3 * q + 1] = M.t2;
+                    aff_bond_bb<2>(M, c[2], s[2]);
+                    px[3 * q + 2] = M.t0; py[3 * q + 2] = M.t1; pz[3 * q + 2] = M.t2;
+                }
+            }
+        };
+        pass1(std::false_type{});
+        if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
+        if (kNS >= 1) aff_orthonormalize(M);
+        if (tid == 0) bulk_wait_read_all();  // the output staging is free again
+        Aff P = block_exclusive_scan<NT, kNS>(M, aff_identity(), scratch, s_total);  // tile-local prefix
+        if (t > 0 || it.nt > 1) {
+            if (tid == 0) {
+                float* slot = slots + ((size_t)b * max_tiles + t) * 16;
+                if (t + 1 < it.nt) {  // publish A_t for the later tiles
+#pragma unroll
+                    for (int q = 0; q < 12; ++q) slot[q] = s_total[q];
+                    __threadfence();
+                    st_release_gpu(reinterpret_cast<unsigned*>(slot + 12), fv);
+                }
+                Aff C = aff_identity();
+                for (int u = 0; u < t; ++u) {  // fixed order: deterministic rounding
+                    const float* su = slots + ((size_t)b * max_tiles + u) * 16;
+                    wait_flag(reinterpret_cast<const unsigned*>(su + 12), fv);
+                    Aff A;
+                    A.r00 = __ldcg(su + 0); A.r01 = __ldcg(su + 1); A.r02 = __ldcg(su + 2); A.t0 = __ldcg(su + 3);
+                    A.r10 = __ldcg(su + 4); A.r11 = __ldcg(su + 5); A.r12 = __ldcg(su + 6); A.t1 = __ldcg(su + 7);
+                    A.r20 = __ldcg(su + 8); A.r21 = __ldcg(su + 9); A.r22 = __ldcg(su + 10); A.t2 = __ldcg(su + 11);
+                    C = aff_compose(C, A);
+                    if (kNS >= 1) aff_orthonormalize(C);
+                }
+                store_aff(s_pre, C);
+            }
+            __syncthreads();
+            if (t > 0) {
+                P = aff_compose(load_aff(s_pre), P);
+                if (kNS >= 1) aff_orthonormalize(P);
+            }
+        }
+        if (!nx.valid) pdl_trigger();
+
+        // pass 2: prefix applied, positions to the output staging buffer
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            if (q < nq) {
+                float* o = s_out + 9 * (rl0 + q);
+#pragma unroll
+                for (int kk = 0; kk < 3; ++kk) {
+                    const int a = 3 * q + kk;
+                    apply(P, px[a], py[a], pz[a], o[3 * kk], o[3 * kk + 1], o[3 * kk + 2]);
+                }
+            }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            span_store_bulk(so, s_out_base);
+            bulk_commit();
+        }
+        span_store_edges_f32(so, s_out_base);
+        it = nx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        bulk_wait_read_all();
+        finish_epoch(hdr);
+    }
 }
 
 template <int NT, int RPT, int kNS>
@@ -646,6 +838,195 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
     if (tid == 0) bulk_wait_read_all();
 }
 
+// Decoupled coordinate backward: every (chain, tile) item sums its tile, publishes
+// (S_t, T_t about c_t, c_t) unless it is the chain's first tile, and adds the
+// later tiles' totals (fixed order, moved to its own reference) as its carry.
+// omega of the tile's last residue is computed here from the next tile's first
+// atom N: its own term drops out of e . (T - (r_N - c) x S) (zero lever arm).
+template <int NT, int RPT>
+__global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_dl_kernel(
+    const float* __restrict__ coords, const int* __restrict__ lengths, int B, int Lmax,
+    const float* __restrict__ grad_coords, float* __restrict__ grad_angles, unsigned* __restrict__ hdr,
+    float* __restrict__ slots, int max_tiles) {
+    constexpr int TILE = NT * RPT;
+    constexpr int XB = round16(16 + 36 * TILE + 24);  // the previous atom, the tile, the next atom
+    constexpr int GB = round16(16 + 36 * TILE);
+    using S = BBSmem<NT>;
+    extern __shared__ __align__(16) char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
+    float* s_suf = reinterpret_cast<float*>(smem + S::kSuf);
+    float* s_misc = reinterpret_cast<float*>(smem + S::kMisc);  // carry (6)
+    char* s_x_buf = smem + S::kData;   // 2 x XB
+    char* s_g_buf = s_x_buf + 2 * XB;  // 2 x GB
+    char* s_go_base = s_g_buf + 2 * GB;
+
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        fence_barrier_init();
+    }
+    pdl_wait();
+    const unsigned fv = launch_epoch(hdr) + 1u;
+    DLIter it{lengths, B, Lmax, TILE, max_tiles, int(gridDim.x), false, hdr};
+    it.init();
+    auto spans = [&](const DLIter& w, Span& sx, Span& sg) {
+        const int r0 = w.r0(), n = w.n(), pre = r0 > 0 ? 1 : 0, post = r0 + n < w.L ? 1 : 0;
+        const size_t base = ((size_t)w.b * 3 * w.Lmax + 3 * (size_t)r0) * 3;
+        sx = make_span(coords + base - 3 * pre, (3 * n + pre + post) * 12);
+        sg = make_span(grad_coords + base, n * 36);
+    };
+    auto issue = [&](const DLIter& w, int buf) {
+        Span sx, sg;
+        spans(w, sx, sg);
+        mbar_arrive_expect_tx(bar + buf, unsigned(sx.mid + sg.mid));
+        span_load_bulk(sx, s_x_buf + buf * XB, bar + buf);
+        span_load_bulk(sg, s_g_buf + buf * GB, bar + buf);
+    };
+    __syncthreads();
+    if (tid == 0 && it.valid) issue(it, 0);
+
+    unsigned phases = 0;
+    const int rl0 = tid * RPT;
+    for (int k = 0; it.valid; ++k) {
+        const int buf = k & 1;
+        const int b = it.b, L = it.L, r0 = it.r0(), n = it.n(), t = it.t, pre = r0 > 0 ? 1 : 0;
+        const bool last_tile = r0 + n == L;
+        DLIter nx = it;
+        nx.advance();
+        if (tid == 0 && nx.valid) issue(nx, buf ^ 1);
+        char* s_x_base = s_x_buf + buf * XB;
+        char* s_g_base = s_g_buf + buf * GB;
+        Span sx, sg;
+        spans(it, sx, sg);
+        span_load_edges_f32(sx, s_x_base);
+        span_load_edges_f32(sg, s_g_base);
+        mbar_wait(bar + buf, (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+        __syncthreads();
+        const float* s_x = reinterpret_cast<const float*>(s_x_base + sx.mis()) + 3 * pre;  // atom 0 of the tile
+        const float* s_g = reinterpret_cast<const float*>(s_g_base + sg.mis());
+        const int nq = max(0, min(RPT, n - rl0));
+        const float cx = s_x[0], cy = s_x[1], cz = s_x[2];
+
+        // pass 1: this thread's (S, T) about c
+        float sum6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int a = 0; a < 3 * RPT; ++a) {
+            if (a / 3 < nq) {
+                const float* x = s_x + 9 * rl0 + 3 * a;
+                const float* g = s_g + 9 * rl0 + 3 * a;
+                const float px = x[0] - cx, py = x[1] - cy, pz = x[2] - cz, gx = g[0], gy = g[1], gz = g[2];
+                sum6[0] += gx; sum6[1] += gy; sum6[2] += gz;
+                sum6[3] += fmaf(py, gz, -pz * gy);
+                sum6[4] += fmaf(pz, gx, -px * gz);
+                sum6[5] += fmaf(px, gy, -py * gx);
+            }
+        }
+        if (tid == 0) bulk_wait_read_all();  // the output staging is free again
+        const float zero6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        float su[6], tot6[6];
+        block_exclusive_suffix6<NT>(sum6, zero6, s_suf, su, tot6);  // tile-local
+        if (tid == 0) {
+            float* slot = slots + ((size_t)b * max_tiles + t) * 16;
+            if (t > 0) {  // publish for the earlier tiles
+#pragma unroll
+                for (int q = 0; q < 6; ++q) slot[q] = tot6[q];
+                slot[6] = cx; slot[7] = cy; slot[8] = cz;
+                __threadfence();
+                st_release_gpu(reinterpret_cast<unsigned*>(slot + 12), fv);
+            }
+            float cr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int u = it.nt - 1; u > t; --u) {  // fixed order: deterministic rounding
+                const float* sl = slots + ((size_t)b * max_tiles + u) * 16;
+                wait_flag(reinterpret_cast<const unsigned*>(sl + 12), fv);
+                const float S0 = __ldcg(sl + 0), S1 = __ldcg(sl + 1), S2 = __ldcg(sl + 2);
+                const float dx = __ldcg(sl + 6) - cx, dy = __ldcg(sl + 7) - cy, dz = __ldcg(sl + 8) - cz;
+                cr[0] += S0; cr[1] += S1; cr[2] += S2;
+                cr[3] += __ldcg(sl + 3) + fmaf(dy, S2, -dz * S1);
+                cr[4] += __ldcg(sl + 4) + fmaf(dz, S0, -dx * S2);
+                cr[5] += __ldcg(sl + 5) + fmaf(dx, S1, -dy * S0);
+            }
+#pragma unroll
+            for (int q = 0; q < 6; ++q) s_misc[q] = cr[q];
+        }
+        __syncthreads();
+        float carry[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            carry[q] = s_misc[q];
+            su[q] += carry[q];
+        }
+        if (!nx.valid) pdl_trigger();
+
+        // pass 2: atoms last to first
+        const Span so = make_span(grad_angles + ((size_t)b * Lmax + r0) * 3, n * 12);
+        float* s_go = reinterpret_cast<float*>(s_go_base + so.mis());
+        if (nq > 0 && rl0 + nq == n) {  // omega of the tile's last residue (0 at the chain end)
+            float gw = 0.f;
+            if (!last_tile) {
+                const float* xn = s_x + 9 * n;  // N of the next tile's first residue
+                const float* xc = xn - 3;       // C of this tile's last residue
+                const float ux = xn[0] - xc[0], uy = xn[1] - xc[1], uz = xn[2] - xc[2];
+                const float px = xn[0] - cx, py = xn[1] - cy, pz = xn[2] - cz;
+                const float c0 = carry[3] - fmaf(py, carry[2], -pz * carry[1]);
+                const float c1 = carry[4] - fmaf(pz, carry[0], -px * carry[2]);
+                const float c2 = carry[5] - fmaf(px, carry[1], -py * carry[0]);
+                gw = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * fmaf(ux, c0, fmaf(uy, c1, uz * c2));
+            }
+            s_go[3 * (n - 1) + 2] = gw;
+        }
+#pragma unroll
+        for (int q = RPT - 1; q >= 0; --q) {
+            if (q < nq) {
+                const int rl = rl0 + q;
+                const int j = r0 + rl;
+                float ga[3];
+#pragma unroll
+                for (int kk = 2; kk >= 0; --kk) {
+                    const int a = 3 * rl + kk;
+                    const float* x = s_x + 3 * a;
+                    const float* g = s_g + 3 * a;
+                    const float x0 = x[0], x1 = x[1], x2 = x[2];
+                    const float px = x0 - cx, py = x1 - cy, pz = x2 - cz;
+                    const float gx = g[0], gy = g[1], gz = g[2];
+                    if (j > 0 || kk > 0) {
+                        const float ux = x0 - x[-3], uy = x1 - x[-2], uz = x2 - x[-1];
+                        const float inv = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
+                        const float c0 = su[3] - fmaf(py, su[2], -pz * su[1]);
+                        const float c1 = su[4] - fmaf(pz, su[0], -px * su[2]);
+                        const float c2 = su[5] - fmaf(px, su[1], -py * su[0]);
+                        ga[kk] = inv * fmaf(ux, c0, fmaf(uy, c1, uz * c2));
+                    } else {
+                        ga[kk] = 0.f;
+                    }
+                    su[0] += gx; su[1] += gy; su[2] += gz;
+                    su[3] += fmaf(py, gz, -pz * gy);
+                    su[4] += fmaf(pz, gx, -px * gz);
+                    su[5] += fmaf(px, gy, -py * gx);
+                }
+                s_go[3 * rl + 0] = ga[1];                   // phi_j
+                s_go[3 * rl + 1] = ga[2];                   // psi_j
+                if (rl > 0) s_go[3 * (rl - 1) + 2] = ga[0];  // omega_{j-1} (the previous tile owns rl = 0's)
+            }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            span_store_bulk(so, s_go_base);
+            bulk_commit();
+        }
+        span_store_edges_f32(so, s_go_base);
+        __syncthreads();
+        it = nx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        bulk_wait_read_all();
+        finish_epoch(hdr);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Host-side launch helpers (called from capi.cu).
 
@@ -812,7 +1193,20 @@ static BBShape bbx_shape(int B, int Lmax) {
     return {nt, 5};
 }
 
+static bool dl_enabled(int B, int Lmax);
+static BBShape bbx_dl_shape(int B, int Lmax);
+template <int NT, int RPT>
+static cudaError_t launch_bwd_xyz_dl(const BBArgs& a, cudaStream_t st);
+
 cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
+    if (dl_enabled(a.B, a.Lmax)) {
+        const BBShape d = bbx_dl_shape(a.B, a.Lmax);
+        if (d.nt == 128 && d.rpt == 1) return launch_bwd_xyz_dl<128, 1>(a, st);
+        if (d.nt == 128 && d.rpt == 3) return launch_bwd_xyz_dl<128, 3>(a, st);
+        if (d.nt == 128 && d.rpt == 5) return launch_bwd_xyz_dl<128, 5>(a, st);
+        if (d.nt == 256 && d.rpt == 3) return launch_bwd_xyz_dl<256, 3>(a, st);
+        return cudaErrorInvalidConfiguration;
+    }
     const BBShape s = bbx_shape(a.B, a.Lmax);
 #define TPL_BBX(NT_, R_) \
     if (s.nt == NT_ && s.rpt == R_) return launch_bwd_xyz<NT_, R_>(a, st);
@@ -832,7 +1226,95 @@ extern "C" __attribute__((visibility("default"))) int tpl_debug_stamps_clear(voi
 }
 #endif
 
+// ---- decoupled (DL) kernels: tiles of a chain on different CTAs
+// When to split chains over CTAs.  Measured (tools/gpu_bbx.sh): splitting adds
+// a carry exchange per tile and does not reduce the work of the busiest SM, so
+// it only pays when few long chains would leave SMs idle (f4: 1 x 20000 fwd+bwd
+// 154 -> 42 us, 64 x 2000 23 -> 20 us; 256 x 700 and 4096 x 700 stay
+// chain-serial).  TPL_DL=0/1 forces it.
+static bool dl_enabled(int B, int Lmax) {
+    static int v = -2;
+    if (v == -2) {
+        const char* e = std::getenv("TPL_DL");
+        v = e ? (e[0] == '0' ? 0 : 1) : -1;
+    }
+    if (v >= 0) return v == 1;
+    return B <= 2 * sm_count() && Lmax > 1024;
+}
+static BBShape env_shape(const char* name) {
+    const char* e = std::getenv(name);
+    int nt = 0, r = 0;
+    if (e && std::sscanf(e, "%dx%d", &nt, &r) == 2) return {nt, r};
+    return {0, 0};
+}
+// Forward: 128 threads; residues per thread chosen so that the batch's tiles
+// fill the GPU about twice (small tiles shorten each CTA's serial chain; too
+// small tiles pay the scan once more per residue).  TPL_BBF=NTxRPT overrides.
+static BBShape bbf_dl_shape(int, int) {
+    static const BBShape env = env_shape("TPL_BBF");
+    if (env.nt) return env;
+    return {128, 5};  // measured best of 1/3/5 for 64 x 2000 and 1 x 20000
+}
+int bb_dl_max_tiles(int Lmax) { return (Lmax + 127) / 128; }  // slots: every DL tile has >= 128 residues
+
+template <int NT, int RPT, int NS>
+static cudaError_t launch_fwd_dl(const BBArgs& a, cudaStream_t st) {
+    auto k = bb_forward_dl_kernel<NT, RPT, NS>;
+    const size_t sm = fwd_smem<NT>(RPT);
+    static size_t configured = 0;
+    static int grid_cap = 0;
+    if (configured < sm) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+        configured = sm;
+        grid_cap = persistent_grid(k, NT, sm, 1 << 30);
+    }
+    const int max_tiles = (a.Lmax + NT * RPT - 1) / (NT * RPT);
+    const long items = long(a.B) * max_tiles;
+    const int grid = int(items < grid_cap ? items : grid_cap);  // co-resident: waits only on smaller items
+    return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err, a.ws_prefix,
+                      max_tiles);
+}
+template <int NT, int RPT>
+static cudaError_t launch_bwd_xyz_dl(const BBArgs& a, cudaStream_t st) {
+    auto k = bb_backward_xyz_dl_kernel<NT, RPT>;
+    const int tile = NT * RPT;
+    const size_t sm = BBSmem<NT>::kData + 2 * round16(16 + 36 * tile + 24) + 2 * round16(16 + 36 * tile) +
+                      round16(16 + 12 * tile);
+    static size_t configured = 0;
+    static int grid_cap = 0;
+    if (configured < sm) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+        configured = sm;
+        grid_cap = persistent_grid(k, NT, sm, 1 << 30);
+    }
+    const int max_tiles = (a.Lmax + tile - 1) / tile;
+    const long items = long(a.B) * max_tiles;
+    const int grid = int(items < grid_cap ? items : grid_cap);
+    return launch_pdl(k, grid, NT, sm, st, static_cast<const float*>(a.coords), a.lengths, a.B, a.Lmax,
+                      a.grad_coords, a.grad_angles, a.err, a.ws_prefix, max_tiles);
+}
+// Backward: the same rule with 3 resident CTAs per SM (60 KB of staging each at 128 x 3).
+static BBShape bbx_dl_shape(int, int) {
+    static const BBShape env = env_shape("TPL_BBXD");
+    if (env.nt) return env;
+    return {128, 5};
+}
+
+template <int NS>
+static cudaError_t dispatch_fwd_dl(const BBArgs& a, cudaStream_t st) {
+    const BBShape s = bbf_dl_shape(a.B, a.Lmax);
+    if (s.nt == 128 && s.rpt == 1) return launch_fwd_dl<128, 1, NS>(a, st);
+    if (s.nt == 128 && s.rpt == 3) return launch_fwd_dl<128, 3, NS>(a, st);
+    if (s.nt == 128 && s.rpt == 5) return launch_fwd_dl<128, 5, NS>(a, st);
+    if (s.nt == 128 && s.rpt == 7) return launch_fwd_dl<128, 7, NS>(a, st);
+    if (s.nt == 256 && s.rpt == 3) return launch_fwd_dl<256, 3, NS>(a, st);
+    return cudaErrorInvalidConfiguration;
+}
+
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st) {
+    if (dl_enabled(a.B, a.Lmax)) return a.ns == 0 ? dispatch_fwd_dl<0>(a, st) : dispatch_fwd_dl<1>(a, st);
     return a.ns == 0 ? dispatch<true, 0>(a, st) : dispatch<true, 1>(a, st);
 }
 cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st) {

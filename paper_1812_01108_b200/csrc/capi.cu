@@ -91,6 +91,10 @@ constexpr size_t kWsHeader = 256;  // error word + reserved
 
 int tile_for(int model, int Lmax) { return model == TPL_MODEL_FULLATOM ? fa_tile_for(Lmax) : bb_tile_for(Lmax); }
 int max_tiles_for(int model, int Lmax) {
+    if (model == TPL_MODEL_BACKBONE) {  // the decoupled kernels' tiles (>= 128 residues) need the most slots
+        const int t = tile_for(model, Lmax), old = (Lmax + t - 1) / t, dl = bb_dl_max_tiles(Lmax);
+        return old > dl ? old : dl;
+    }
     const int t = tile_for(model, Lmax);
     return (Lmax + t - 1) / t;
 }
@@ -220,6 +224,8 @@ tpl_status tpl_backbone_backward_from_coords(const float* coords, const int32_t*
     a.grad_coords = grad_coords;
     a.grad_angles = grad_angles;
     a.err = static_cast<unsigned*>(workspace);
+    a.ws_prefix = reinterpret_cast<float*>(static_cast<char*>(workspace) + kWsHeader);  // tile carry slots
+    a.max_tiles = max_tiles_for(TPL_MODEL_BACKBONE, Lmax);
     cudaError_t e = bb_backward_xyz_launch(a, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "backbone backward (from coords) launch");
     return TPL_OK;

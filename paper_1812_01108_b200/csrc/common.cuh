@@ -430,6 +430,37 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// Inter-CTA publication (decoupled tile carries): payload with plain stores,
+// then a release store of the flag; the reader acquires the flag and reads the
+// payload through L2 (.cg: L1 is not coherent across SMs).
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void wait_flag(const unsigned* p, unsigned v) {
+    while (ld_acquire_gpu(p) != v) __nanosleep(32);
+}
+
+// Launch epoch of the workspace (header word 1): flags written by this launch
+// carry epoch + 1, so stale flags of earlier launches never match.  The last
+// CTA to finish (counter in header word 2) advances the epoch.
+__device__ __forceinline__ unsigned launch_epoch(const unsigned* hdr) {
+    return *reinterpret_cast<const volatile unsigned*>(hdr + 1);
+}
+__device__ __forceinline__ void finish_epoch(unsigned* hdr) {  // call once per CTA, thread 0, at exit
+    __threadfence();
+    const unsigned prev = atomicAdd(hdr + 2, 1u);
+    if (prev == gridDim.x - 1) {
+        *reinterpret_cast<volatile unsigned*>(hdr + 2) = 0u;
+        __threadfence();
+        atomicAdd(hdr + 1, 1u);
+    }
+}
+
 // Programmatic dependent launch (PDL).  Kernels are launched with
 // programmatic stream serialization: everything before pdl_wait() (CTA
 // launch, shared-memory and mbarrier setup) may overlap the tail of the

@@ -50,6 +50,7 @@ int bb_tile_for(int Lmax);
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st);  // a.coords is the input
+int bb_dl_max_tiles(int Lmax);  // per-chain carry slots of the decoupled backbone kernels
 // the paper's own GPU design (paper_baseline.cu), a comparison point
 cudaError_t paper_bb_forward_launch(const BBArgs& a, float* Msave, cudaStream_t st);
 cudaError_t paper_bb_backward_launch(const BBArgs& a, const float* Msave, cudaStream_t st);
