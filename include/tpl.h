@@ -136,6 +136,33 @@ TPL_API tpl_status tpl_backbone_backward_from_coords(const float* coords, const 
                                              int32_t Lmax, const float* grad_coords, float* grad_angles,
                                              void* workspace, size_t ws_bytes, void* stream);
 
+/* one chain split over n_seg ranks (segment s holds residues
+ * [j_s, j_{s+1}) of every chain; lengths[b] = its segment length >= 1), one
+ * exchange per pass.  Forward: each rank computes its segment in
+ * the segment's own frame -- identity at the previous segment's last C, with
+ * omega_prev[b] (= omega_{j_s - 1}, NULL for the first segment) driving the
+ * bond to its first N -- and exports the aggregate transform A_s [B][12]
+ * (row-major 3x4).  The caller all-gathers A into [n_seg][B][12]; _place
+ * maps the local coordinates to the chain frame with A_0 ... A_{s-1} composed
+ * in that order.  Backward (Eq. 2 as e . (T - r x S)): _totals writes
+ * (S = sum g, T = sum (r - c) x g, c = the segment's first atom, 0,0,0) [B][12]
+ * of the placed coordinates; after an all-gather into [n_seg][B][12], _backward
+ * adds the later segments' sums and closes omega of the segment's last residue
+ * with the next segment's first atom.  All arrays are device memory. */
+TPL_API tpl_status tpl_backbone_segment_forward(const float* angles, const int32_t* lengths, int32_t B,
+                                        int32_t Lmax, const float* omega_prev, float* coords, float* aggregate,
+                                        void* workspace, size_t ws_bytes, void* stream);
+TPL_API tpl_status tpl_backbone_segment_place(float* coords, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                      const float* aggregates, int32_t n_seg, int32_t seg, void* workspace,
+                                      size_t ws_bytes, void* stream);
+TPL_API tpl_status tpl_backbone_segment_totals(const float* coords, const int32_t* lengths, int32_t B,
+                                       int32_t Lmax, const float* grad_coords, float* totals, void* workspace,
+                                       size_t ws_bytes, void* stream);
+TPL_API tpl_status tpl_backbone_segment_backward(const float* coords, const int32_t* lengths, int32_t B,
+                                         int32_t Lmax, const float* grad_coords, const float* totals,
+                                         int32_t n_seg, int32_t seg, float* grad_angles, void* workspace,
+                                         size_t ws_bytes, void* stream);
+
 /* the paper's own GPU design, built as a measured comparison
  * point (not the product path).  Forward: one thread per chain saves every
  * cumulative transform M_i = R_0...R_i as a row-major 4x4 fp32

@@ -31,7 +31,8 @@ EXPORTS = [
     "tpl_tables_n_types", "tpl_fullatom_atoms", "tpl_fullatom_forward", "tpl_fullatom_backward",
     "tpl_fullatom_backward_from_coords", "tpl_tables_backward_from_coords_ok",
     "tpl_lrmsd_forward", "tpl_lrmsd_backward",
-    "tpl_paper_backbone_saved_floats", "tpl_paper_backbone_forward", "tpl_paper_backbone_backward",
+    "tpl_backbone_segment_forward", "tpl_backbone_segment_place", "tpl_backbone_segment_totals",
+    "tpl_backbone_segment_backward", "tpl_paper_backbone_saved_floats", "tpl_paper_backbone_forward", "tpl_paper_backbone_backward",
 ]
 
 
@@ -95,6 +96,14 @@ def _load():
     L.tpl_fullatom_backward_from_coords.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]
     L.tpl_tables_backward_from_coords_ok.restype = i32
     L.tpl_tables_backward_from_coords_ok.argtypes = [vp]
+    L.tpl_backbone_segment_forward.restype = ctypes.c_int
+    L.tpl_backbone_segment_forward.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, sz, vp]
+    L.tpl_backbone_segment_place.restype = ctypes.c_int
+    L.tpl_backbone_segment_place.argtypes = [vp, vp, i32, i32, vp, i32, i32, vp, sz, vp]
+    L.tpl_backbone_segment_totals.restype = ctypes.c_int
+    L.tpl_backbone_segment_totals.argtypes = [vp, vp, i32, i32, vp, vp, vp, sz, vp]
+    L.tpl_backbone_segment_backward.restype = ctypes.c_int
+    L.tpl_backbone_segment_backward.argtypes = [vp, vp, i32, i32, vp, vp, i32, i32, vp, vp, sz, vp]
     L.tpl_paper_backbone_saved_floats.restype = i64
     L.tpl_paper_backbone_saved_floats.argtypes = [i32, i32]
     L.tpl_paper_backbone_forward.restype = ctypes.c_int
@@ -248,6 +257,54 @@ def tpl_fullatom_backward_from_coords(handle, coords, restype, lengths, grad_coo
 
 def tpl_tables_backward_from_coords_ok(handle):
     return bool(lib.tpl_tables_backward_from_coords_ok(ctypes.c_void_p(handle)))
+
+
+def tpl_backbone_segment_forward(angles, lengths, omega_prev, coords, aggregate, workspace, stream=None):
+    B, Lmax, three = angles.shape
+    if three != BB_SLOTS or tuple(coords.shape) != (B, 3 * Lmax, 3) or aggregate.numel() != 12 * B:
+        raise ValueError("shapes: angles [B,Lmax,3], coords [B,3*Lmax,3], aggregate [B,12]")
+    om = _dev(omega_prev, torch.float32, "omega_prev") if omega_prev is not None else None
+    _check(lib.tpl_backbone_segment_forward(_dev(angles, torch.float32, "angles"),
+                                            _dev(lengths, torch.int32, "lengths"), B, Lmax, om,
+                                            _dev(coords, torch.float32, "coords"),
+                                            _dev(aggregate, torch.float32, "aggregate"),
+                                            _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                            _stream(stream)))
+
+
+def tpl_backbone_segment_place(coords, lengths, aggregates, seg, workspace, stream=None):
+    B, atoms, _ = coords.shape
+    n_seg = aggregates.numel() // (12 * B)
+    _check(lib.tpl_backbone_segment_place(_dev(coords, torch.float32, "coords"), _dev(lengths, torch.int32, "lengths"),
+                                          B, atoms // 3, _dev(aggregates, torch.float32, "aggregates"), n_seg, seg,
+                                          _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                          _stream(stream)))
+
+
+def tpl_backbone_segment_totals(coords, lengths, grad_coords, totals, workspace, stream=None):
+    B, atoms, _ = coords.shape
+    if tuple(grad_coords.shape) != tuple(coords.shape) or totals.numel() != 12 * B:
+        raise ValueError("shapes: coords/grad_coords [B,3*Lmax,3], totals [B,12]")
+    _check(lib.tpl_backbone_segment_totals(_dev(coords, torch.float32, "coords"),
+                                           _dev(lengths, torch.int32, "lengths"), B, atoms // 3,
+                                           _dev(grad_coords, torch.float32, "grad_coords"),
+                                           _dev(totals, torch.float32, "totals"),
+                                           _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                           _stream(stream)))
+
+
+def tpl_backbone_segment_backward(coords, lengths, grad_coords, totals, seg, grad_angles, workspace, stream=None):
+    B, atoms, _ = coords.shape
+    n_seg = totals.numel() // (12 * B)
+    if tuple(grad_angles.shape) != (B, atoms // 3, 3) or tuple(grad_coords.shape) != tuple(coords.shape):
+        raise ValueError("shapes: coords/grad_coords [B,3*Lmax,3], totals [n_seg,B,12], grad_angles [B,Lmax,3]")
+    _check(lib.tpl_backbone_segment_backward(_dev(coords, torch.float32, "coords"),
+                                             _dev(lengths, torch.int32, "lengths"), B, atoms // 3,
+                                             _dev(grad_coords, torch.float32, "grad_coords"),
+                                             _dev(totals, torch.float32, "totals"), n_seg, seg,
+                                             _dev(grad_angles, torch.float32, "grad_angles"),
+                                             _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                             _stream(stream)))
 
 
 def tpl_paper_backbone_saved_floats(B, Lmax):

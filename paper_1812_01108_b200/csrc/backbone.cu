@@ -56,8 +56,9 @@ __host__ __device__ constexpr int kMinBlocks128Regs(int nt) { return 65536 / (nt
 // redoes the tile with kSlow = true if any |angle| > kSinCosFastMax.
 template <bool kSlow>
 __device__ __forceinline__ void bb_residue_trig(const float* s_ang, int rl, int j, float (&c)[3], float (&s)[3],
-                                                float* maxabs) {
-    const float x[3] = {j > 0 ? s_ang[3 * rl - 1] : 0.f, s_ang[3 * rl + 0], s_ang[3 * rl + 1]};
+                                                float* maxabs, float om0 = 0.f) {
+    // om0: omega_{-1} of a chain segment that continues an earlier one (f4)
+    const float x[3] = {j > 0 ? s_ang[3 * rl - 1] : om0, s_ang[3 * rl + 0], s_ang[3 * rl + 1]};
     if (kSlow) tpl_sincos_n<3>(x, s, c);
     else tpl_sincos_hot<3>(x, s, c, maxabs);
 }
@@ -191,10 +192,16 @@ __device__ __forceinline__ void bb_issue(const It& it, const float* angles, cons
     if (with_g) span_load_bulk(sg, s_g, bar);
 }
 
+// Segment mode (f4, both pointers non-null): chain b continues an earlier
+// segment, so its residue 0 carries the omega bond omega_prev[b] from an
+// identity frame (the previous segment's last C), and the chain's aggregate
+// transform is written to agg_out[b][12] for the exchange between ranks.
 template <int NT, int RPT, int kNS>
 __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(const float* __restrict__ angles,
                                                         const int* __restrict__ lengths, int B, int Lmax,
-                                                        float* __restrict__ coords, unsigned* __restrict__ err) {
+                                                        float* __restrict__ coords, unsigned* __restrict__ err,
+                                                        const float* __restrict__ omega_prev,
+                                                        float* __restrict__ agg_out) {
     constexpr int TILE = NT * RPT;
     constexpr int ANG = round16(16 + 12 * (TILE + 1));
     using S = BBSmem<NT>;
@@ -241,6 +248,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
         __syncthreads();
         TPL_STAMP(3);
         const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 3 * pre;
+        const bool seg0 = omega_prev != nullptr && r0 == 0;  // residue 0 continues a segment
+        const float om0 = seg0 ? __ldg(omega_prev + b) : 0.f;
 
         // ---- pass 1: the thread's chunk composed from the identity; local
         //      atom positions stay in registers (RPT is small and odd, so the
@@ -257,8 +266,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
                 if (q < nq) {
                     const int rl = rl0 + q;
                     float c[3], s[3];
-                    bb_residue_trig<kSlow>(s_ang, rl, r0 + rl, c, s, &maxabs);
-                    if (r0 + rl > 0) aff_bond_bb<0>(M, c[0], s[0]);
+                    bb_residue_trig<kSlow>(s_ang, rl, r0 + rl, c, s, &maxabs, om0);
+                    if (r0 + rl > 0 || seg0) aff_bond_bb<0>(M, c[0], s[0]);
                     px[3 * q] = M.t0; py[3 * q] = M.t1; pz[3 * q] = M.t2;
                     aff_bond_bb<1>(M, c[1], s[1]);
                     px[3 * q + 1] = M.t0; py[3 * q + 1] = M.t1; pz[3 * q + 1] = M.t2;
@@ -274,6 +283,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
         TPL_STAMP(4);
         const Aff P = block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
         carry = load_aff(s_total);
+        if (agg_out != nullptr && r0 + n == L && tid < 12) agg_out[(size_t)b * 12 + tid] = s_total[tid];
         // Let the next kernel launch only now: dependents launched earlier sit on
         // SM resources while waiting and slowed alternating fwd/bwd by ~3 us.
         if (!nx.valid) pdl_trigger();
@@ -698,7 +708,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
                                                              const int* __restrict__ lengths, int B, int Lmax,
                                                              const float* __restrict__ grad_coords,
                                                              float* __restrict__ grad_angles,
-                                                             unsigned* __restrict__ err) {
+                                                             unsigned* __restrict__ err,
+                                                             const float* __restrict__ seg_totals, int n_seg,
+                                                             int seg) {
     constexpr int TILE = NT * RPT;
     constexpr int XB = round16(16 + 36 * TILE + 12);  // tile atoms + the previous atom
     constexpr int GB = round16(16 + 36 * TILE);
@@ -728,6 +740,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
     float carry6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // (S, T) of the later tiles, about c_prev
     float cpx = 0.f, cpy = 0.f, cpz = 0.f;              // reference point of the later tile
     float omega_next = 0.f;
+    bool has_ext = false;                                      // f4: later segments exist
+    float ext[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, cnx = 0.f, cny = 0.f, cnz = 0.f;
     for (int k = 0; it.valid; ++k) {
         const int buf = k & 1;
         const int b = it.b, L = it.L, r0 = it.r0(), n = it.n(), pre = r0 > 0 ? 1 : 0;
@@ -754,6 +768,24 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
 #pragma unroll
             for (int q = 0; q < 6; ++q) carry6[q] = 0.f;
             omega_next = 0.f;
+            // f4 segments: the later segments' totals (fixed order) about the next
+            // segment's first atom N, which also closes omega of the last residue
+            has_ext = seg_totals != nullptr && seg + 1 < n_seg;
+            if (has_ext) {
+                const float* nt0 = seg_totals + ((size_t)(seg + 1) * B + b) * 12;
+                cnx = __ldg(nt0 + 6); cny = __ldg(nt0 + 7); cnz = __ldg(nt0 + 8);
+#pragma unroll
+                for (int q = 0; q < 6; ++q) ext[q] = 0.f;
+                for (int r = n_seg - 1; r > seg; --r) {
+                    const float* tr = seg_totals + ((size_t)r * B + b) * 12;
+                    const float S0 = __ldg(tr), S1 = __ldg(tr + 1), S2 = __ldg(tr + 2);
+                    const float dx = __ldg(tr + 6) - cnx, dy = __ldg(tr + 7) - cny, dz = __ldg(tr + 8) - cnz;
+                    ext[0] += S0; ext[1] += S1; ext[2] += S2;
+                    ext[3] += __ldg(tr + 3) + fmaf(dy, S2, -dz * S1);
+                    ext[4] += __ldg(tr + 4) + fmaf(dz, S0, -dx * S2);
+                    ext[5] += __ldg(tr + 5) + fmaf(dx, S1, -dy * S0);
+                }
+            }
         } else {  // move the later tiles' moment to this tile's reference: T_c = T_c' + (c' - c) x S
             const float dx = cpx - cx, dy = cpy - cy, dz = cpz - cz;
             carry6[3] += fmaf(dy, carry6[2], -dz * carry6[1]);
@@ -780,6 +812,13 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
         float su[6], tot6[6];
         block_exclusive_suffix6<NT>(sum6, carry6, s_suf, su, tot6);
         if (!nx.valid) pdl_trigger();
+        if (has_ext) {  // later segments, about this tile's reference: T_c = T_n + (n - c) x S
+            const float dx = cnx - cx, dy = cny - cy, dz = cnz - cz;
+            su[0] += ext[0]; su[1] += ext[1]; su[2] += ext[2];
+            su[3] += ext[3] + fmaf(dy, ext[2], -dz * ext[1]);
+            su[4] += ext[4] + fmaf(dz, ext[0], -dx * ext[2]);
+            su[5] += ext[5] + fmaf(dx, ext[1], -dy * ext[0]);
+        }
 
         // pass 2: atoms last to first
         const Span so = make_span(grad_angles + ((size_t)b * Lmax + r0) * 3, n * 12);
@@ -821,7 +860,15 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
                 }
             }
         }
-        if (tid == 0) s_go[3 * (n - 1) + 2] = last_tile ? 0.f : omega_next;
+        if (tid == 0) {
+            float w = last_tile ? 0.f : omega_next;
+            if (last_tile && has_ext) {  // omega_{L-1} = e . T_n (the later segments about their N)
+                const float* xc = s_x + 3 * (3 * n - 1);
+                const float ux = cnx - xc[0], uy = cny - xc[1], uz = cnz - xc[2];
+                w = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * fmaf(ux, ext[3], fmaf(uy, ext[4], uz * ext[5]));
+            }
+            s_go[3 * (n - 1) + 2] = w;
+        }
         fence_proxy_async_smem();
         __syncthreads();
         if (tid == 0) {
@@ -1112,7 +1159,8 @@ static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
         grid_cap = persistent_grid(k, NT, sm, 1 << 30);
     }
     const int grid = a.B < grid_cap ? a.B : grid_cap;
-    return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err);
+    return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err,
+                      static_cast<const float*>(a.seg_omega_prev), a.seg_agg_out);
 }
 template <int NT, int RPT, int NS>
 static cudaError_t launch_bwd(const BBArgs& a, cudaStream_t st) {
@@ -1167,7 +1215,7 @@ static cudaError_t launch_bwd_xyz(const BBArgs& a, cudaStream_t st) {
     }
     const int grid = a.B < grid_cap ? a.B : grid_cap;
     return launch_pdl(k, grid, NT, sm, st, static_cast<const float*>(a.coords), a.lengths, a.B, a.Lmax,
-                      a.grad_coords, a.grad_angles, a.err);
+                      a.grad_coords, a.grad_angles, a.err, a.seg_totals, a.n_seg, a.seg);
 }
 
 // Shape of the coordinate backward: TPL_BBX=NTxRPT (tuning) or the default.
@@ -1199,7 +1247,7 @@ template <int NT, int RPT>
 static cudaError_t launch_bwd_xyz_dl(const BBArgs& a, cudaStream_t st);
 
 cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
-    if (dl_enabled(a.B, a.Lmax)) {
+    if (!a.seg_totals && dl_enabled(a.B, a.Lmax)) {
         const BBShape d = bbx_dl_shape(a.B, a.Lmax);
         if (d.nt == 128 && d.rpt == 1) return launch_bwd_xyz_dl<128, 1>(a, st);
         if (d.nt == 128 && d.rpt == 3) return launch_bwd_xyz_dl<128, 3>(a, st);
@@ -1314,7 +1362,8 @@ static cudaError_t dispatch_fwd_dl(const BBArgs& a, cudaStream_t st) {
 }
 
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st) {
-    if (dl_enabled(a.B, a.Lmax)) return a.ns == 0 ? dispatch_fwd_dl<0>(a, st) : dispatch_fwd_dl<1>(a, st);
+    if (!a.seg_agg_out && dl_enabled(a.B, a.Lmax))
+        return a.ns == 0 ? dispatch_fwd_dl<0>(a, st) : dispatch_fwd_dl<1>(a, st);
     return a.ns == 0 ? dispatch<true, 0>(a, st) : dispatch<true, 1>(a, st);
 }
 cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st) {

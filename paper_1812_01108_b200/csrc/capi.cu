@@ -231,6 +231,88 @@ tpl_status tpl_backbone_backward_from_coords(const float* coords, const int32_t*
     return TPL_OK;
 }
 
+// ---------------------------------------------------------------- f4: one chain over several ranks
+static tpl_status seg_args(BBArgs& a, const float* coords_or_angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                           void* workspace, size_t ws_bytes) {
+    tpl_status s = bb_common(coords_or_angles, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    a = BBArgs{};
+    a.lengths = lengths;
+    a.B = B;
+    a.Lmax = Lmax;
+    a.err = static_cast<unsigned*>(workspace);
+    a.ws_prefix = reinterpret_cast<float*>(static_cast<char*>(workspace) + kWsHeader);
+    a.max_tiles = max_tiles_for(TPL_MODEL_BACKBONE, Lmax);
+    a.ns = ns_policy();
+    a.K = backbone_constants();
+    return TPL_OK;
+}
+
+tpl_status tpl_backbone_segment_forward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                        const float* omega_prev, float* coords, float* aggregate, void* workspace,
+                                        size_t ws_bytes, void* stream) {
+    BBArgs a;
+    tpl_status s = seg_args(a, angles, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!coords || !aggregate) return fail(TPL_ERR_NULL, "coords/aggregate is NULL");
+    if (!aligned4(coords) || !aligned4(aggregate) || (omega_prev && !aligned4(omega_prev)))
+        return fail(TPL_ERR_ALIGN, "pointers not 4-byte aligned");
+    a.angles = angles;
+    a.coords = coords;
+    a.seg_omega_prev = omega_prev;
+    a.seg_agg_out = aggregate;
+    cudaError_t e = bb_forward_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "segment forward launch");
+    return TPL_OK;
+}
+
+tpl_status tpl_backbone_segment_place(float* coords, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                      const float* aggregates, int32_t n_seg, int32_t seg, void* workspace,
+                                      size_t ws_bytes, void* stream) {
+    BBArgs a;
+    tpl_status s = seg_args(a, coords, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!aggregates) return fail(TPL_ERR_NULL, "aggregates is NULL");
+    if (n_seg < 1 || seg < 0 || seg >= n_seg) return fail(TPL_ERR_SHAPE, "seg=%d n_seg=%d", seg, n_seg);
+    a.coords = coords;
+    cudaError_t e = segment_place_launch(a, aggregates, seg, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "segment place launch");
+    return TPL_OK;
+}
+
+tpl_status tpl_backbone_segment_totals(const float* coords, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                       const float* grad_coords, float* totals, void* workspace, size_t ws_bytes,
+                                       void* stream) {
+    BBArgs a;
+    tpl_status s = seg_args(a, coords, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!grad_coords || !totals) return fail(TPL_ERR_NULL, "grad_coords/totals is NULL");
+    a.coords = const_cast<float*>(coords);
+    a.grad_coords = grad_coords;
+    cudaError_t e = segment_totals_launch(a, totals, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "segment totals launch");
+    return TPL_OK;
+}
+
+tpl_status tpl_backbone_segment_backward(const float* coords, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                         const float* grad_coords, const float* totals, int32_t n_seg, int32_t seg,
+                                         float* grad_angles, void* workspace, size_t ws_bytes, void* stream) {
+    BBArgs a;
+    tpl_status s = seg_args(a, coords, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!grad_coords || !totals || !grad_angles) return fail(TPL_ERR_NULL, "grad_coords/totals/grad_angles is NULL");
+    if (n_seg < 1 || seg < 0 || seg >= n_seg) return fail(TPL_ERR_SHAPE, "seg=%d n_seg=%d", seg, n_seg);
+    a.coords = const_cast<float*>(coords);
+    a.grad_coords = grad_coords;
+    a.grad_angles = grad_angles;
+    a.seg_totals = totals;
+    a.n_seg = n_seg;
+    a.seg = seg;
+    cudaError_t e = bb_backward_xyz_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "segment backward launch");
+    return TPL_OK;
+}
+
 // ---------------------------------------------------------------- f3: the paper's GPU design
 int64_t tpl_paper_backbone_saved_floats(int32_t B, int32_t Lmax) {
     return (B < 1 || Lmax < 1) ? 0 : static_cast<int64_t>(B) * 3 * Lmax * 16;

@@ -41,6 +41,11 @@ struct BBArgs {
     int max_tiles;
     int ns;  // Newton-Schulz policy: 0 none, 1 prefix/total, 2 every combine
     BBConst K;
+    // f4 chain segments (nullptr otherwise): see tpl_backbone_segment_*
+    const float* seg_omega_prev;  // [B] omega of the residue before the segment
+    float* seg_agg_out;           // [B][12] the segment's aggregate transform
+    const float* seg_totals;      // [n_seg][B][12] (S, T about c, c, pad) of every segment
+    int n_seg, seg;
 };
 
 bool pdl_enabled();  // capi.cu: programmatic dependent launch on (TPL_PDL != 0)
@@ -50,7 +55,10 @@ int bb_tile_for(int Lmax);
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st);  // a.coords is the input
-int bb_dl_max_tiles(int Lmax);  // per-chain carry slots of the decoupled backbone kernels
+int bb_dl_max_tiles(int Lmax);
+// f4 across ranks (segment.cu)
+cudaError_t segment_totals_launch(const BBArgs& a, float* totals, cudaStream_t st);
+cudaError_t segment_place_launch(const BBArgs& a, const float* aggs, int seg, cudaStream_t st);  // per-chain carry slots of the decoupled backbone kernels
 // the paper's own GPU design (paper_baseline.cu), a comparison point
 cudaError_t paper_bb_forward_launch(const BBArgs& a, float* Msave, cudaStream_t st);
 cudaError_t paper_bb_backward_launch(const BBArgs& a, const float* Msave, cudaStream_t st);

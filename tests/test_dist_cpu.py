@@ -55,7 +55,10 @@ def _worker(rank, world, port, q):
     # every rank sees the same global plan: gather the chain ids and check coverage
     ids = [None] * world
     dist.all_gather_object(ids, mine)
-    q.put((rank, tot, mx, sorted(i for s in ids for i in s), sum(lengths)))
+    # f4 exchange step: rank r's record lands at index r of the stacked result
+    stacked = tdist.gather_stack(torch.full((3, 12), float(rank)), None)
+    order_ok = all(bool((stacked[r] == r).all()) for r in range(world))
+    q.put((rank, tot, mx, sorted(i for s in ids for i in s), sum(lengths), order_ok))
     dist.destroy_process_group()
 
 
@@ -71,7 +74,19 @@ def test_gloo_world2_reductions_and_coverage():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, tot, mx, ids, total in res:
+    for rank, tot, mx, ids, total, order_ok in res:
+        assert order_ok
         assert tot == total
         assert mx == 3.0
         assert ids == list(range(64))
+
+
+def test_segment_bounds():
+    for L, w in ((700, 2), (700, 8), (8, 8), (20001, 3)):
+        b = tdist.segment_bounds(L, w)
+        assert b[0][0] == 0 and b[-1][1] == L
+        assert all(hi > lo for lo, hi in b) and all(b[i][1] == b[i + 1][0] for i in range(w - 1))
+        sizes = [hi - lo for lo, hi in b]
+        assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        tdist.segment_bounds(3, 4)

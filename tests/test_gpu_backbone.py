@@ -256,3 +256,43 @@ def test_regular_structures_report(tpl, oracle_lib):
         err = np.abs(coords - X).max()
         print(f"{kind}: max coord err {err:.3e} A at L=700")
         assert err < 0.1
+
+
+@pytest.mark.parametrize("n_seg", [2, 3])
+def test_segments_across_ranks_match_oracle(tpl, oracle_lib, n_seg):
+    """SURVEY f4 across GPUs, by construction on one device: the per-rank segment
+    kernels with the exchange done in-process (stacked in rank order, as the
+    all-gather does) reproduce the whole chain's coordinates and gradients."""
+    from paper_1812_01108_b200 import _abi
+    from paper_1812_01108_b200 import dist as tdist
+
+    B, L = 3, 1500
+    ang = synth.angles_uniform(B, L, 3, 9101 + n_seg)
+    grad = synth.grad_normal((B, 3 * L, 3), 9102 + n_seg)
+    bounds = tdist.segment_bounds(L, n_seg)
+    parts = []
+    for (j0, j1) in bounds:
+        n = j1 - j0
+        a = ang[:, j0:j1].contiguous().cuda()
+        ln = torch.full((B,), n, dtype=torch.int32, device="cuda")
+        om = ang[:, j0 - 1, 2].contiguous().cuda() if j0 > 0 else None
+        ws = torch.zeros(_abi.tpl_workspace_bytes(0, B, n), dtype=torch.uint8, device="cuda")
+        c = torch.empty(B, 3 * n, 3, device="cuda")
+        agg = torch.empty(B, 12, device="cuda")
+        _abi.tpl_backbone_segment_forward(a, ln, om, c, agg, ws)
+        parts.append(dict(a=a, ln=ln, ws=ws, c=c, agg=agg, g=grad[:, 3 * j0:3 * j1].contiguous().cuda()))
+    aggs = torch.stack([p["agg"] for p in parts])  # the forward exchange
+    for s, p in enumerate(parts):
+        _abi.tpl_backbone_segment_place(p["c"], p["ln"], aggs, s, p["ws"])
+        p["tot"] = torch.empty(B, 12, device="cuda")
+        _abi.tpl_backbone_segment_totals(p["c"], p["ln"], p["g"], p["tot"], p["ws"])
+    tots = torch.stack([p["tot"] for p in parts])  # the backward exchange
+    for s, p in enumerate(parts):
+        p["ga"] = torch.zeros(B, p["c"].shape[1] // 3, 3, device="cuda")
+        _abi.tpl_backbone_segment_backward(p["c"], p["ln"], p["g"], tots, s, p["ga"], p["ws"])
+        _abi.tpl_sync_status(p["ws"])
+    coords = torch.cat([p["c"] for p in parts], 1).cpu().numpy()
+    gang = torch.cat([p["ga"] for p in parts], 1).cpu().numpy()
+    lengths = torch.full((B,), L, dtype=torch.int32)
+    c, g = _check(oracle_lib, ang, lengths, grad, coords, gang, coord_tol=2e-3)
+    print(f"{n_seg} segments, L={L}: max coord err {c:.3e} A, grad rel err {g:.3e}")
