@@ -942,7 +942,7 @@ static cudaError_t fa_fwd_v(const FAArgs& a, cudaStream_t st) {
 struct FAFShape {
     int nt, ts, minb;
 };
-static FAFShape faf_shape(int B) {
+static FAFShape faf_shape(int B, int Lmax) {
     static FAFShape env{-1, 0, 0};
     if (env.nt < 0) {
         env = {0, 0, 0};
@@ -954,14 +954,17 @@ static FAFShape faf_shape(int B) {
     if (env.nt) return env;
     // measured (tools/gpu_faf.sh): few chains -> 256 threads, table in shared
     // memory; many chains -> 128 threads, table through L1, 6 CTAs/SM
+    // at most one chain per SM and chains longer than 256 residues: one 512-thread
+    // tile per chain instead of two serial 256-residue tiles (config 3: 13.7 -> 10.6 us)
+    if (B <= 148 && Lmax > 256) return FAFShape{512, 1, 1};
     return B <= 2 * 148 ? FAFShape{256, 1, 2} : FAFShape{128, 0, 6};
 }
 template <int NS>
 static cudaError_t fa_fwd(const FAArgs& a, cudaStream_t st) {
-    const FAFShape s = faf_shape(a.B);
+    const FAFShape s = faf_shape(a.B, a.Lmax);
 #define TPL_FAF(NT_, TS_, MB_) \
     if (s.nt == NT_ && s.ts == TS_ && s.minb == MB_) return fa_fwd_v<NT_, NS, TS_, MB_>(a, st);
-    TPL_FAF(256, 1, 2) TPL_FAF(256, 0, 2) TPL_FAF(256, 0, 3) TPL_FAF(256, 1, 3)
+    TPL_FAF(256, 1, 2) TPL_FAF(256, 0, 2) TPL_FAF(256, 0, 3) TPL_FAF(256, 1, 3) TPL_FAF(512, 1, 1)
     TPL_FAF(128, 1, 4) TPL_FAF(128, 0, 4) TPL_FAF(128, 0, 6) TPL_FAF(128, 1, 6)
 #undef TPL_FAF
     return cudaErrorInvalidConfiguration;
@@ -983,7 +986,7 @@ static cudaError_t fa_bwd(const FAArgs& a, cudaStream_t st) {
 struct FAXShape {
     int nt, rpt, db, ts;
 };
-static FAXShape fax_shape(int B) {
+static FAXShape fax_shape(int B, int Lmax) {
     static FAXShape env{-1, 0, 0, 0};
     if (env.nt < 0) {
         env = {0, 0, 0, 0};
@@ -995,6 +998,7 @@ static FAXShape fax_shape(int B) {
     if (env.nt) return env;
     // measured (tools/gpu_fax.sh): single buffer + table through L1 (more resident
     // CTAs) wins; few chains -> long tiles (latency), many chains -> 64 threads
+    if (B <= 148 && Lmax > 256) return FAXShape{512, 1, 0, 0};  // config 3: 15.3 -> 11.2 us
     return B <= 2 * 148 ? FAXShape{256, 1, 0, 0} : FAXShape{64, 1, 0, 0};
 }
 
@@ -1015,10 +1019,10 @@ static cudaError_t fa_bwd_xyz(const FAArgs& a, cudaStream_t st) {
 }
 
 cudaError_t fa_backward_xyz_launch(const FAArgs& a, cudaStream_t st) {
-    const FAXShape s = fax_shape(a.B);
+    const FAXShape s = fax_shape(a.B, a.Lmax);
 #define TPL_FAX(NT_, R_, DB_, TS_) \
     if (s.nt == NT_ && s.rpt == R_ && s.db == DB_ && s.ts == TS_) return fa_bwd_xyz<NT_, R_, DB_, TS_>(a, st);
-    TPL_FAX(64, 1, 0, 0) TPL_FAX(128, 1, 0, 0) TPL_FAX(256, 1, 0, 0)
+    TPL_FAX(64, 1, 0, 0) TPL_FAX(128, 1, 0, 0) TPL_FAX(256, 1, 0, 0) TPL_FAX(512, 1, 0, 0)
     TPL_FAX(64, 1, 1, 1) TPL_FAX(128, 1, 1, 1) TPL_FAX(256, 1, 1, 1)
 #undef TPL_FAX
     return cudaErrorInvalidConfiguration;
