@@ -81,4 +81,4 @@ def test_pipeline_angles_to_lrmsd_gradient(tpl, oracle_lib):
     g = a.grad.cpu().numpy()
     for b in range(B):
         assert np.abs(g[b] - G[b]).max() / np.abs(G[b]).max() <= 2e-3
-    assert abs(float(loss) - vals.sum()) <= 1e-3 * vals.sum()
+    assert abs(float(loss.detach()) - vals.sum()) <= 1e-3 * vals.sum()
