@@ -62,7 +62,7 @@ def parse():
 
 
 def cfg_key(c):
-    return c if c == "metric" else int(c)
+    return c if c in synth.CONFIGS else int(c)
 
 
 def load_peaks():
@@ -168,6 +168,7 @@ def sum_over_ranks(x, dist):
 # --------------------------------------------------------------- workloads
 class BackboneWork:
     model = "backbone"
+    launches_per_step = 2
 
     def __init__(self, c, rank, world=1, strong=False):
         cfg = synth.CONFIGS[c]
@@ -223,6 +224,54 @@ class BackboneWork:
                 "L": self.Lmax, "batch_per_gpu": self.B}
 
 
+class LossBackboneWork(BackboneWork):
+    """f1: the step a structure-prediction model takes -- forward, LRMSD against a
+    target (PAPER 4), its gradient, backward (from the coordinates)."""
+    launches_per_step = 4
+
+    def __init__(self, c, rank, world=1, strong=False):
+        super().__init__(c, rank, world, strong)
+        self.host["target"] = synth.grad_normal((self.B, 3 * self.Lmax, 3), 5000 + synth.config_id(c) + 7919 * rank)
+
+    def alloc_set(self, ws_bytes):
+        s = super().alloc_set(ws_bytes)
+        s["target"] = self.host["target"].cuda()
+        s["n_atoms"] = 3 * s["lengths"]
+        s["loss"] = torch.empty(self.B, device="cuda")
+        s["state"] = torch.empty(self.B, 16, device="cuda")
+        s["gl"] = torch.ones(self.B, device="cuda")
+        return s
+
+    def footprint(self):
+        return super().footprint() + self.B * self.Lmax * 36
+
+    def fwd(self, s, stream=None):
+        from paper_1812_01108_b200 import _abi
+
+        super().fwd(s, stream)
+        _abi.tpl_lrmsd_forward(s["coords"], s["target"], s["n_atoms"], s["loss"], s["state"], s["ws"], stream)
+
+    def bwd(self, s, stream=None):
+        from paper_1812_01108_b200 import _abi
+
+        _abi.tpl_lrmsd_backward(s["coords"], s["target"], s["n_atoms"], s["state"], s["gl"], s["grad"], s["ws"],
+                                stream)
+        super().bwd(s, stream)
+
+    def algo_bytes(self):
+        r = self.residues
+        return {"fwd": r * (48 + 72), "bwd": r * (108 + 60)}
+
+    def e2e_io(self):
+        h = self.host
+        return ([("angles", h["angles"]), ("target", h["target"])], [("loss", (self.B,)), ("gang", (self.B, self.Lmax, 3))])
+
+    def config(self):
+        d = super().config()
+        d["workload"] += "; LRMSD loss vs a synthetic target between forward and backward"
+        return d
+
+
 class PaperBackboneWork(BackboneWork):
     """the paper's GPU design on the same workload -- forward saves M_i
     (64 B/atom), backward sums Eq. 2 per angle without a reduction."""
@@ -250,6 +299,7 @@ class PaperBackboneWork(BackboneWork):
 
 class FullAtomWork:
     model = "fullatom"
+    launches_per_step = 2
 
     def __init__(self, c, rank, world=1, strong=False):
         import paper_1812_01108_b200 as tpl
@@ -324,6 +374,8 @@ def make_work(c, rank, world=1, strong=False, paper=False):
         if synth.CONFIGS[c]["model"] != "backbone":
             raise SystemExit("--impl paper: the paper's GPU design is the backbone model (its full atom ran on CPU)")
         return PaperBackboneWork(c, rank, world, strong)
+    if synth.CONFIGS[c].get("loss") == "lrmsd":
+        return LossBackboneWork(c, rank, world, strong)
     cls = BackboneWork if synth.CONFIGS[c]["model"] == "backbone" else FullAtomWork
     return cls(c, rank, world, strong)
 
@@ -505,7 +557,10 @@ def run_ours(args):
             "step_frac": (ab["fwd"] + ab["bwd"]) / (ms_step * 1e-3) / 1e9 / peak}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.impl != "paper":
+    # the oracle's O(L^2) backward makes a 20000-residue chain a minute of CPU: no sample for "long";
+    # the loss config's oracle would time the same backbone work as the metric config
+    skip_cpu = args.impl == "paper" or work.Lmax > 5000 or isinstance(work, LossBackboneWork)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not skip_cpu:
         cpu = cpu_baseline(work, args.cpu_seconds)
 
     if rank == 0:
@@ -518,7 +573,7 @@ def run_ours(args):
                "value": value, "unit": "residues/s", "n_gpus": world, "steps": K, "warmup": W,
                "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
                "dtype": "f32", "data": "synthetic (seeded uniform angles, N(0,1) dL/dr)", "config": cfgd,
-               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": 2 * K,
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": work.launches_per_step * K,
                "impl": "paper_gpu_design" if args.impl == "paper" else "ours"}
         print(json.dumps(out))
     if dist is not None:

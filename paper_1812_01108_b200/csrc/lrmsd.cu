@@ -25,8 +25,10 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Largest eigenpair of a symmetric 4x4 (fp64, cyclic Jacobi).
-__device__ void sym4_max_eigen(double A[4][4], double* lam, double q[4]) {
+// Largest eigenpair of a symmetric 4x4 (fp64, cyclic Jacobi).  Out of line: it is
+// only the fallback for a degenerate pair, and its dynamically indexed arrays
+// must not put the fast path on the stack.
+__device__ __noinline__ void sym4_max_eigen(double A[4][4], double* lam, double q[4]) {
     double V[4][4];
     for (int i = 0; i < 4; ++i)
         for (int j = 0; j < 4; ++j) V[i][j] = i == j ? 1.0 : 0.0;
@@ -76,6 +78,96 @@ __device__ void sym4_max_eigen(double A[4][4], double* lam, double q[4]) {
     for (int i = 0; i < 4; ++i) q[i] = V[i][m] * sg;
 }
 
+__device__ __forceinline__ double det3(double a, double b, double c, double d, double e, double f, double g,
+                                       double h, double i) {
+    return a * (e * i - f * h) - b * (d * i - f * g) + c * (d * h - e * g);
+}
+
+// Largest eigenpair of the traceless symmetric 4x4 T of P:220-227, the fast way:
+// Newton on its characteristic polynomial lambda^4 + c2 lambda^2 + c1 lambda + c0
+// (c2 = -2 |R|_F^2, c1 = -8 det R, c0 = det T) from the upper bound e0 =
+// (|x~|^2 + |y~|^2) / 2, which converges monotonically to the largest root; the
+// eigenvector is the largest column of adj(T - lambda I).  A degenerate pair
+// (adjugate ~ 0) falls back to Jacobi.  Returns false on fallback needed.
+__device__ bool sym4_max_eigen_newton(const double T[4][4], const double R[3][3], double e0, double* lam,
+                                      double q[4]) {
+    double c2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) c2 += R[a][c] * R[a][c];
+    c2 *= -2.0;
+    const double c1 = -8.0 * det3(R[0][0], R[0][1], R[0][2], R[1][0], R[1][1], R[1][2], R[2][0], R[2][1], R[2][2]);
+    // det T by cofactors along row 0
+    double c0 = 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        double m[9];
+        int k = 0;
+#pragma unroll
+        for (int r = 1; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (c != j) m[k++] = T[r][c];
+        const double mn = det3(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], m[8]);
+        c0 += ((j & 1) ? -1.0 : 1.0) * T[0][j] * mn;
+    }
+    double l = e0;
+    for (int it = 0; it < 60; ++it) {
+        const double l2 = l * l;
+        const double p = (l2 + c2) * l2 + c1 * l + c0;
+        const double dp = 4.0 * l2 * l + 2.0 * c2 * l + c1;
+        if (dp == 0.0) break;
+        const double nl = l - p / dp;
+        if (fabs(nl - l) <= 1e-13 * fabs(nl)) {
+            l = nl;
+            break;
+        }
+        l = nl;
+    }
+    *lam = l;
+    double M[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) M[i][j] = T[i][j] - (i == j ? l : 0.0);
+    // adj(M)[i][j] = (-1)^(i+j) det(M without row j, column i); keep the largest column
+    double best[4] = {0, 0, 0, 0}, bn = -1.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        double col[4], n2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            double m[9];
+            int k = 0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                if (r == j) continue;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (c != i) m[k++] = M[r][c];
+            }
+            col[i] = (((i + j) & 1) ? -1.0 : 1.0) * det3(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], m[8]);
+            n2 += col[i] * col[i];
+        }
+        const bool better = n2 > bn;
+        bn = better ? n2 : bn;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) best[i] = better ? col[i] : best[i];
+    }
+    const double scale = fmax(fabs(l), 1e-300);
+    if (!(bn > 1e-24 * scale * scale * scale * scale * scale * scale)) return false;  // degenerate: Jacobi
+    const double inv = 1.0 / sqrt(bn);
+    // first nonzero component > 0 (as the oracle)
+    const double lead = fabs(best[0]) * inv >= 1e-12 ? best[0]
+                      : fabs(best[1]) * inv >= 1e-12 ? best[1]
+                      : fabs(best[2]) * inv >= 1e-12 ? best[2] : best[3];
+    const double sg = lead < 0.0 ? -inv : inv;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[i] = best[i] * sg;
+    return true;
+}
+
 __global__ void __launch_bounds__(kLRThreads) lrmsd_forward_kernel(const float* __restrict__ x,
                                                                    const float* __restrict__ y,
                                                                    const int* __restrict__ n_atoms, int stride,
@@ -110,12 +202,18 @@ __global__ void __launch_bounds__(kLRThreads) lrmsd_forward_kernel(const float* 
         if (lane == 0) s_red[warp][k] = v;
     }
     __syncthreads();
+    __shared__ double s_tot[17];
+    if (threadIdx.x < 17) {  // the warp partials, one moment per lane (fixed order)
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < kLRThreads / 32; ++w) v += s_red[w][threadIdx.x];
+        s_tot[threadIdx.x] = v;
+    }
+    __syncwarp();
     if (threadIdx.x != 0) return;
     double s[17];
-    for (int k = 0; k < 17; ++k) {
-        s[k] = 0.0;
-        for (int w = 0; w < kLRThreads / 32; ++w) s[k] += s_red[w][k];
-    }
+#pragma unroll
+    for (int k = 0; k < 17; ++k) s[k] = s_tot[k];
     const double n = double(N);
     const double cx[3] = {s[0] / n, s[1] / n, s[2] / n}, cy[3] = {s[3] / n, s[4] / n, s[5] / n};
     double R[3][3];  // R_ac = sum (x_a - cx_a)(y_c - cy_c) = sum x_a y_c - N cx_a cy_c
@@ -131,7 +229,12 @@ __global__ void __launch_bounds__(kLRThreads) lrmsd_forward_kernel(const float* 
         {R[0][1] - R[1][0], R[0][2] + R[2][0], R[1][2] + R[2][1], -R[0][0] - R[1][1] + R[2][2]},
     };
     double lam, q[4];
-    sym4_max_eigen(T, &lam, q);
+    if (!sym4_max_eigen_newton(T, R, 0.5 * (sxx + syy), &lam, q)) {
+        double A[4][4];  // the fallback works on a copy (the fast path keeps T in registers)
+        for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 4; ++j) A[i][j] = T[i][j];
+        sym4_max_eigen(A, &lam, q);
+    }
     const double q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
     const double U[9] = {q0 * q0 + q1 * q1 - q2 * q2 - q3 * q3, 2 * (q1 * q2 - q0 * q3), 2 * (q1 * q3 + q0 * q2),
                          2 * (q1 * q2 + q0 * q3), q0 * q0 - q1 * q1 + q2 * q2 - q3 * q3, 2 * (q2 * q3 - q0 * q1),

@@ -35,11 +35,16 @@ CONFIGS = {
     4: dict(model="backbone", B=4096, L=2000, ragged=(50, 2000), desc="ragged backbone L in [50,2000], batch 4096"),
     5: dict(model="fullatom", B=8192, L=500, desc="full-atom 8192 x L=500 (8-GPU stress)"),
     "metric": dict(model="backbone", B=256, L=700, desc="headline: backbone L=700 batch 256 fwd+bwd"),
+    # NEXT rows, measured beside the BASELINE configs
+    "lrmsd": dict(model="backbone", B=256, L=700, loss="lrmsd",
+                  desc="f1: headline shape with the LRMSD loss (PAPER 4) between forward and backward"),
+    "long": dict(model="backbone", B=1, L=20000, desc="f4: one 20000-residue chain split over CTAs"),
 }
+_IDS = {"metric": 0, "lrmsd": 6, "long": 7}
 
 
 def config_id(c):
-    return 0 if c == "metric" else int(c)
+    return _IDS[c] if c in _IDS else int(c)
 
 
 def _gen(seed):
