@@ -226,8 +226,9 @@ class BackboneWork:
 
 class LossBackboneWork(BackboneWork):
     """f1: the step a structure-prediction model takes -- forward, LRMSD against a
-    target (PAPER 4), its gradient, backward (from the coordinates)."""
-    launches_per_step = 4
+    target (PAPER 4), its gradient, backward -- through the fused pair
+    tpl_backbone_lrmsd_forward / _backward (no dL/dr array)."""
+    launches_per_step = 3  # forward (+ moments), per-chain eigen solve, backward
 
     def __init__(self, c, rank, world=1, strong=False):
         super().__init__(c, rank, world, strong)
@@ -236,7 +237,6 @@ class LossBackboneWork(BackboneWork):
     def alloc_set(self, ws_bytes):
         s = super().alloc_set(ws_bytes)
         s["target"] = self.host["target"].cuda()
-        s["n_atoms"] = 3 * s["lengths"]
         s["loss"] = torch.empty(self.B, device="cuda")
         s["state"] = torch.empty(self.B, 16, device="cuda")
         s["gl"] = torch.ones(self.B, device="cuda")
@@ -248,19 +248,19 @@ class LossBackboneWork(BackboneWork):
     def fwd(self, s, stream=None):
         from paper_1812_01108_b200 import _abi
 
-        super().fwd(s, stream)
-        _abi.tpl_lrmsd_forward(s["coords"], s["target"], s["n_atoms"], s["loss"], s["state"], s["ws"], stream)
+        _abi.tpl_backbone_lrmsd_forward(s["angles"], s["lengths"], s["target"], s["coords"], s["loss"], s["state"],
+                                        s["ws"], stream)
 
     def bwd(self, s, stream=None):
         from paper_1812_01108_b200 import _abi
 
-        _abi.tpl_lrmsd_backward(s["coords"], s["target"], s["n_atoms"], s["state"], s["gl"], s["grad"], s["ws"],
-                                stream)
-        super().bwd(s, stream)
+        _abi.tpl_backbone_lrmsd_backward(s["coords"], s["lengths"], s["target"], s["state"], s["gl"], s["gang"],
+                                         s["ws"], stream)
 
     def algo_bytes(self):
+        # the op's own bytes: fwd angles + target in, coords out; bwd angles + target in, dL/dangles out
         r = self.residues
-        return {"fwd": r * (48 + 72), "bwd": r * (108 + 60)}
+        return {"fwd": r * (12 + 36 + 36), "bwd": r * (12 + 36 + 12)}
 
     def e2e_io(self):
         h = self.host
@@ -268,7 +268,7 @@ class LossBackboneWork(BackboneWork):
 
     def config(self):
         d = super().config()
-        d["workload"] += "; LRMSD loss vs a synthetic target between forward and backward"
+        d["workload"] += "; LRMSD loss vs a synthetic target, fused into the forward and backward kernels"
         return d
 
 

@@ -136,6 +136,21 @@ TPL_API tpl_status tpl_backbone_backward_from_coords(const float* coords, const 
                                              int32_t Lmax, const float* grad_coords, float* grad_angles,
                                              void* workspace, size_t ws_bytes, void* stream);
 
+/* the backbone map and the LRMSD loss (PAPER §4)
+ * fused: the forward also reduces, per chain, the moments of (r, y) over the
+ * chain's 3L atoms against the reference y [B][3*Lmax][3] and returns
+ * lrmsd[B] and state[B][16] (as tpl_lrmsd_forward); the backward forms
+ * dL/dr_i = grad_lrmsd[b] (r~_i - U^T y~_i) / (3L LRMSD) on the fly inside the
+ * coordinate backward (no dL/dr array), giving grad_angles [B][Lmax][3].
+ * coords is the forward's output (kept by the caller for the backward). */
+TPL_API tpl_status tpl_backbone_lrmsd_forward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                      const float* target, float* coords, float* lrmsd, float* state,
+                                      void* workspace, size_t ws_bytes, void* stream);
+TPL_API tpl_status tpl_backbone_lrmsd_backward(const float* coords, const int32_t* lengths, int32_t B,
+                                       int32_t Lmax, const float* target, const float* state,
+                                       const float* grad_lrmsd, float* grad_angles, void* workspace,
+                                       size_t ws_bytes, void* stream);
+
 /* one chain split over n_seg ranks (segment s holds residues
  * [j_s, j_{s+1}) of every chain; lengths[b] = its segment length >= 1), one
  * exchange per pass.  Forward: each rank computes its segment in

@@ -8,8 +8,8 @@ marshalling, autograd glue, batch sharding for multi-GPU runs).
 """
 from . import _abi
 from ._abi import TplError, lib
-from .api import (BackboneFunction, FullAtomFunction, LRMSDFunction, Tables, Workspace, backbone,
-                  default_workspace, fullatom, lrmsd)
+from .api import (BackboneFunction, BackboneLRMSDFunction, FullAtomFunction, LRMSDFunction, Tables, Workspace,
+                  backbone, backbone_lrmsd, default_workspace, fullatom, lrmsd)
 
 __all__ = ["TplError", "lib", "Tables", "Workspace", "backbone", "fullatom", "BackboneFunction",
-           "FullAtomFunction", "LRMSDFunction", "lrmsd", "default_workspace", "_abi"]
+           "FullAtomFunction", "LRMSDFunction", "lrmsd", "backbone_lrmsd", "BackboneLRMSDFunction", "default_workspace", "_abi"]

@@ -31,7 +31,7 @@ EXPORTS = [
     "tpl_tables_n_types", "tpl_fullatom_atoms", "tpl_fullatom_forward", "tpl_fullatom_backward",
     "tpl_fullatom_backward_from_coords", "tpl_tables_backward_from_coords_ok",
     "tpl_lrmsd_forward", "tpl_lrmsd_backward",
-    "tpl_backbone_segment_forward", "tpl_backbone_segment_place", "tpl_backbone_segment_totals",
+    "tpl_backbone_lrmsd_forward", "tpl_backbone_lrmsd_backward", "tpl_backbone_segment_forward", "tpl_backbone_segment_place", "tpl_backbone_segment_totals",
     "tpl_backbone_segment_backward", "tpl_paper_backbone_saved_floats", "tpl_paper_backbone_forward", "tpl_paper_backbone_backward",
 ]
 
@@ -96,6 +96,10 @@ def _load():
     L.tpl_fullatom_backward_from_coords.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]
     L.tpl_tables_backward_from_coords_ok.restype = i32
     L.tpl_tables_backward_from_coords_ok.argtypes = [vp]
+    L.tpl_backbone_lrmsd_forward.restype = ctypes.c_int
+    L.tpl_backbone_lrmsd_forward.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp, sz, vp]
+    L.tpl_backbone_lrmsd_backward.restype = ctypes.c_int
+    L.tpl_backbone_lrmsd_backward.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp, sz, vp]
     L.tpl_backbone_segment_forward.restype = ctypes.c_int
     L.tpl_backbone_segment_forward.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, sz, vp]
     L.tpl_backbone_segment_place.restype = ctypes.c_int
@@ -257,6 +261,34 @@ def tpl_fullatom_backward_from_coords(handle, coords, restype, lengths, grad_coo
 
 def tpl_tables_backward_from_coords_ok(handle):
     return bool(lib.tpl_tables_backward_from_coords_ok(ctypes.c_void_p(handle)))
+
+
+def tpl_backbone_lrmsd_forward(angles, lengths, target, coords, lrmsd, state, workspace, stream=None):
+    """f1: backbone forward + LRMSD against target, fused (per-chain loss over the 3L backbone atoms)."""
+    B, Lmax, three = angles.shape
+    if (three != BB_SLOTS or tuple(coords.shape) != (B, 3 * Lmax, 3) or tuple(target.shape) != (B, 3 * Lmax, 3)
+            or tuple(lrmsd.shape) != (B,) or tuple(state.shape) != (B, 16)):
+        raise ValueError("shapes: angles [B,Lmax,3], target/coords [B,3*Lmax,3], lrmsd [B], state [B,16]")
+    _check(lib.tpl_backbone_lrmsd_forward(_dev(angles, torch.float32, "angles"),
+                                          _dev(lengths, torch.int32, "lengths"), B, Lmax,
+                                          _dev(target, torch.float32, "target"), _dev(coords, torch.float32, "coords"),
+                                          _dev(lrmsd, torch.float32, "lrmsd"), _dev(state, torch.float32, "state"),
+                                          _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                          _stream(stream)))
+
+
+def tpl_backbone_lrmsd_backward(coords, lengths, target, state, grad_lrmsd, grad_angles, workspace, stream=None):
+    B, atoms, _ = coords.shape
+    if (tuple(target.shape) != tuple(coords.shape) or tuple(grad_angles.shape) != (B, atoms // 3, 3)
+            or tuple(grad_lrmsd.shape) != (B,) or tuple(state.shape) != (B, 16)):
+        raise ValueError("shapes: coords/target [B,3*Lmax,3], state [B,16], grad_lrmsd [B], grad_angles [B,Lmax,3]")
+    _check(lib.tpl_backbone_lrmsd_backward(_dev(coords, torch.float32, "coords"),
+                                           _dev(lengths, torch.int32, "lengths"), B, atoms // 3,
+                                           _dev(target, torch.float32, "target"), _dev(state, torch.float32, "state"),
+                                           _dev(grad_lrmsd, torch.float32, "grad_lrmsd"),
+                                           _dev(grad_angles, torch.float32, "grad_angles"),
+                                           _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                           _stream(stream)))
 
 
 def tpl_backbone_segment_forward(angles, lengths, omega_prev, coords, aggregate, workspace, stream=None):

@@ -169,6 +169,39 @@ def fullatom(angles, restype, lengths, tables, atom_stride=None):
     return FullAtomFunction.apply(angles, restype, lengths, tables, int(atom_stride))
 
 
+class BackboneLRMSDFunction(torch.autograd.Function):
+    """f1: angles -> (LRMSD to target [B], coords) in one fused forward; the backward
+    forms dL/dr from the LRMSD state inside the coordinate backward."""
+
+    @staticmethod
+    def forward(ctx, angles, target, lengths):
+        angles, target = angles.contiguous(), target.contiguous()
+        B, Lmax, _ = angles.shape
+        coords = torch.empty((B, 3 * Lmax, 3), dtype=torch.float32, device=angles.device)
+        out = torch.empty(B, dtype=torch.float32, device=angles.device)
+        state = torch.empty((B, 16), dtype=torch.float32, device=angles.device)
+        ws = default_workspace(angles.device).get(MODEL_BACKBONE, B, Lmax)
+        _abi.tpl_backbone_lrmsd_forward(angles, lengths, target, coords, out, state, ws)
+        ctx.save_for_backward(coords, target, lengths, state)
+        ctx.mark_non_differentiable(coords)
+        return out, coords
+
+    @staticmethod
+    def backward(ctx, grad_out, _grad_coords):
+        coords, target, lengths, state = ctx.saved_tensors
+        B, Lmax = coords.shape[0], coords.shape[1] // 3
+        grad_angles = torch.zeros((B, Lmax, 3), dtype=torch.float32, device=coords.device)
+        ws = default_workspace(coords.device).get(MODEL_BACKBONE, B, Lmax)
+        _abi.tpl_backbone_lrmsd_backward(coords, lengths, target, state, grad_out.contiguous(), grad_angles, ws)
+        return grad_angles, None, None
+
+
+def backbone_lrmsd(angles, target, lengths=None):
+    """angles [B, Lmax, 3], target [B, 3*Lmax, 3] -> (LRMSD over each chain's 3L atoms [B],
+    coords [B, 3*Lmax, 3] (not differentiable: the gradient flows through the LRMSD))."""
+    return BackboneLRMSDFunction.apply(angles, target.to(angles.device), _lengths_for(angles, lengths))
+
+
 class LRMSDFunction(torch.autograd.Function):
     """LRMSD (PAPER §4) per chain between x (differentiated) and the reference y."""
 

@@ -30,6 +30,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "lrmsd_math.cuh"
 
 namespace tpl {
 
@@ -196,14 +197,22 @@ __device__ __forceinline__ void bb_issue(const It& it, const float* angles, cons
 // segment, so its residue 0 carries the omega bond omega_prev[b] from an
 // identity frame (the previous segment's last C), and the chain's aggregate
 // transform is written to agg_out[b][12] for the exchange between ranks.
-template <int NT, int RPT, int kNS>
+// kLoss (f1, fused LRMSD): the target tile is bulk-loaded beside the output, the
+// chain's raw fp64 moments (sum x, sum y, sum x y^T, sum |x|^2, sum |y|^2; PAPER
+// §4 step 1) are reduced over its tiles, and at the chain's end thread
+// 0 solves steps 2-3 (lrmsd_math.cuh) into loss_out[b] and loss_state[b][16].
+template <int NT, int RPT, int kNS, bool kLoss = false>
 __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(const float* __restrict__ angles,
                                                         const int* __restrict__ lengths, int B, int Lmax,
                                                         float* __restrict__ coords, unsigned* __restrict__ err,
                                                         const float* __restrict__ omega_prev,
-                                                        float* __restrict__ agg_out) {
+                                                        float* __restrict__ agg_out,
+                                                        const float* __restrict__ target,
+                                                        float* __restrict__ loss_out,
+                                                        float* __restrict__ loss_state) {
     constexpr int TILE = NT * RPT;
     constexpr int ANG = round16(16 + 12 * (TILE + 1));
+    constexpr int OUT = round16(16 + 36 * TILE);
     using S = BBSmem<NT>;
     extern __shared__ __align__(16) char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
@@ -211,14 +220,20 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
     float* s_total = reinterpret_cast<float*>(smem + S::kTotal);
     char* s_ang_buf = smem + S::kData;  // 2 x ANG
     char* s_out_base = s_ang_buf + 2 * ANG;
+    char* s_tgt_base = s_out_base + OUT;                                            // kLoss: target tile
+    double* s_mred = reinterpret_cast<double*>(s_tgt_base + OUT);                   // kLoss: 17 x NT partials
+    double* s_macc = s_mred + 17 * NT;                                              // kLoss: the chain's moments
+    uint64_t* bar_t = reinterpret_cast<uint64_t*>(s_macc + 18);                     // kLoss
 
     const int tid = threadIdx.x;
     TPL_STAMP(0);
     if (tid == 0) {
         mbar_init(bar, 1);
         mbar_init(bar + 1, 1);
+        if (kLoss) mbar_init(bar_t, 1);
         fence_barrier_init();
     }
+    unsigned tphase = 0;
     pdl_wait();
     BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), true, err, false};
     it.init();
@@ -242,6 +257,16 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
         span_load_edges_f32(sa, s_ang_base);
         const Span so = make_span(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3, n * 36);
         float* s_out = reinterpret_cast<float*>(s_out_base + so.mis());
+        Span stg{};
+        if (kLoss) {  // the target tile (single buffer: the previous item's moments pass is done)
+            stg = make_span(target + ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3, n * 36);
+            if (tid == 0) {
+                mbar_arrive_expect_tx(bar_t, unsigned(stg.mid));
+                span_load_bulk(stg, s_tgt_base, bar_t);
+            }
+            span_load_edges_f32(stg, s_tgt_base);
+            if (r0 == 0 && tid < 17) s_macc[tid] = 0.0;  // read after the moments pass's barrier
+        }
         TPL_STAMP(2);
         mbar_wait(bar + buf, (phases >> buf) & 1u);
         phases ^= 1u << buf;
@@ -310,6 +335,43 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
             bulk_commit();
         }
         span_store_edges_f32(so, s_out_base);
+        if (kLoss) {  // moments of (x, y) over the tile's atoms, fp64
+            mbar_wait(bar_t, tphase);
+            tphase ^= 1u;
+            __syncthreads();  // the target edges are in place
+            const float* xo = s_out;
+            const float* yo = reinterpret_cast<const float*>(s_tgt_base + stg.mis());
+            double m[17];
+#pragma unroll
+            for (int q = 0; q < 17; ++q) m[q] = 0.0;
+            for (int a = tid; a < 3 * n; a += NT) {
+                const double x0 = xo[3 * a], x1 = xo[3 * a + 1], x2 = xo[3 * a + 2];
+                const double y0 = yo[3 * a], y1 = yo[3 * a + 1], y2 = yo[3 * a + 2];
+                m[0] += x0; m[1] += x1; m[2] += x2;
+                m[3] += y0; m[4] += y1; m[5] += y2;
+                m[6] += x0 * y0; m[7] += x0 * y1; m[8] += x0 * y2;
+                m[9] += x1 * y0; m[10] += x1 * y1; m[11] += x1 * y2;
+                m[12] += x2 * y0; m[13] += x2 * y1; m[14] += x2 * y2;
+                m[15] += x0 * x0 + x1 * x1 + x2 * x2;
+                m[16] += y0 * y0 + y1 * y1 + y2 * y2;
+            }
+            // transposed reduction (fixed order): every thread parks its 17 partials, then
+            // warp w folds moments w, w + NW, ... (NT/32 values per lane, then a shuffle tree)
+            const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+            for (int q = 0; q < 17; ++q) s_mred[q * NT + tid] = m[q];
+            __syncthreads();
+            for (int q = warp; q < 17; q += NT / 32) {
+                double v = 0.0;
+#pragma unroll
+                for (int k = 0; k < NT / 32; ++k) v += s_mred[q * NT + lane + 32 * k];
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+                if (lane == 0) s_macc[q] += v;
+            }
+            __syncthreads();
+            if (tid == 0 && r0 + n == L) lrmsd_solve(s_macc, 3.0 * L, loss_out + b, loss_state + (size_t)b * 16);
+        }
         (void)L;
         it = nx;
     }
@@ -703,14 +765,18 @@ __device__ __forceinline__ void bbx_issue(const BBIter& it, const float* coords,
     span_load_bulk(sg, s_g, bar);
 }
 
-template <int NT, int RPT>
+// kLoss (f1, fused LRMSD): grad_coords is the LRMSD target y, and dL/dr_i =
+// dL/dLRMSD (x~_i - U^T y~_i) / (N LRMSD) (reading Q19) is formed
+// on the fly from the forward's state -- no dL/dr array is written or read.
+template <int NT, int RPT, bool kLoss = false>
 __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_kernel(const float* __restrict__ coords,
                                                              const int* __restrict__ lengths, int B, int Lmax,
                                                              const float* __restrict__ grad_coords,
                                                              float* __restrict__ grad_angles,
                                                              unsigned* __restrict__ err,
                                                              const float* __restrict__ seg_totals, int n_seg,
-                                                             int seg) {
+                                                             int seg, const float* __restrict__ loss_state,
+                                                             const float* __restrict__ loss_grad) {
     constexpr int TILE = NT * RPT;
     constexpr int XB = round16(16 + 36 * TILE + 12);  // tile atoms + the previous atom
     constexpr int GB = round16(16 + 36 * TILE);
@@ -740,6 +806,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
     float carry6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // (S, T) of the later tiles, about c_prev
     float cpx = 0.f, cpy = 0.f, cpz = 0.f;              // reference point of the later tile
     float omega_next = 0.f;
+    float lU[9], lcx[3], lcy[3], lsc = 0.f;                     // kLoss: the chain's LRMSD state
     bool has_ext = false;                                      // f4: later segments exist
     float ext[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, cnx = 0.f, cny = 0.f, cnz = 0.f;
     for (int k = 0; it.valid; ++k) {
@@ -762,12 +829,34 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
         __syncthreads();
         const float* s_x = reinterpret_cast<const float*>(s_x_base + sx.mis()) + 3 * pre;  // atom 0 of the tile
         const float* s_g = reinterpret_cast<const float*>(s_g_base + sg.mis());
+        // dL/dr of one atom: the staged array, or (kLoss) the LRMSD gradient from x and y
+        auto grad_of = [&](const float* xa, const float* ga, float& gx, float& gy, float& gz) {
+            if (kLoss) {
+                const float yx = ga[0] - lcy[0], yy = ga[1] - lcy[1], yz = ga[2] - lcy[2];
+                gx = lsc * (xa[0] - lcx[0] - fmaf(lU[0], yx, fmaf(lU[3], yy, lU[6] * yz)));
+                gy = lsc * (xa[1] - lcx[1] - fmaf(lU[1], yx, fmaf(lU[4], yy, lU[7] * yz)));
+                gz = lsc * (xa[2] - lcx[2] - fmaf(lU[2], yx, fmaf(lU[5], yy, lU[8] * yz)));
+            } else {
+                gx = ga[0]; gy = ga[1]; gz = ga[2];
+            }
+        };
         const int nq = max(0, min(RPT, n - rl0));
         const float cx = s_x[0], cy = s_x[1], cz = s_x[2];
         if (last_tile) {
 #pragma unroll
             for (int q = 0; q < 6; ++q) carry6[q] = 0.f;
             omega_next = 0.f;
+            if (kLoss) {
+                const float* st = loss_state + (size_t)b * 16;
+#pragma unroll
+                for (int q = 0; q < 9; ++q) lU[q] = __ldg(st + q);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    lcx[q] = __ldg(st + 9 + q);
+                    lcy[q] = __ldg(st + 12 + q);
+                }
+                lsc = __ldg(st + 15) * __ldg(loss_grad + b);
+            }
             // f4 segments: the later segments' totals (fixed order) about the next
             // segment's first atom N, which also closes omega of the last residue
             has_ext = seg_totals != nullptr && seg + 1 < n_seg;
@@ -801,7 +890,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
             if (a / 3 < nq) {
                 const float* x = s_x + 9 * rl0 + 3 * a;
                 const float* g = s_g + 9 * rl0 + 3 * a;
-                const float px = x[0] - cx, py = x[1] - cy, pz = x[2] - cz, gx = g[0], gy = g[1], gz = g[2];
+                const float px = x[0] - cx, py = x[1] - cy, pz = x[2] - cz;
+                float gx, gy, gz;
+                grad_of(x, g, gx, gy, gz);
                 sum6[0] += gx; sum6[1] += gy; sum6[2] += gz;
                 sum6[3] += fmaf(py, gz, -pz * gy);
                 sum6[4] += fmaf(pz, gx, -px * gz);
@@ -836,7 +927,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
                     const float* g = s_g + 3 * a;
                     const float x0 = x[0], x1 = x[1], x2 = x[2];
                     const float px = x0 - cx, py = x1 - cy, pz = x2 - cz;
-                    const float gx = g[0], gy = g[1], gz = g[2];
+                    float gx, gy, gz;
+                    grad_of(x, g, gx, gy, gz);
                     if (j > 0 || kk > 0) {  // atom 0 of the chain carries no angle
                         const float ux = x0 - x[-3], uy = x1 - x[-2], uz = x2 - x[-1];
                         const float inv = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
@@ -1113,9 +1205,11 @@ int bb_tile_for(int Lmax) {  // backward tile: sizes the workspace's per-tile pr
 }
 
 template <int NT>
-static size_t fwd_smem(int rpt) {
+static size_t fwd_smem(int rpt, bool loss = false) {
     const int tile = NT * rpt;
-    return BBSmem<NT>::kData + 2 * round16(16 + 12 * (tile + 1)) + round16(16 + 36 * tile);
+    const size_t out = round16(16 + 36 * tile);
+    return BBSmem<NT>::kData + 2 * round16(16 + 12 * (tile + 1)) + out +
+           (loss ? out + 17 * NT * 8 + 18 * 8 + 16 : 0);
 }
 template <int NT>
 static size_t bwd_smem(int rpt) {
@@ -1146,10 +1240,10 @@ static int persistent_grid(K kernel, int nt, size_t smem, int B) {
     return int(B < cap ? B : cap);
 }
 
-template <int NT, int RPT, int NS>
+template <int NT, int RPT, int NS, bool LOSS = false>
 static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
-    auto k = bb_forward_kernel<NT, RPT, NS>;
-    const size_t sm = fwd_smem<NT>(RPT);
+    auto k = bb_forward_kernel<NT, RPT, NS, LOSS>;
+    const size_t sm = fwd_smem<NT>(RPT, LOSS);
     static size_t configured = 0;  // set the smem opt-in once per instance (not inside graph capture)
     static int grid_cap = 0;
     if (configured < sm) {
@@ -1160,7 +1254,8 @@ static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
     }
     const int grid = a.B < grid_cap ? a.B : grid_cap;
     return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err,
-                      static_cast<const float*>(a.seg_omega_prev), a.seg_agg_out);
+                      static_cast<const float*>(a.seg_omega_prev), a.seg_agg_out, a.loss_target, a.loss_out,
+                      a.loss_state_out);
 }
 template <int NT, int RPT, int NS>
 static cudaError_t launch_bwd(const BBArgs& a, cudaStream_t st) {
@@ -1199,9 +1294,9 @@ static cudaError_t dispatch(const BBArgs& a, cudaStream_t st) {
     return cudaErrorInvalidConfiguration;
 }
 
-template <int NT, int RPT>
+template <int NT, int RPT, bool LOSS = false>
 static cudaError_t launch_bwd_xyz(const BBArgs& a, cudaStream_t st) {
-    auto k = bb_backward_xyz_kernel<NT, RPT>;
+    auto k = bb_backward_xyz_kernel<NT, RPT, LOSS>;
     const int tile = NT * RPT;
     const size_t sm = BBSmem<NT>::kData + 2 * round16(16 + 36 * tile + 12) + 2 * round16(16 + 36 * tile) +
                       round16(16 + 12 * tile);
@@ -1215,7 +1310,8 @@ static cudaError_t launch_bwd_xyz(const BBArgs& a, cudaStream_t st) {
     }
     const int grid = a.B < grid_cap ? a.B : grid_cap;
     return launch_pdl(k, grid, NT, sm, st, static_cast<const float*>(a.coords), a.lengths, a.B, a.Lmax,
-                      a.grad_coords, a.grad_angles, a.err, a.seg_totals, a.n_seg, a.seg);
+                      LOSS ? a.loss_target : a.grad_coords, a.grad_angles, a.err, a.seg_totals, a.n_seg, a.seg,
+                      a.loss_state, a.loss_grad);
 }
 
 // Shape of the coordinate backward: TPL_BBX=NTxRPT (tuning) or the default.
@@ -1247,6 +1343,14 @@ template <int NT, int RPT>
 static cudaError_t launch_bwd_xyz_dl(const BBArgs& a, cudaStream_t st);
 
 cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
+    if (a.loss_state) {  // f1 fused LRMSD: chain-serial shapes
+        const BBShape l = bbx_shape(a.B, a.Lmax);
+#define TPL_BBXL(NT_, R_) \
+    if (l.nt == NT_ && l.rpt == R_) return launch_bwd_xyz<NT_, R_, true>(a, st);
+        TPL_BBXL(128, 1) TPL_BBXL(128, 3) TPL_BBXL(128, 5) TPL_BBXL(256, 1) TPL_BBXL(256, 3) TPL_BBXL(256, 5)
+#undef TPL_BBXL
+        return cudaErrorInvalidConfiguration;
+    }
     if (!a.seg_totals && dl_enabled(a.B, a.Lmax)) {
         const BBShape d = bbx_dl_shape(a.B, a.Lmax);
         if (d.nt == 128 && d.rpt == 1) return launch_bwd_xyz_dl<128, 1>(a, st);
@@ -1361,7 +1465,20 @@ static cudaError_t dispatch_fwd_dl(const BBArgs& a, cudaStream_t st) {
     return cudaErrorInvalidConfiguration;
 }
 
+template <int NS>
+static cudaError_t dispatch_fwd_loss(const BBArgs& a, cudaStream_t st) {  // f1: 128-thread chain-serial shapes
+    static const int opts[4] = {1, 3, 5, 7};
+    int r = 7;
+    for (int i = 0; i < 4; ++i)
+        if (128 * opts[i] >= a.Lmax) { r = opts[i]; break; }
+    if (r == 1) return launch_fwd<128, 1, NS, true>(a, st);
+    if (r == 3) return launch_fwd<128, 3, NS, true>(a, st);
+    if (r == 5) return launch_fwd<128, 5, NS, true>(a, st);
+    return launch_fwd<128, 7, NS, true>(a, st);
+}
+
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st) {
+    if (a.loss_out) return a.ns == 0 ? dispatch_fwd_loss<0>(a, st) : dispatch_fwd_loss<1>(a, st);
     if (!a.seg_agg_out && dl_enabled(a.B, a.Lmax))
         return a.ns == 0 ? dispatch_fwd_dl<0>(a, st) : dispatch_fwd_dl<1>(a, st);
     return a.ns == 0 ? dispatch<true, 0>(a, st) : dispatch<true, 1>(a, st);

@@ -132,7 +132,8 @@ int64_t tpl_backbone_atoms(int32_t L) { return L < 0 ? 0 : 3 * static_cast<int64
 size_t tpl_workspace_bytes(int32_t model, int32_t B, int32_t Lmax) {
     if (B < 1 || Lmax < 1) return kWsHeader;
     const size_t tiles = static_cast<size_t>(max_tiles_for(model, Lmax));
-    return kWsHeader + static_cast<size_t>(B) * tiles * 16 * sizeof(float);
+    const size_t slots = kWsHeader + static_cast<size_t>(B) * tiles * 16 * sizeof(float);
+    return slots;
 }
 
 tpl_status tpl_sync_status(void* stream, void* workspace) {
@@ -228,6 +229,60 @@ tpl_status tpl_backbone_backward_from_coords(const float* coords, const int32_t*
     a.max_tiles = max_tiles_for(TPL_MODEL_BACKBONE, Lmax);
     cudaError_t e = bb_backward_xyz_launch(a, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "backbone backward (from coords) launch");
+    return TPL_OK;
+}
+
+// ---------------------------------------------------------------- f1: backbone + LRMSD, fused
+tpl_status tpl_backbone_lrmsd_forward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                      const float* target, float* coords, float* lrmsd, float* state,
+                                      void* workspace, size_t ws_bytes, void* stream) {
+    tpl_status s = bb_common(angles, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!target || !coords || !lrmsd || !state) return fail(TPL_ERR_NULL, "target/coords/lrmsd/state is NULL");
+    if (!aligned4(target) || !aligned4(coords) || !aligned4(lrmsd) || !aligned4(state))
+        return fail(TPL_ERR_ALIGN, "pointers not 4-byte aligned");
+    BBArgs a{};
+    a.angles = angles;
+    a.lengths = lengths;
+    a.B = B;
+    a.Lmax = Lmax;
+    a.coords = coords;
+    a.err = static_cast<unsigned*>(workspace);
+    a.ws_prefix = reinterpret_cast<float*>(static_cast<char*>(workspace) + kWsHeader);
+    a.max_tiles = max_tiles_for(TPL_MODEL_BACKBONE, Lmax);
+    a.ns = ns_policy();
+    a.K = backbone_constants();
+    a.loss_target = target;
+    a.loss_out = lrmsd;
+    a.loss_state_out = state;
+    cudaError_t e = bb_forward_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "fused backbone+LRMSD forward launch");
+    return TPL_OK;
+}
+
+tpl_status tpl_backbone_lrmsd_backward(const float* coords, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                       const float* target, const float* state, const float* grad_lrmsd,
+                                       float* grad_angles, void* workspace, size_t ws_bytes, void* stream) {
+    tpl_status s = bb_common(coords, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!target || !state || !grad_lrmsd || !grad_angles)
+        return fail(TPL_ERR_NULL, "target/state/grad_lrmsd/grad_angles is NULL");
+    if (!aligned4(target) || !aligned4(state) || !aligned4(grad_lrmsd) || !aligned4(grad_angles))
+        return fail(TPL_ERR_ALIGN, "pointers not 4-byte aligned");
+    BBArgs a{};
+    a.lengths = lengths;
+    a.B = B;
+    a.Lmax = Lmax;
+    a.coords = const_cast<float*>(coords);
+    a.grad_angles = grad_angles;
+    a.err = static_cast<unsigned*>(workspace);
+    a.ws_prefix = reinterpret_cast<float*>(static_cast<char*>(workspace) + kWsHeader);
+    a.max_tiles = max_tiles_for(TPL_MODEL_BACKBONE, Lmax);
+    a.loss_target = target;
+    a.loss_state = state;
+    a.loss_grad = grad_lrmsd;
+    cudaError_t e = bb_backward_xyz_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "fused LRMSD+backbone backward launch");
     return TPL_OK;
 }
 

@@ -46,6 +46,12 @@ struct BBArgs {
     float* seg_agg_out;           // [B][12] the segment's aggregate transform
     const float* seg_totals;      // [n_seg][B][12] (S, T about c, c, pad) of every segment
     int n_seg, seg;
+    // f1 fused LRMSD (nullptr otherwise): see tpl_backbone_lrmsd_*
+    const float* loss_target;  // [B][3*Lmax][3] the reference coordinates y
+    float* loss_out;           // [B] LRMSD (forward)
+    float* loss_state_out;     // [B][16] U, barycentres, 1/(N LRMSD) (forward)
+    const float* loss_state;   // [B][16] U, barycentres, 1/(N LRMSD) (backward)
+    const float* loss_grad;    // [B] dL/dLRMSD (backward)
 };
 
 bool pdl_enabled();  // capi.cu: programmatic dependent launch on (TPL_PDL != 0)

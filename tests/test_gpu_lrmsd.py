@@ -82,3 +82,32 @@ def test_pipeline_angles_to_lrmsd_gradient(tpl, oracle_lib):
     for b in range(B):
         assert np.abs(g[b] - G[b]).max() / np.abs(G[b]).max() <= 2e-3
     assert abs(float(loss.detach()) - vals.sum()) <= 1e-3 * vals.sum()
+
+
+@pytest.mark.parametrize("B,L,lengths", [(4, 300, None), (5, 700, [700, 1, 2, 350, 699]), (2, 2300, [2300, 1500])])
+def test_fused_backbone_lrmsd(tpl, oracle_lib, B, L, lengths):
+    """f1 fused (tpl_backbone_lrmsd_*): LRMSD values and dLRMSD/dangles == oracle
+    backbone + oracle LRMSD (Q19) + oracle Eq. 2, ragged and multi-tile."""
+    ang = synth.angles_uniform(B, L, 3, 41 + L)
+    ref = synth.angles_uniform(B, L, 3, 42 + L)
+    ln = torch.full((B,), L, dtype=torch.int32) if lengths is None else torch.tensor(lengths, dtype=torch.int32)
+    target = tpl.backbone(ref.cuda(), ln.cuda()).detach()
+    a = ang.cuda().requires_grad_(True)
+    vals_gpu, coords = tpl.backbone_lrmsd(a, target, ln.cuda())
+    gl = synth.grad_normal((B,), 43).abs() + 0.5  # dL/dLRMSD per chain
+    (vals_gpu * gl.cuda()).sum().backward()
+    a64, lnn = synth.numpy64(ang), ln.numpy()
+    X = oracle_lib.backbone_forward(a64, lnn)
+    Y = target.cpu().numpy().astype(np.float64)
+    vals, gx = OL.batch(X, Y, [3 * int(l) for l in lnn])
+    gx = gx * gl.numpy().astype(np.float64)[:, None, None]
+    G = oracle_lib.backbone_backward(a64, lnn, gx)
+    g = a.grad.cpu().numpy()
+    v = vals_gpu.detach().cpu().numpy()
+    for b in range(B):
+        Lb = int(lnn[b])
+        assert abs(v[b] - vals[b]) <= 1e-3 * max(vals[b], 1e-3), (b, v[b], vals[b])
+        if Lb > 1:
+            rel = np.abs(g[b, :Lb] - G[b, :Lb]).max() / np.abs(G[b, :Lb]).max()
+            assert rel <= 2e-3, (b, rel)
+        assert np.abs(coords[b, :3 * Lb].cpu().numpy() - X[b, :3 * Lb]).max() <= 5e-3
