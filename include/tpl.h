@@ -136,6 +136,15 @@ TPL_API tpl_status tpl_backbone_backward_from_coords(const float* coords, const 
                                              int32_t Lmax, const float* grad_coords, float* grad_angles,
                                              void* workspace, size_t ws_bytes, void* stream);
 
+/* precise mode: the same map as tpl_backbone_forward (P:143-175,
+ * Q1/Q2) computed entirely in fp64 (the paper's decimal theta/d, fp64 sincos,
+ * transforms and scan), coordinates rounded once to fp32.  For regular chains
+ * that span hundreds to thousands of Angstrom, where the fp32 path's rounding
+ * crosses 1e-3 A (f2).  Slower: fp64 arithmetic throughout. */
+TPL_API tpl_status tpl_backbone_forward_precise(const float* angles, const int32_t* lengths, int32_t B,
+                                        int32_t Lmax, float* coords, void* workspace, size_t ws_bytes,
+                                        void* stream);
+
 /* the backbone map and the LRMSD loss (PAPER §4)
  * fused: the forward also reduces, per chain, the moments of (r, y) over the
  * chain's 3L atoms against the reference y [B][3*Lmax][3] and returns

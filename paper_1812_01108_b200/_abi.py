@@ -31,7 +31,7 @@ EXPORTS = [
     "tpl_tables_n_types", "tpl_fullatom_atoms", "tpl_fullatom_forward", "tpl_fullatom_backward",
     "tpl_fullatom_backward_from_coords", "tpl_tables_backward_from_coords_ok",
     "tpl_lrmsd_forward", "tpl_lrmsd_backward",
-    "tpl_backbone_lrmsd_forward", "tpl_backbone_lrmsd_backward", "tpl_backbone_segment_forward", "tpl_backbone_segment_place", "tpl_backbone_segment_totals",
+    "tpl_backbone_forward_precise", "tpl_backbone_lrmsd_forward", "tpl_backbone_lrmsd_backward", "tpl_backbone_segment_forward", "tpl_backbone_segment_place", "tpl_backbone_segment_totals",
     "tpl_backbone_segment_backward", "tpl_paper_backbone_saved_floats", "tpl_paper_backbone_forward", "tpl_paper_backbone_backward",
 ]
 
@@ -96,6 +96,8 @@ def _load():
     L.tpl_fullatom_backward_from_coords.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]
     L.tpl_tables_backward_from_coords_ok.restype = i32
     L.tpl_tables_backward_from_coords_ok.argtypes = [vp]
+    L.tpl_backbone_forward_precise.restype = ctypes.c_int
+    L.tpl_backbone_forward_precise.argtypes = [vp, vp, i32, i32, vp, vp, sz, vp]
     L.tpl_backbone_lrmsd_forward.restype = ctypes.c_int
     L.tpl_backbone_lrmsd_forward.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp, sz, vp]
     L.tpl_backbone_lrmsd_backward.restype = ctypes.c_int
@@ -261,6 +263,18 @@ def tpl_fullatom_backward_from_coords(handle, coords, restype, lengths, grad_coo
 
 def tpl_tables_backward_from_coords_ok(handle):
     return bool(lib.tpl_tables_backward_from_coords_ok(ctypes.c_void_p(handle)))
+
+
+def tpl_backbone_forward_precise(angles, lengths, coords, workspace, stream=None):
+    """f2: the backbone forward computed in fp64 internally (coords rounded to fp32)."""
+    B, Lmax, three = angles.shape
+    if three != BB_SLOTS or tuple(coords.shape) != (B, 3 * Lmax, 3) or tuple(lengths.shape) != (B,):
+        raise ValueError("shapes: angles [B,Lmax,3], lengths [B], coords [B,3*Lmax,3]")
+    _check(lib.tpl_backbone_forward_precise(_dev(angles, torch.float32, "angles"),
+                                            _dev(lengths, torch.int32, "lengths"), B, Lmax,
+                                            _dev(coords, torch.float32, "coords"),
+                                            _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                            _stream(stream)))
 
 
 def tpl_backbone_lrmsd_forward(angles, lengths, target, coords, lrmsd, state, workspace, stream=None):

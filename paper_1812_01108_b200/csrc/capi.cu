@@ -232,6 +232,25 @@ tpl_status tpl_backbone_backward_from_coords(const float* coords, const int32_t*
     return TPL_OK;
 }
 
+// ---------------------------------------------------------------- f2: fp64-internal forward
+tpl_status tpl_backbone_forward_precise(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                        float* coords, void* workspace, size_t ws_bytes, void* stream) {
+    tpl_status s = bb_common(angles, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!coords) return fail(TPL_ERR_NULL, "coords is NULL");
+    if (!aligned4(coords)) return fail(TPL_ERR_ALIGN, "coords not 4-byte aligned");
+    BBArgs a{};
+    a.angles = angles;
+    a.lengths = lengths;
+    a.B = B;
+    a.Lmax = Lmax;
+    a.coords = coords;
+    a.err = static_cast<unsigned*>(workspace);
+    cudaError_t e = bb_forward_precise_launch(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "precise backbone forward launch");
+    return TPL_OK;
+}
+
 // ---------------------------------------------------------------- f1: backbone + LRMSD, fused
 tpl_status tpl_backbone_lrmsd_forward(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
                                       const float* target, float* coords, float* lrmsd, float* state,

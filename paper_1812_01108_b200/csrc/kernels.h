@@ -62,6 +62,7 @@ cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st);  // a.coords is the input
 int bb_dl_max_tiles(int Lmax);
+cudaError_t bb_forward_precise_launch(const BBArgs& a, cudaStream_t st);  // f2: fp64-internal forward
 // f4 across ranks (segment.cu)
 cudaError_t segment_totals_launch(const BBArgs& a, float* totals, cudaStream_t st);
 cudaError_t segment_place_launch(const BBArgs& a, const float* aggs, int seg, cudaStream_t st);  // per-chain carry slots of the decoupled backbone kernels

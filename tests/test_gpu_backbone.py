@@ -296,3 +296,28 @@ def test_segments_across_ranks_match_oracle(tpl, oracle_lib, n_seg):
     lengths = torch.full((B,), L, dtype=torch.int32)
     c, g = _check(oracle_lib, ang, lengths, grad, coords, gang, coord_tol=2e-3)
     print(f"{n_seg} segments, L={L}: max coord err {c:.3e} A, grad rel err {g:.3e}")
+
+
+def test_precise_mode(tpl, oracle_lib):
+    """the fp64-internal forward stays within 1e-3 A where the fp32 path
+    does not (regular chains spanning up to ~2600 A), and agrees on random chains."""
+    from paper_1812_01108_b200 import _abi
+
+    cases = [("random", synth.angles_uniform(3, 2300, 3, 9301), [2300, 1, 1000])]
+    cases += [(k, synth.regular_angles(2, 2000, k), [2000, 1999]) for k in ("helix", "strand", "extended")]
+    for name, ang, lengths in cases:
+        B, Lmax, _ = ang.shape
+        ln = torch.tensor(lengths, dtype=torch.int32)
+        coords = torch.full((B, 3 * Lmax, 3), float("nan"), device="cuda")
+        ws = torch.zeros(_abi.tpl_workspace_bytes(0, B, Lmax), dtype=torch.uint8, device="cuda")
+        _abi.tpl_backbone_forward_precise(ang.cuda(), ln.cuda(), coords, ws)
+        _abi.tpl_sync_status(ws)
+        c = coords.cpu().numpy()
+        X = oracle_lib.backbone_forward(synth.numpy64(ang), ln.numpy())
+        for b, L in enumerate(lengths):
+            err = np.abs(c[b, :3 * L] - X[b, :3 * L]).max()
+            # fp32 rounding of the output: half an ulp of |r| (up to ~2^11 A here)
+            bound = max(1e-5, 2.0 ** -23 * np.abs(X[b, :3 * L]).max())
+            print(f"precise {name} L={L}: max err {err:.3e} A (fp32 output ulp/2 {bound:.1e})")
+            assert err <= 1e-3 and err <= 4 * bound
+            assert np.isnan(c[b, 3 * L:]).all()

@@ -24,6 +24,7 @@ def main():
     p.add_argument("--L", type=int, default=700)
     p.add_argument("--K", type=int, default=120)
     p.add_argument("--xyz", action="store_true", help="backward from the forward's coordinates")
+    p.add_argument("--precise", action="store_true", help="the fp64-internal forward (f2)")
     a = p.parse_args()
     torch.cuda.set_device(0)
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
@@ -34,7 +35,10 @@ def main():
                  c=torch.empty(a.B, 3 * a.L, 3, device="cuda"), ga=torch.empty(a.B, a.L, 3, device="cuda"),
                  ws=torch.zeros(_abi.tpl_workspace_bytes(0, a.B, a.L), dtype=torch.uint8, device="cuda"))
             for _ in range(n)]
-    if a.xyz:
+    if a.precise:
+        fwd = lambda s: _abi.tpl_backbone_forward_precise(s["a"], s["l"], s["c"], s["ws"])  # noqa: E731
+        bwd = lambda s: _abi.tpl_backbone_backward_from_coords(s["c"], s["l"], s["g"], s["ga"], s["ws"])  # noqa: E731
+    elif a.xyz:
         fwd = lambda s: _abi.tpl_backbone_forward(s["a"], s["l"], s["c"], s["ws"])  # noqa: E731
         bwd = lambda s: _abi.tpl_backbone_backward_from_coords(s["c"], s["l"], s["g"], s["ga"], s["ws"])  # noqa: E731
     else:
@@ -65,7 +69,7 @@ def main():
         return best
 
     f, b, fb = timeit([fwd]), timeit([bwd]), timeit([fwd, bwd])
-    print(f"{'xyz ' if a.xyz else ''}{os.environ.get('TPL_BBX', '')} B={a.B} L={a.L} sets={n}: fwd {f:.2f} us, bwd {b:.2f} us, fwd+bwd step {fb:.2f} us "
+    print(f"{'precise ' if a.precise else 'xyz ' if a.xyz else ''}{os.environ.get('TPL_BBX', '')} B={a.B} L={a.L} sets={n}: fwd {f:.2f} us, bwd {b:.2f} us, fwd+bwd step {fb:.2f} us "
           f"(sum {f + b:.2f}, step overhead {fb - f - b:+.2f})")
 
 
