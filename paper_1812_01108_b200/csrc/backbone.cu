@@ -768,7 +768,10 @@ __device__ __forceinline__ void bbx_issue(const BBIter& it, const float* coords,
 // kLoss (f1, fused LRMSD): grad_coords is the LRMSD target y, and dL/dr_i =
 // dL/dLRMSD (x~_i - U^T y~_i) / (N LRMSD) (reading Q19) is formed
 // on the fly from the forward's state -- no dL/dr array is written or read.
-template <int NT, int RPT, bool kLoss = false>
+// kDB: two staging buffers (the next item's tiles load during this one); without
+// it one buffer, refilled after the walk -- for grids where every CTA owns one
+// item, so that twice the threads fit per SM.
+template <int NT, int RPT, bool kLoss = false, bool kDB = true>
 __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_kernel(const float* __restrict__ coords,
                                                              const int* __restrict__ lengths, int B, int Lmax,
                                                              const float* __restrict__ grad_coords,
@@ -785,11 +788,13 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
     float* s_suf = reinterpret_cast<float*>(smem + S::kSuf);
     float* s_misc = reinterpret_cast<float*>(smem + S::kMisc);
-    char* s_x_buf = smem + S::kData;   // 2 x XB
-    char* s_g_buf = s_x_buf + 2 * XB;  // 2 x GB
-    char* s_go_base = s_g_buf + 2 * GB;
+    constexpr int NB = kDB ? 2 : 1;
+    char* s_x_buf = smem + S::kData;    // NB x XB
+    char* s_g_buf = s_x_buf + NB * XB;  // NB x GB
+    char* s_go_base = s_g_buf + NB * GB;
 
     const int tid = threadIdx.x;
+    TPL_STAMP(0);
     if (tid == 0) {
         mbar_init(bar, 1);
         mbar_init(bar + 1, 1);
@@ -810,12 +815,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
     bool has_ext = false;                                      // f4: later segments exist
     float ext[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, cnx = 0.f, cny = 0.f, cnz = 0.f;
     for (int k = 0; it.valid; ++k) {
-        const int buf = k & 1;
+        const int buf = kDB ? (k & 1) : 0;
         const int b = it.b, L = it.L, r0 = it.r0(), n = it.n(), pre = r0 > 0 ? 1 : 0;
         const bool last_tile = r0 + n == L;
         BBIter nx = it;
         nx.advance();
-        if (tid == 0 && nx.valid)
+        if (kDB && tid == 0 && nx.valid)
             bbx_issue(nx, coords, grad_coords, s_x_buf + (buf ^ 1) * XB, s_g_buf + (buf ^ 1) * GB, bar + (buf ^ 1));
         char* s_x_base = s_x_buf + buf * XB;
         char* s_g_base = s_g_buf + buf * GB;
@@ -827,6 +832,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
         mbar_wait(bar + buf, (phases >> buf) & 1u);
         phases ^= 1u << buf;
         __syncthreads();
+        if (k < 2) TPL_STAMP(2 + 4 * k);
         const float* s_x = reinterpret_cast<const float*>(s_x_base + sx.mis()) + 3 * pre;  // atom 0 of the tile
         const float* s_g = reinterpret_cast<const float*>(s_g_base + sg.mis());
         // dL/dr of one atom: the staged array, or (kLoss) the LRMSD gradient from x and y
@@ -883,25 +889,36 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
         }
         cpx = cx; cpy = cy; cpz = cz;
 
-        // pass 1: this thread's (S, T) about c
+        // pass 1: this thread's atoms into registers (positions about c, dL/dr, unit
+        // bond vectors -- all independent of the suffix sums), and its (S, T) about c
+        constexpr int APT = 3 * RPT;
+        float Px[APT], Py[APT], Pz[APT], Gx[APT], Gy[APT], Gz[APT], Ex[APT], Ey[APT], Ez[APT];
         float sum6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int a = 0; a < 3 * RPT; ++a) {
+        for (int a = 0; a < APT; ++a) {
+            Px[a] = Py[a] = Pz[a] = Gx[a] = Gy[a] = Gz[a] = Ex[a] = Ey[a] = Ez[a] = 0.f;
             if (a / 3 < nq) {
                 const float* x = s_x + 9 * rl0 + 3 * a;
                 const float* g = s_g + 9 * rl0 + 3 * a;
-                const float px = x[0] - cx, py = x[1] - cy, pz = x[2] - cz;
-                float gx, gy, gz;
-                grad_of(x, g, gx, gy, gz);
-                sum6[0] += gx; sum6[1] += gy; sum6[2] += gz;
-                sum6[3] += fmaf(py, gz, -pz * gy);
-                sum6[4] += fmaf(pz, gx, -px * gz);
-                sum6[5] += fmaf(px, gy, -py * gx);
+                const float x0 = x[0], x1 = x[1], x2 = x[2];
+                Px[a] = x0 - cx; Py[a] = x1 - cy; Pz[a] = x2 - cz;
+                grad_of(x, g, Gx[a], Gy[a], Gz[a]);
+                if (r0 + rl0 + a / 3 > 0 || a % 3 > 0) {  // atom 0 of the chain carries no angle
+                    const float ux = x0 - x[-3], uy = x1 - x[-2], uz = x2 - x[-1];
+                    const float inv = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
+                    Ex[a] = ux * inv; Ey[a] = uy * inv; Ez[a] = uz * inv;
+                }
+                sum6[0] += Gx[a]; sum6[1] += Gy[a]; sum6[2] += Gz[a];
+                sum6[3] += fmaf(Py[a], Gz[a], -Pz[a] * Gy[a]);
+                sum6[4] += fmaf(Pz[a], Gx[a], -Px[a] * Gz[a]);
+                sum6[5] += fmaf(Px[a], Gy[a], -Py[a] * Gx[a]);
             }
         }
         if (tid == 0) bulk_wait_read_all();  // the output staging is free again
+        if (k < 2) TPL_STAMP(3 + 4 * k);
         float su[6], tot6[6];
         block_exclusive_suffix6<NT>(sum6, carry6, s_suf, su, tot6);
+        if (k < 2) TPL_STAMP(4 + 4 * k);
         if (!nx.valid) pdl_trigger();
         if (has_ext) {  // later segments, about this tile's reference: T_c = T_n + (n - c) x S
             const float dx = cnx - cx, dy = cny - cy, dz = cnz - cz;
@@ -922,23 +939,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
                 float ga[3];
 #pragma unroll
                 for (int kk = 2; kk >= 0; --kk) {
-                    const int a = 3 * rl + kk;  // atom index within the tile
-                    const float* x = s_x + 3 * a;
-                    const float* g = s_g + 3 * a;
-                    const float x0 = x[0], x1 = x[1], x2 = x[2];
-                    const float px = x0 - cx, py = x1 - cy, pz = x2 - cz;
-                    float gx, gy, gz;
-                    grad_of(x, g, gx, gy, gz);
-                    if (j > 0 || kk > 0) {  // atom 0 of the chain carries no angle
-                        const float ux = x0 - x[-3], uy = x1 - x[-2], uz = x2 - x[-1];
-                        const float inv = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
-                        const float c0 = su[3] - fmaf(py, su[2], -pz * su[1]);
-                        const float c1 = su[4] - fmaf(pz, su[0], -px * su[2]);
-                        const float c2 = su[5] - fmaf(px, su[1], -py * su[0]);
-                        ga[kk] = inv * fmaf(ux, c0, fmaf(uy, c1, uz * c2));
-                    } else {
-                        ga[kk] = 0.f;
-                    }
+                    const int a = 3 * q + kk;  // the thread's atom (registers)
+                    const float px = Px[a], py = Py[a], pz = Pz[a], gx = Gx[a], gy = Gy[a], gz = Gz[a];
+                    const float c0 = su[3] - fmaf(py, su[2], -pz * su[1]);
+                    const float c1 = su[4] - fmaf(pz, su[0], -px * su[2]);
+                    const float c2 = su[5] - fmaf(px, su[1], -py * su[0]);
+                    ga[kk] = fmaf(Ex[a], c0, fmaf(Ey[a], c1, Ez[a] * c2));  // 0 for atom 0 of the chain
                     su[0] += gx; su[1] += gy; su[2] += gz;
                     su[3] += fmaf(py, gz, -pz * gy);
                     su[4] += fmaf(pz, gx, -px * gz);
@@ -952,6 +958,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
                 }
             }
         }
+        if (k < 2) TPL_STAMP(11 + k);
         if (tid == 0) {
             float w = last_tile ? 0.f : omega_next;
             if (last_tile && has_ext) {  // omega_{L-1} = e . T_n (the later segments about their N)
@@ -966,7 +973,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
         if (tid == 0) {
             span_store_bulk(so, s_go_base);
             bulk_commit();
+            if (!kDB && nx.valid) bbx_issue(nx, coords, grad_coords, s_x_buf, s_g_buf, bar);  // buffer released
         }
+        if (k < 2) TPL_STAMP(5 + 4 * k);
         span_store_edges_f32(so, s_go_base);
         omega_next = s_misc[0];
 #pragma unroll
@@ -975,6 +984,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
         it = nx;
     }
     if (tid == 0) bulk_wait_read_all();
+    TPL_STAMP(10);
 }
 
 // Decoupled coordinate backward: every (chain, tile) item sums its tile, publishes
@@ -1294,11 +1304,12 @@ static cudaError_t dispatch(const BBArgs& a, cudaStream_t st) {
     return cudaErrorInvalidConfiguration;
 }
 
-template <int NT, int RPT, bool LOSS = false>
+template <int NT, int RPT, bool LOSS = false, bool DB = true>
 static cudaError_t launch_bwd_xyz(const BBArgs& a, cudaStream_t st) {
-    auto k = bb_backward_xyz_kernel<NT, RPT, LOSS>;
+    auto k = bb_backward_xyz_kernel<NT, RPT, LOSS, DB>;
     const int tile = NT * RPT;
-    const size_t sm = BBSmem<NT>::kData + 2 * round16(16 + 36 * tile + 12) + 2 * round16(16 + 36 * tile) +
+    const int nb = DB ? 2 : 1;
+    const size_t sm = BBSmem<NT>::kData + nb * round16(16 + 36 * tile + 12) + nb * round16(16 + 36 * tile) +
                       round16(16 + 12 * tile);
     static size_t configured = 0;
     static int grid_cap = 0;
@@ -1359,6 +1370,10 @@ cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
         if (d.nt == 256 && d.rpt == 3) return launch_bwd_xyz_dl<256, 3>(a, st);
         return cudaErrorInvalidConfiguration;
     }
+    // one 768-residue tile per chain and at most ~3 chains per SM: single-buffered
+    // 256 x 3 (65 KB, 3 CTAs/SM) keeps every chain resident with 8 warps each
+    if (!std::getenv("TPL_BBX") && a.Lmax <= 768 && a.B <= 3 * sm_count())
+        return launch_bwd_xyz<256, 3, false, false>(a, st);
     const BBShape s = bbx_shape(a.B, a.Lmax);
 #define TPL_BBX(NT_, R_) \
     if (s.nt == NT_ && s.rpt == R_) return launch_bwd_xyz<NT_, R_>(a, st);

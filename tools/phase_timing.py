@@ -29,6 +29,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--B", type=int, default=256)
     p.add_argument("--L", type=int, default=700)
+    p.add_argument("--bwd", action="store_true", help="the coordinate backward (two tiles per CTA stamped)")
     a = p.parse_args()
     torch.cuda.set_device(0)
     L = _abi.lib
@@ -37,15 +38,38 @@ def main():
     ln = torch.full((a.B,), a.L, dtype=torch.int32, device="cuda")
     c = torch.empty(a.B, 3 * a.L, 3, device="cuda")
     ws = torch.zeros(_abi.tpl_workspace_bytes(0, a.B, a.L), dtype=torch.uint8, device="cuda")
+    g = torch.randn(a.B, 3 * a.L, 3, device="cuda")
+    ga = torch.empty(a.B, a.L, 3, device="cuda")
+
+    def run():
+        if a.bwd:
+            _abi.tpl_backbone_backward_from_coords(c, ln, g, ga, ws)
+        else:
+            _abi.tpl_backbone_forward(ang, ln, c, ws)
+
+    _abi.tpl_backbone_forward(ang, ln, c, ws)
     for _ in range(3):
-        _abi.tpl_backbone_forward(ang, ln, c, ws)
+        run()
     torch.cuda.synchronize()
     L.tpl_debug_stamps_clear()
-    _abi.tpl_backbone_forward(ang, ln, c, ws)
+    run()
     torch.cuda.synchronize()
     n = min(a.B, 4096)
     buf = (ctypes.c_ulonglong * (n * 16))()
     L.tpl_debug_stamps(buf, n * 16)
+    if a.bwd:
+        names = ["start", "tile A landed", "tile A pass1", "tile A scan", "tile A walk", "tile A stored",
+                 "tile B landed", "tile B pass1", "tile B scan", "tile B walk", "tile B stored", "end"]
+        st = np.array(buf, dtype=np.int64).reshape(n, 16)[:, [0, 2, 3, 4, 11, 5, 6, 7, 8, 12, 9, 10]]
+        st = st[(st > 0).all(axis=1)] if ((st > 0).all(axis=1)).any() else st[:, [0, 1, 2, 3, 4, 5, 11]]
+        t0 = st[:, 0].min()
+        rel = st - t0
+        print(f"bwd B={a.B} L={a.L}: CTAs with two tiles {len(st)}; span {rel[:, -1].max() / 1e3:.2f} us")
+        for i in range(st.shape[1]):
+            step = (st[:, i] - st[:, i - 1]) if i else rel[:, 0]
+            print(f"  {names[i] if st.shape[1] == 12 else str(i):15s} at median {np.median(rel[:, i]) / 1e3:6.2f} us"
+                  f"  phase median {np.median(step) / 1e3:6.2f} us")
+        return
     st = np.array(buf, dtype=np.int64).reshape(n, 16)[:, :10]
     t0 = st[:, 0].min()
     rel = st - t0
