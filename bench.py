@@ -622,6 +622,19 @@ def cpu_baseline(work, seconds):
             "sample": f"{what} (fwd + O(L^2) Eq. 2/Eq. 1 bwd, fp64), {dt:.1f} s", "host_cpus": os.cpu_count()}
 
 
+def ref_config(work, cfg, n):
+    """The same config keys and workload text as the GPU arm (run_ours)."""
+    if work.model == "backbone":
+        d = {"workload": f"backbone phi,psi,omega -> N,CA,C; L={cfg['L']}, batch {cfg['B']} per GPU",
+             "L": cfg["L"], "batch_per_gpu": cfg["B"]}
+    else:
+        d = {"workload": f"full-atom phi,psi,omega,chi1-5 -> heavy atoms; 20 random residue types; "
+                         f"L={cfg['L']}, batch {cfg['B']} per GPU", "L": cfg["L"], "batch_per_gpu": cfg["B"]}
+    d.update({"global_batch": cfg["B"], "parallelism": "host cores (OpenMP over chains)",
+              "sample_chains_per_step": n})
+    return d
+
+
 def run_reference(args):
     """--impl reference: the oracle timed as the reference arm (rank 0 only)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -685,7 +698,7 @@ def run_reference(args):
             "unit": "residues/s", "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": 1e3 * total / K,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded uniform angles, N(0,1) dL/dr)",
-            "config": {"workload": f"{work.model} L={cfg['L']} batch {cfg['B']}", "sample_chains_per_step": n},
+            "config": ref_config(work, cfg, n),
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "residues/s", "cores": threads, "kind": "oracle",
                              "sample": f"{n} chains per step of the {cfg['B']}-chain workload"},
