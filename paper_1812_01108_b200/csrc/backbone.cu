@@ -1197,7 +1197,12 @@ static int bb_nt_env() {  // TPL_BB_NT=32|128|256 forces the block size (tuning)
 // 9*RPT (coordinates) in shared memory are then bank-conflict free.
 // Forward: 128 threads, RPT in {1,3,5,7} (tile <= 896).  Backward keeps 9
 // floats per atom in registers: 256 threads, RPT in {1,3} (tile <= 768).
+static BBShape env_shape(const char* name);
 static BBShape bb_shape(bool fwd, int Lmax) {
+    if (fwd) {  // TPL_BBFS=NTxRPT forces the chain-serial forward shape (tuning)
+        static const BBShape e = env_shape("TPL_BBFS");
+        if (e.nt) return e;
+    }
     int nt = bb_nt_env();
     if (!nt) nt = (fwd || Lmax > 128) ? (fwd ? 128 : 256) : 128;
     static const int f128[4] = {1, 3, 5, 7}, f256[3] = {1, 3, 5}, b128[2] = {1, 3}, b256[2] = {1, 3},
