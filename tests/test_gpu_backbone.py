@@ -321,3 +321,17 @@ def test_precise_mode(tpl, oracle_lib):
             print(f"precise {name} L={L}: max err {err:.3e} A (fp32 output ulp/2 {bound:.1e})")
             assert err <= 1e-3 and err <= 4 * bound
             assert np.isnan(c[b, 3 * L:]).all()
+
+
+def test_decoupled_more_items_than_resident_ctas(tpl, oracle_lib):
+    """f4 within a GPU with more (chain, tile) items than co-resident CTAs: 296 ragged
+    chains up to 5000 residues (~1300 items) -- every CTA walks several items, later
+    tiles wait on earlier ones held by other CTAs.  Parity on sampled chains."""
+    B, Lmax = 296, 5000
+    ang = synth.angles_uniform(B, Lmax, 3, 9401)
+    grad = synth.grad_normal((B, 3 * Lmax, 3), 9402)
+    ln = synth.lengths_uniform(B, 1025, Lmax, 9403)
+    coords, gang = _run(tpl, ang, ln, grad, xyz=True)
+    lnn = ln.numpy()
+    sample = sorted({int(np.argmax(lnn)), int(np.argmin(lnn)), 7, 150})
+    _check(oracle_lib, ang, ln, grad, coords, gang, chains=sample, coord_tol=2e-3)
