@@ -1233,40 +1233,17 @@ static size_t bwd_smem(int rpt) {
            round16(16 + 12 * tile);
 }
 
-// Persistent grid: at most the resident CTAs, never more than the chains.
-static int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
+static int sm_count() { return device_sm_count(); }
 
-template <typename K>
-static int persistent_grid(K kernel, int nt, size_t smem, int B) {
-    const int sms = sm_count();
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, smem) != cudaSuccess || per_sm < 1)
-        per_sm = 1;
-    const long cap = long(per_sm) * sms;
-    return int(B < cap ? B : cap);
-}
 
 template <int NT, int RPT, int NS, bool LOSS = false>
 static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
     auto k = bb_forward_kernel<NT, RPT, NS, LOSS>;
     const size_t sm = fwd_smem<NT>(RPT, LOSS);
-    static size_t configured = 0;  // set the smem opt-in once per instance (not inside graph capture)
-    static int grid_cap = 0;
-    if (configured < sm) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        if (e != cudaSuccess) return e;
-        configured = sm;
-        grid_cap = persistent_grid(k, NT, sm, 1 << 30);
-    }
+    static LaunchCfg cfg;
+    cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
+    if (e != cudaSuccess) return e;
+    const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
     const int grid = a.B < grid_cap ? a.B : grid_cap;
     return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err,
                       static_cast<const float*>(a.seg_omega_prev), a.seg_agg_out, a.loss_target, a.loss_out,
@@ -1276,14 +1253,10 @@ template <int NT, int RPT, int NS>
 static cudaError_t launch_bwd(const BBArgs& a, cudaStream_t st) {
     auto k = bb_backward_kernel<NT, RPT, NS>;
     const size_t sm = bwd_smem<NT>(RPT);
-    static size_t configured = 0;
-    static int grid_cap = 0;
-    if (configured < sm) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        if (e != cudaSuccess) return e;
-        configured = sm;
-        grid_cap = persistent_grid(k, NT, sm, 1 << 30);
-    }
+    static LaunchCfg cfg;
+    cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
+    if (e != cudaSuccess) return e;
+    const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
     const int grid = a.B < grid_cap ? a.B : grid_cap;
     return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.grad_coords, a.grad_angles, a.err,
                       a.ws_prefix, a.max_tiles);
@@ -1316,14 +1289,10 @@ static cudaError_t launch_bwd_xyz(const BBArgs& a, cudaStream_t st) {
     const int nb = DB ? 2 : 1;
     const size_t sm = BBSmem<NT>::kData + nb * round16(16 + 36 * tile + 12) + nb * round16(16 + 36 * tile) +
                       round16(16 + 12 * tile);
-    static size_t configured = 0;
-    static int grid_cap = 0;
-    if (configured < sm) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        if (e != cudaSuccess) return e;
-        configured = sm;
-        grid_cap = persistent_grid(k, NT, sm, 1 << 30);
-    }
+    static LaunchCfg cfg;
+    cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
+    if (e != cudaSuccess) return e;
+    const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
     const int grid = a.B < grid_cap ? a.B : grid_cap;
     return launch_pdl(k, grid, NT, sm, st, static_cast<const float*>(a.coords), a.lengths, a.B, a.Lmax,
                       LOSS ? a.loss_target : a.grad_coords, a.grad_angles, a.err, a.seg_totals, a.n_seg, a.seg,
@@ -1433,14 +1402,10 @@ template <int NT, int RPT, int NS>
 static cudaError_t launch_fwd_dl(const BBArgs& a, cudaStream_t st) {
     auto k = bb_forward_dl_kernel<NT, RPT, NS>;
     const size_t sm = fwd_smem<NT>(RPT);
-    static size_t configured = 0;
-    static int grid_cap = 0;
-    if (configured < sm) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        if (e != cudaSuccess) return e;
-        configured = sm;
-        grid_cap = persistent_grid(k, NT, sm, 1 << 30);
-    }
+    static LaunchCfg cfg;
+    cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
+    if (e != cudaSuccess) return e;
+    const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
     const int max_tiles = (a.Lmax + NT * RPT - 1) / (NT * RPT);
     const long items = long(a.B) * max_tiles;
     const int grid = int(items < grid_cap ? items : grid_cap);  // co-resident: waits only on smaller items
@@ -1453,14 +1418,10 @@ static cudaError_t launch_bwd_xyz_dl(const BBArgs& a, cudaStream_t st) {
     const int tile = NT * RPT;
     const size_t sm = BBSmem<NT>::kData + 2 * round16(16 + 36 * tile + 24) + 2 * round16(16 + 36 * tile) +
                       round16(16 + 12 * tile);
-    static size_t configured = 0;
-    static int grid_cap = 0;
-    if (configured < sm) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        if (e != cudaSuccess) return e;
-        configured = sm;
-        grid_cap = persistent_grid(k, NT, sm, 1 << 30);
-    }
+    static LaunchCfg cfg;
+    cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
+    if (e != cudaSuccess) return e;
+    const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
     const int max_tiles = (a.Lmax + tile - 1) / tile;
     const long items = long(a.B) * max_tiles;
     const int grid = int(items < grid_cap ? items : grid_cap);

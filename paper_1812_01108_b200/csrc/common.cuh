@@ -12,7 +12,10 @@
 // mbarrier completion, head/tail handled by plain loads so any 4-byte aligned
 // range can be staged.
 #pragma once
+#include <atomic>
 #include <cstdint>
+#include <mutex>
+
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -471,6 +474,41 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Host: launch with programmatic stream serialization (TPL_PDL=0 disables).
+// SMs of the current device (cached once per process).
+inline int device_sm_count() {
+    static const int sms = [] {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 148;
+    }();
+    return sms;
+}
+
+// Per kernel instance: the dynamic shared-memory opt-in, raised monotonically to
+// the largest size requested so far, and the co-resident grid (resident CTAs per
+// SM x SMs) at that size for the persistent kernels.  Thread-safe; the attribute
+// call happens on first use of a size (outside graph capture in practice).
+struct LaunchCfg {
+    std::atomic<size_t> smem{0};
+    std::atomic<int> cap{0};
+    std::mutex m;
+};
+template <typename K>
+inline cudaError_t ensure_launch_cfg(LaunchCfg& c, K kernel, int block, size_t smem) {
+    if (c.smem.load(std::memory_order_acquire) >= smem && smem > 0) return cudaSuccess;
+    std::lock_guard<std::mutex> g(c.m);
+    if (c.smem.load(std::memory_order_relaxed) >= smem && smem > 0) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    c.cap.store(per_sm * device_sm_count(), std::memory_order_relaxed);
+    c.smem.store(smem, std::memory_order_release);
+    return cudaSuccess;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
                               Args... args) {

@@ -930,12 +930,9 @@ template <int NT, int NS, bool TS, int MINB>
 static cudaError_t fa_fwd_v(const FAArgs& a, cudaStream_t st) {
     auto k = fa_forward_kernel<NT, 1, NS, TS, MINB>;
     const size_t sm = fa_fwd_smem<NT, 1>(a.n_types, a.max_atoms, TS);
-    static size_t configured = 0;  // set the smem opt-in once per size (not inside graph capture)
-    if (configured < sm) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        if (e != cudaSuccess) return e;
-        configured = sm;
-    }
+    static LaunchCfg cfg;  // one grid CTA per chain: only the shared-memory opt-in is used
+    cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
+    if (e != cudaSuccess) return e;
     return launch_pdl(k, a.B, NT, sm, st, a, a.max_atoms);
 }
 // TPL_FAF=NTxTSxMINB (tuning) or the default.
@@ -973,12 +970,9 @@ template <int NS>
 static cudaError_t fa_bwd(const FAArgs& a, cudaStream_t st) {
     auto k = fa_backward_kernel<kFABwdThreads, kFABwdRPT, NS>;
     const size_t sm = fa_bwd_smem<kFABwdThreads, kFABwdRPT>(a.n_types, a.max_atoms);
-    static size_t configured = 0;
-    if (configured < sm) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        if (e != cudaSuccess) return e;
-        configured = sm;
-    }
+    static LaunchCfg cfg;  // one grid CTA per chain: only the shared-memory opt-in is used
+    cudaError_t e = ensure_launch_cfg(cfg, k, kFABwdThreads, sm);
+    if (e != cudaSuccess) return e;
     return launch_pdl(k, a.B, kFABwdThreads, sm, st, a, a.max_atoms);
 }
 
@@ -1009,12 +1003,9 @@ static cudaError_t fa_bwd_xyz(const FAArgs& a, cudaStream_t st) {
     const int max_tiles = (a.Lmax + TILE - 1) / TILE;
     const size_t sm = FAXSmem<NT>::kTable + fax_table_bytes(TS, a.n_types) + r16(4 * (max_tiles + 1)) +
                       r16(16 + a.Lmax) + (DB ? 2 : 1) * fax_tile_layout(TILE, a.max_atoms).total + r16(32 * TILE);
-    static size_t configured = 0;
-    if (configured < sm) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        if (e != cudaSuccess) return e;
-        configured = sm;
-    }
+    static LaunchCfg cfg;  // one grid CTA per chain: only the shared-memory opt-in is used
+    cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
+    if (e != cudaSuccess) return e;
     return launch_pdl(k, a.B, NT, sm, st, a, max_tiles);
 }
 
