@@ -68,6 +68,12 @@ __device__ __forceinline__ float axis_moment(float ex, float ey, float ez, float
     return fmaf(ex, c0, fmaf(ey, c1, ez * c2));
 }
 
+// r° of atom k as one 16-byte load (the table row is float[4], 16-byte aligned)
+__device__ __forceinline__ float4 r0_of(const FAType& T, int k) { return *reinterpret_cast<const float4*>(T.r[k]); }
+__device__ __forceinline__ void apply4(const Aff& M, float4 r, float& ox, float& oy, float& oz) {
+    apply(M, r.x, r.y, r.z, ox, oy, oz);
+}
+
 // Backbone chunk of one thread: residues [rl0, rl0+RPT) of the tile.
 // Saves the local N, CA and C frames of every residue and returns the
 // chunk aggregate (product of all its transforms) in M.
@@ -214,9 +220,9 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
                 const float* ang = s_ang + 8 * rl;
                 float* o = s_out + 3 * off;
                 int k = 0;
-                for (; k < T.n_N; ++k) apply(gN, T.r[k][0], T.r[k][1], T.r[k][2], o[3 * k], o[3 * k + 1], o[3 * k + 2]);
+                for (; k < T.n_N; ++k) apply4(gN, r0_of(T, k), o[3 * k], o[3 * k + 1], o[3 * k + 2]);
                 for (; k < T.n_N + T.n_CA; ++k)
-                    apply(gCA, T.r[k][0], T.r[k][1], T.r[k][2], o[3 * k], o[3 * k + 1], o[3 * k + 2]);
+                    apply4(gCA, r0_of(T, k), o[3 * k], o[3 * k + 1], o[3 * k + 2]);
                 Aff G = gCA;
                 for (int g = 0; g < T.n_groups; ++g) {
                     const FAGroup& gr = T.g[g];
@@ -230,10 +236,10 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
                     const BondC bc{gr.ct, gr.st, gr.d};
                     aff_bond(G, c, s, bc);
                     for (k = gr.first_atom; k < gr.end_atom; ++k)
-                        apply(G, T.r[k][0], T.r[k][1], T.r[k][2], o[3 * k], o[3 * k + 1], o[3 * k + 2]);
+                        apply4(G, r0_of(T, k), o[3 * k], o[3 * k + 1], o[3 * k + 2]);
                 }
                 for (k = T.first_C; k < T.n_atoms; ++k)
-                    apply(gC, T.r[k][0], T.r[k][1], T.r[k][2], o[3 * k], o[3 * k + 1], o[3 * k + 2]);
+                    apply4(gC, r0_of(T, k), o[3 * k], o[3 * k + 1], o[3 * k + 2]);
                 off += T.n_atoms;
             }
         }
@@ -268,17 +274,17 @@ __device__ __forceinline__ void fa_residue_backward(const FAType& T, const float
     int k = 0;
     for (; k < T.n_N; ++k) {
         float x, y, z;
-        apply(gN, T.r[k][0], T.r[k][1], T.r[k][2], x, y, z);
+        apply4(gN, r0_of(T, k), x, y, z);
         cross_acc(R.nN, x - cx, y - cy, z - cz, gk[3 * k], gk[3 * k + 1], gk[3 * k + 2]);
     }
     for (; k < T.n_N + T.n_CA; ++k) {
         float x, y, z;
-        apply(gCA, T.r[k][0], T.r[k][1], T.r[k][2], x, y, z);
+        apply4(gCA, r0_of(T, k), x, y, z);
         cross_acc(R.all, x - cx, y - cy, z - cz, gk[3 * k], gk[3 * k + 1], gk[3 * k + 2]);
     }
     for (k = T.first_C; k < T.n_atoms; ++k) {
         float x, y, z;
-        apply(gC, T.r[k][0], T.r[k][1], T.r[k][2], x, y, z);
+        apply4(gC, r0_of(T, k), x, y, z);
         cross_acc(R.cC, x - cx, y - cy, z - cz, gk[3 * k], gk[3 * k + 1], gk[3 * k + 2]);
     }
     // side-chain branches: forward to the branch tip, then walk back
@@ -300,7 +306,7 @@ __device__ __forceinline__ void fa_residue_backward(const FAType& T, const float
             const FAGroup& gr = T.g[g];
             for (k = gr.first_atom; k < gr.end_atom; ++k) {
                 float x, y, z;
-                apply(G, T.r[k][0], T.r[k][1], T.r[k][2], x, y, z);
+                apply4(G, r0_of(T, k), x, y, z);
                 cross_acc(br, x - cx, y - cy, z - cz, gk[3 * k], gk[3 * k + 1], gk[3 * k + 2]);
             }
             if (gr.slot >= 0) go[gr.slot] = axis_moment(G.r00, G.r10, G.r20, G.t0 - cx, G.t1 - cy, G.t2 - cz, br);
