@@ -1236,6 +1236,21 @@ static size_t bwd_smem(int rpt) {
 static int sm_count() { return device_sm_count(); }
 
 
+// Grid of the chain-serial kernels: the co-resident CTAs, each walking chains
+// b, b + grid, ...  TPL_GRID=<m> uses m x that (0: one CTA per chain, which lets
+// the block scheduler balance ragged batches: config 4 214 -> 187 us, but 4096 x
+// 700 108 -> 117 us; dynamic chain claiming through a workspace counter cost
+// more in atomics than it saved).
+static int chain_grid(int B, int cap) {
+    static const int mult = [] {
+        const char* e = std::getenv("TPL_GRID");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (mult <= 0) return B;
+    const long g = long(mult) * cap;
+    return B < g ? B : int(g);
+}
+
 template <int NT, int RPT, int NS, bool LOSS = false>
 static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
     auto k = bb_forward_kernel<NT, RPT, NS, LOSS>;
@@ -1244,7 +1259,7 @@ static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
     const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
-    const int grid = a.B < grid_cap ? a.B : grid_cap;
+    const int grid = chain_grid(a.B, grid_cap);
     return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err,
                       static_cast<const float*>(a.seg_omega_prev), a.seg_agg_out, a.loss_target, a.loss_out,
                       a.loss_state_out);
@@ -1257,7 +1272,7 @@ static cudaError_t launch_bwd(const BBArgs& a, cudaStream_t st) {
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
     const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
-    const int grid = a.B < grid_cap ? a.B : grid_cap;
+    const int grid = chain_grid(a.B, grid_cap);
     return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.grad_coords, a.grad_angles, a.err,
                       a.ws_prefix, a.max_tiles);
 }
@@ -1293,7 +1308,7 @@ static cudaError_t launch_bwd_xyz(const BBArgs& a, cudaStream_t st) {
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
     const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
-    const int grid = a.B < grid_cap ? a.B : grid_cap;
+    const int grid = chain_grid(a.B, grid_cap);
     return launch_pdl(k, grid, NT, sm, st, static_cast<const float*>(a.coords), a.lengths, a.B, a.Lmax,
                       LOSS ? a.loss_target : a.grad_coords, a.grad_angles, a.err, a.seg_totals, a.n_seg, a.seg,
                       a.loss_state, a.loss_grad);
