@@ -9,21 +9,25 @@
 // Backward (Eq. 2): dr_j/dalpha_i = e_i x (r_j - r_i) for j > i
 // (e_i = x-axis of frame M_i, the rotation axis of R_x(alpha_i)), hence
 //   dL/dalpha_i = e_i . (T_i - r_i x S_i),  S_i = sum_{j>i} g_j,  T_i = sum_{j>i} r_j x g_j,
-// one reverse suffix sum per chain: O(L) instead of the paper's O(L^2).
-// The forward frames are recomputed from the angles (no saved state).  Each
-// thread works in the local frame of its chunk (positions relative to the
-// chunk start, gradients rotated into it): fewer flops than moving every
-// position and axis to the global frame, and smaller moments.
+// one reverse suffix sum per chain: O(L) instead of the paper's O(L^2).  Two
+// entry points: from the angles (bb_backward_kernel: the frames are recomputed,
+// each thread in the local frame of its chunk) and from the forward's
+// coordinates (bb_backward_xyz_kernel: e_i is the unit bond vector, no trig and
+// no transform scan -- the path the autograd layer and the bench take).
 //
 // Work decomposition: a CTA of NT threads owns one chain at a time; a tile is
-// NT*RPT residues; each thread composes RPT consecutive residues (3*RPT
-// transforms) in registers, then one block-wide affine scan combines the
-// chunks.  CTAs are persistent over chains (grid <= resident CTAs) and run a
-// two-deep TMA pipeline: the next work item's tile is bulk-copied into the
-// other shared-memory buffer while the current one is computed.  Work items:
+// NT*RPT residues; each thread handles RPT consecutive residues, one block-wide
+// scan combines the chunks.  CTAs are persistent over chains (grid <= resident
+// CTAs) and run a two-deep TMA pipeline: the next work item's tile is bulk-copied
+// into the other shared-memory buffer while the current one is computed.
 //   forward : every tile of every chain, first to last (prefix carried);
-//   backward: phase A = tile prefixes of all but the last tile (to the
-//             workspace), then phase B = tiles last to first (suffix carried).
+//   backward: from angles, phase A = tile prefixes of all but the last tile (to
+//             the workspace), then phase B = tiles last to first (suffix
+//             carried); from coordinates, tiles last to first only.
+// Few long chains (f4): the *_dl_kernel variants put the tiles of a chain on
+// different CTAs that exchange their aggregates through workspace slots.
+// Variants of the chain-serial kernels: chain segments over ranks (f4,
+// segment.cu) and the fused LRMSD loss (f1, kLoss).
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
