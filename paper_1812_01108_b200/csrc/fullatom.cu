@@ -18,6 +18,9 @@
 // Chi subtrees are residue-local: a side-chain branch is walked from its tip
 // back to the CA frame (frames undone with the rigid inverse of each bond)
 // accumulating the local sums.  One reverse suffix scan per chain: O(L).
+// fa_backward_xyz_kernel computes the same from the forward's coordinates:
+// every axis is the vector between two frame-origin atoms, so no angle, trig
+// or transform is needed (the path the autograd layer takes).
 #include <cstdio>
 #include <cstdlib>
 
