@@ -1,0 +1,104 @@
+"""Randomised GPU parity (seeded): shapes that cross tile and shape-selection
+boundaries, and huge angles that take the exact (Payne-Hanek) sincos path."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def abi():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1812_01108_b200 import _abi
+
+    return _abi
+
+
+def _bb(abi, ang, ln, grad):
+    B, Lmax, _ = ang.shape
+    a, l, g = ang.cuda(), ln.cuda(), grad.cuda()
+    c = torch.full((B, 3 * Lmax, 3), float("nan"), device="cuda")
+    ga = torch.full((B, Lmax, 3), float("nan"), device="cuda")
+    gx = torch.full((B, Lmax, 3), float("nan"), device="cuda")
+    ws = torch.zeros(abi.tpl_workspace_bytes(0, B, Lmax), dtype=torch.uint8, device="cuda")
+    abi.tpl_backbone_forward(a, l, c, ws)
+    abi.tpl_backbone_backward(a, l, g, ga, ws)
+    abi.tpl_backbone_backward_from_coords(c, l, g, gx, ws)
+    abi.tpl_sync_status(ws)
+    return c.cpu().numpy(), ga.cpu().numpy(), gx.cpu().numpy()
+
+
+def _check_bb(oracle_lib, ang, ln, grad, c, ga, gx, chains):
+    a64, lnn, g64 = synth.numpy64(ang), ln.numpy(), synth.numpy64(grad)
+    idx = np.array(chains)
+    X = oracle_lib.backbone_forward(a64[idx], lnn[idx])
+    G = oracle_lib.backbone_backward(a64[idx], lnn[idx], g64[idx])
+    for n, b in enumerate(idx):
+        L = int(lnn[b])
+        tol = 1e-3 if L <= 1000 else 5e-3
+        assert np.abs(c[b, :3 * L] - X[n, :3 * L]).max() <= tol, (b, L)
+        ref = G[n, :L]
+        scale = max(np.abs(ref).max(), 1e-30)
+        for g in (ga, gx):
+            assert np.abs(g[b, :L] - ref).max() / scale <= 1e-3, (b, L)
+        assert np.isnan(c[b, 3 * L:]).all() and np.isnan(ga[b, L:]).all() and np.isnan(gx[b, L:]).all()
+
+
+def test_huge_angles_backbone(abi, oracle_lib):
+    """|alpha| up to 3e7 (beyond the fast range 2^17): the tile is redone with the
+    exact reduction; results still match the oracle's fp64 sin/cos of the same fp32."""
+    B, L = 3, 400
+    ang = synth.angles_uniform(B, L, 3, 9501)
+    rng = np.random.default_rng(9502)
+    mask = rng.random((B, L, 3)) < 0.05
+    huge = rng.choice([1.0e6, -3.0e7, 123456.7, 2.0 ** 20 + 0.1, -987654.3], size=(B, L, 3))
+    ang = torch.where(torch.tensor(mask), torch.tensor(huge, dtype=torch.float32), ang)
+    grad = synth.grad_normal((B, 3 * L, 3), 9503)
+    ln = torch.tensor([400, 257, 3], dtype=torch.int32)
+    c, ga, gx = _bb(abi, ang, ln, grad)
+    _check_bb(oracle_lib, ang, ln, grad, c, ga, gx, [0, 1, 2])
+
+
+def test_huge_angles_fullatom(abi, oracle_lib, table):
+    import paper_1812_01108_b200 as tpl
+
+    B, L = 2, 60
+    ang = synth.angles_uniform(B, L, 8, 9511)
+    rng = np.random.default_rng(9512)
+    mask = rng.random((B, L, 8)) < 0.05
+    ang = torch.where(torch.tensor(mask), torch.tensor(rng.choice([4.0e5, -7.5e6], size=(B, L, 8)),
+                                                       dtype=torch.float32), ang)
+    rt = synth.restype_uniform(B, L, 20, 9513)
+    ln = torch.full((B,), L, dtype=torch.int32)
+    tables = tpl.Tables(table)
+    a = ang.cuda().requires_grad_(True)
+    coords = tpl.fullatom(a, rt.cuda(), ln.cuda(), tables)
+    grad = synth.grad_normal(tuple(coords.shape), 9514)
+    (coords * grad.cuda()).sum().backward()
+    X, _ = oracle_lib.fullatom_forward(table, synth.numpy64(ang), rt.numpy(), ln.numpy(), coords.shape[1])
+    G = oracle_lib.fullatom_backward(table, synth.numpy64(ang), rt.numpy(), ln.numpy(), synth.numpy64(grad))
+    c = coords.detach().cpu().numpy()
+    n_at = np.array([len(t["atoms"]) for t in table["types"]])
+    for b in range(B):
+        na = int(n_at[rt[b].numpy()].sum())
+        assert np.abs(c[b, :na] - X[b, :na]).max() <= 1e-3
+        assert np.abs(a.grad[b].cpu().numpy() - G[b]).max() / np.abs(G[b]).max() <= 1e-3
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_shapes_backbone(abi, oracle_lib, seed):
+    rng = np.random.default_rng(9600 + seed)
+    B = int(rng.integers(1, 24))
+    Lmax = int(rng.choice([1, 2, 7, 96, 129, 383, 385, 700, 769, 897, 1025, 1800, 2600]))
+    lengths = rng.integers(1, Lmax + 1, size=B)
+    lengths[rng.integers(0, B)] = Lmax
+    ang = synth.angles_uniform(B, Lmax, 3, 9700 + seed)
+    grad = synth.grad_normal((B, 3 * Lmax, 3), 9800 + seed)
+    ln = torch.tensor(lengths, dtype=torch.int32)
+    c, ga, gx = _bb(abi, ang, ln, grad)
+    chains = sorted(set(rng.choice(B, size=min(B, 4), replace=False).tolist()) | {int(np.argmax(lengths))})
+    _check_bb(oracle_lib, ang, ln, grad, c, ga, gx, chains)
