@@ -19,8 +19,10 @@
  * Errors      Host-detectable problems (NULL, B < 1, Lmax < 1, workspace too
  *             small, atom_stride too small, bad table) return a status BEFORE
  *             any launch and set tpl_last_error().  Device-detectable
- *             problems (lengths[b] outside [1, Lmax], a restype >= n_types)
- *             set a flag in the workspace, the offending chain is skipped,
+ *             problems (lengths[b] outside [1, Lmax], a restype >= n_types,
+ *             a chain with more atoms than atom_stride) set a flag in the
+ *             workspace, the offending chain is skipped (a full-atom chain
+ *             over atom_stride keeps the tiles that fit),
  *             and tpl_sync_status reports TPL_ERR_DEVICE_INPUT.  No C++
  *             exception crosses the ABI.
  * Workspace   Device buffer of tpl_workspace_bytes(model, B, Lmax) bytes,

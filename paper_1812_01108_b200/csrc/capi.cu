@@ -147,8 +147,9 @@ tpl_status tpl_sync_status(void* stream, void* workspace) {
     if (flags) {
         e = cudaMemset(workspace, 0, sizeof(unsigned));
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(error word)");
-        return fail(TPL_ERR_DEVICE_INPUT, "device input error flags 0x%x (%s%s)", flags,
-                    (flags & 1u) ? "length outside [1, Lmax] " : "", (flags & 2u) ? "restype >= n_types" : "");
+        return fail(TPL_ERR_DEVICE_INPUT, "device input error flags 0x%x (%s%s%s)", flags,
+                    (flags & 1u) ? "length outside [1, Lmax] " : "", (flags & 2u) ? "restype >= n_types " : "",
+                    (flags & 4u) ? "a chain's atoms exceed atom_stride" : "");
     }
     return TPL_OK;
 }

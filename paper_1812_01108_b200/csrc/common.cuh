@@ -612,6 +612,6 @@ __device__ __forceinline__ unsigned long long tpl_globaltimer() {
 
 // Device error word (workspace[0]): bit 0 = a chain length outside [1, Lmax],
 // bit 1 = a restype outside the table.  The offending chain is skipped.
-enum : unsigned { ERR_LENGTH = 1u, ERR_RESTYPE = 2u };
+enum : unsigned { ERR_LENGTH = 1u, ERR_RESTYPE = 2u, ERR_STRIDE = 4u };  // ERR_STRIDE: atoms > atom_stride
 
 }  // namespace tpl

@@ -200,6 +200,13 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
         }
         int tile_end_atoms;
         const int off0 = block_exclusive_sum_int<NT>(cnt, carry_atoms, s_int, &tile_end_atoms);
+        if (tile_end_atoms > a.atom_stride) {  // the chain's atoms do not fit its row: flag, skip
+            if (tid == 0) {
+                atomicOr(a.err, ERR_STRIDE);
+                bulk_wait_all();
+            }
+            return;
+        }
 
         Aff M;
         Aff FN[RPT], FCA[RPT], FC[RPT];
@@ -407,6 +414,10 @@ __global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_
             }
             int tile_end;
             block_exclusive_sum_int<NT>(cnt, carry_atoms, s_int, &tile_end);
+            if (tile_end > a.atom_stride) {
+                if (tid == 0) atomicOr(a.err, ERR_STRIDE);
+                return;
+            }
             Aff M;
             Aff FN[RPT], FCA[RPT], FC[RPT];
             fa_chunk<RPT>(s_ang, rl0, r0, TILE, M, FN, FCA, FC);
@@ -471,6 +482,13 @@ __global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_
         }
         int tile_end;
         const int off0 = block_exclusive_sum_int<NT>(cnt, carry_atoms, s_int, &tile_end);
+        if (tile_end > a.atom_stride) {
+            if (tid == 0) {
+                atomicOr(a.err, ERR_STRIDE);
+                bulk_wait_all();
+            }
+            return;
+        }
         // stage grad_coords of the tile's atoms (second round on the barrier)
         const Span sg = make_span(gcb + (size_t)carry_atoms * 3, (tile_end - carry_atoms) * 12);
         if (tid == 0) {
@@ -708,6 +726,10 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
         if (tid == 0) s_off[n_tiles] = carry;
         if (__syncthreads_or(bad)) {
             if (tid == 0) atomicOr(a.err, ERR_RESTYPE);
+            return;
+        }
+        if (carry > a.atom_stride) {  // uniform: carry is the block total
+            if (tid == 0) atomicOr(a.err, ERR_STRIDE);
             return;
         }
     }

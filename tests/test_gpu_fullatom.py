@@ -200,3 +200,33 @@ def test_from_coords_needs_origin_atoms(tpl, table):
     a = synth.angles_uniform(B, L, 8, 3).cuda().requires_grad_(True)
     tpl.fullatom(a, rt, ln, tables).sum().backward()
     assert torch.isfinite(a.grad).all()
+
+
+def test_atom_stride_too_small_is_flagged(tpl, table):
+    """A chain with more atoms than atom_stride is flagged on the device
+    (TPL_ERR_DEVICE_INPUT) instead of writing past its row; the other chains run."""
+    from paper_1812_01108_b200 import TplError, _abi
+
+    tables = tpl.Tables(table)
+    B, L = 3, 40
+    ang = synth.angles_uniform(B, L, 8, 61).cuda()
+    rt = synth.restype_uniform(B, L, 20, 62)
+    rt[1] = 17  # TRP: the largest type, so chain 1 needs the most atoms
+    apc, _ = tables.atoms(rt, torch.full((B,), L, dtype=torch.int32))
+    stride = int(apc[0].item()) if int(apc[0]) >= int(apc[2]) else int(apc[2])
+    stride = max(stride, int(sorted(apc.tolist())[1]))  # fits chains 0 and 2, not chain 1
+    assert int(apc[1]) > stride
+    guard = torch.full((B + 1, stride, 3), float("nan"), device="cuda")
+    coords = guard[:B]
+    ln = torch.full((B,), L, dtype=torch.int32, device="cuda")
+    ws = torch.zeros(_abi.tpl_workspace_bytes(1, B, L), dtype=torch.uint8, device="cuda")
+    _abi.tpl_fullatom_forward(tables.handle, ang, rt.cuda(), ln, coords, ws)
+    with pytest.raises(TplError) as e:
+        _abi.tpl_sync_status(ws)
+    assert e.value.status == 6 and "atom_stride" in str(e.value)
+    assert torch.isnan(guard[B]).all()  # nothing written past the last row
+    assert torch.isfinite(coords[0, : int(apc[0])]).all()
+    gang = torch.zeros(B, L, 8, device="cuda")
+    _abi.tpl_fullatom_backward_from_coords(tables.handle, coords, rt.cuda(), ln, torch.zeros_like(coords), gang, ws)
+    with pytest.raises(TplError):
+        _abi.tpl_sync_status(ws)
