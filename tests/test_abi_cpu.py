@@ -78,6 +78,15 @@ def test_null_and_shape_rejected_before_launch(abi):
     assert L.tpl_backbone_forward(q, p, 1, 4, p, p, 4096, None) == 3
     # full atom: NULL tables
     assert L.tpl_fullatom_forward(None, p, p, p, 1, 4, 16, p, p, 4096, None) == 1
+    # f1 fused, f2 precise, f3 paper design, f4 segments: host checks before any launch
+    assert L.tpl_backbone_lrmsd_forward(p, p, 1, 4, None, p, p, p, p, 4096, None) == 1
+    assert L.tpl_backbone_lrmsd_backward(p, p, 0, 4, p, p, p, p, p, 4096, None) == 2
+    assert L.tpl_backbone_forward_precise(p, p, 1, 4, None, p, 4096, None) == 1
+    assert L.tpl_paper_backbone_forward(p, p, 1, 4, p, None, p, 4096, None) == 1
+    assert L.tpl_paper_backbone_saved_floats(2, 5) == 2 * 15 * 16 and L.tpl_paper_backbone_saved_floats(0, 5) == 0
+    assert L.tpl_backbone_segment_place(p, p, 1, 4, p, 2, 2, p, 4096, None) == 2  # seg outside [0, n_seg)
+    assert L.tpl_backbone_segment_backward(p, p, 1, 4, p, p, 0, 0, p, p, 4096, None) == 2
+    assert L.tpl_backbone_segment_totals(p, p, 1, 4, None, p, p, 4096, None) == 1
 
 
 def test_table_validation_before_upload(abi, table):
