@@ -470,6 +470,11 @@ def run_ours(args):
             break
     clocks = sampler.stop()
     ms_step = statistics.median(t_step) / K
+    if len(t_step) > 1:  # 95% CI of the mean step time over the timed regions (P:248 reports CIs)
+        mean, sd = statistics.mean(t_step) / K, statistics.stdev(t_step) / K
+        ci95 = [mean - 1.96 * sd / math.sqrt(len(t_step)), mean + 1.96 * sd / math.sqrt(len(t_step))]
+    else:
+        ci95 = None
     ms_fwd = statistics.median(t_fwd) / K
     ms_bwd = statistics.median(t_bwd) / K
     for s in sets[:1]:
@@ -571,7 +576,8 @@ def run_ours(args):
                      "timing": f"CUDA graphs of K steps, median of {len(t_step)} timed regions"})
         out = {"metric": f"residues/sec fwd+bwd ({work.model}, L={work.Lmax}, batch {work.B})",
                "value": value, "unit": "residues/s", "n_gpus": world, "steps": K, "warmup": W,
-               "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+               "ms_per_step": ms_step, "ms_per_step_ci95": ci95, "higher_is_better": True,
+               "scaling": args.scaling, "vs_baseline": None,
                "dtype": "f32", "data": "synthetic (seeded uniform angles, N(0,1) dL/dr)", "config": cfgd,
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": work.launches_per_step * K,
                "impl": "paper_gpu_design" if args.impl == "paper" else "ours"}
@@ -618,8 +624,18 @@ def cpu_baseline(work, seconds):
     dt = time.perf_counter() - t0
     res = float(ln[idx].sum()) * reps
     what = f"{n} of {B} chains" if n < B else f"the whole {B}-chain batch x {reps}"
+    # the 1-thread rate on a short sample: chains in order until ~2 s
+    oracle.set_num_threads(1)
+    t0, res1, i = time.perf_counter(), 0.0, 0
+    while time.perf_counter() - t0 < 2.0 and i < 4 * B:
+        run(np.array([i % B]))
+        res1 += float(ln[i % B])
+        i += 1
+    one = res1 / (time.perf_counter() - t0)
+    oracle.set_num_threads(threads)
     return {"value": res / dt, "unit": "residues/s", "cores": threads, "kind": "oracle",
-            "sample": f"{what} (fwd + O(L^2) Eq. 2/Eq. 1 bwd, fp64), {dt:.1f} s", "host_cpus": os.cpu_count()}
+            "sample": f"{what} (fwd + O(L^2) Eq. 2/Eq. 1 bwd, fp64), {dt:.1f} s", "host_cpus": os.cpu_count(),
+            "single_thread_value": one, "single_thread_sample": f"{i} chains, 1 thread"}
 
 
 def ref_config(work, cfg, n):

@@ -72,6 +72,8 @@ def lib():
         L.tplref_bond_transform.argtypes = [ctypes.c_double] * 3 + [dp]
         L.tplref_bond_transform_dalpha.argtypes = [ctypes.c_double] * 3 + [dp]
         L.tplref_num_threads.restype = ctypes.c_int
+        L.tplref_set_num_threads.restype = None
+        L.tplref_set_num_threads.argtypes = [ctypes.c_int]
         L.tplref_backbone_forward.argtypes = [dp, ip, i32, i32, dp]
         L.tplref_backbone_backward.argtypes = [dp, ip, i32, i32, dp, dp]
         rp = ctypes.POINTER(RestypeC)
@@ -100,6 +102,10 @@ def _check(rc, what):
 
 def num_threads():
     return int(lib().tplref_num_threads())
+
+
+def set_num_threads(n):
+    lib().tplref_set_num_threads(int(n))
 
 
 def bond_transform(alpha, theta, d):

@@ -98,6 +98,15 @@ int tplref_num_threads(void) {
 #endif
 }
 
+/* Threads of the OpenMP loops over chains (timing the 1-thread rate). */
+void tplref_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 /* ======================================================================= *
  * Backbone model, PAPER §3                                                *
  * ======================================================================= */

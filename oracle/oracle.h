@@ -55,6 +55,7 @@ void tplref_bond_transform(double alpha, double theta, double d, double out[16])
 void tplref_bond_transform_dalpha(double alpha, double theta, double d, double out[16]);
 
 int tplref_num_threads(void);
+void tplref_set_num_threads(int n);
 
 /* Backbone (PAPER §3).  angles [B][Lmax][3] = (phi, psi, omega) per residue,
  * coords [B][3*Lmax][3] (atoms N, CA, C per residue), grad_coords likewise,
