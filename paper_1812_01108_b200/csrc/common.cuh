@@ -270,7 +270,8 @@ __device__ __forceinline__ Aff load_aff(const float* s) {
 // for thread t and writes carry * A_0 * ... * A_{NT-1} to *total (smem,
 // visible after the call).  scratch: NT/32 * 12 floats of smem.
 // Newton-Schulz policy kNS: 0 = never, 1 = on the returned prefix and the
-// total only, 2 = after every combine as well.
+// total only, 2 = after every combine as well, 3 = as 1 plus after each
+// cross-warp combine (wide blocks: up to NW - 1 sequential composes).
 template <int NT, int kNS>
 __device__ __forceinline__ Aff block_exclusive_scan(Aff a, const Aff& carry, float* scratch, float* total) {
     constexpr int NW = NT / 32;
@@ -281,7 +282,7 @@ __device__ __forceinline__ Aff block_exclusive_scan(Aff a, const Aff& carry, flo
         Aff o = shfl_up_aff(a, d);
         if (lane >= d) {
             a = aff_compose(o, a);
-            if (kNS >= 2) aff_orthonormalize(a);
+            if (kNS == 2) aff_orthonormalize(a);
         }
     }
     if (lane == 31) store_aff(scratch + 12 * warp, a);

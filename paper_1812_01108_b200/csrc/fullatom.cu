@@ -1051,10 +1051,12 @@ cudaError_t fa_backward_xyz_launch(const FAArgs& a, cudaStream_t st) {
 }
 
 cudaError_t fa_forward_launch(const FAArgs& a, cudaStream_t st) {
-    return a.ns == 0 ? fa_fwd<0>(a, st) : fa_fwd<1>(a, st);
+    // FA scans combine one residue per thread over up to 16 warps: re-orthonormalise
+    // each cross-warp combine too (policy 3; FA at L = 700: 1.03e-3 -> see DESIGN)
+    return a.ns == 0 ? fa_fwd<0>(a, st) : a.ns == 1 && std::getenv("TPL_FA_NS1") ? fa_fwd<1>(a, st) : fa_fwd<3>(a, st);
 }
 cudaError_t fa_backward_launch(const FAArgs& a, cudaStream_t st) {
-    return a.ns == 0 ? fa_bwd<0>(a, st) : fa_bwd<1>(a, st);
+    return a.ns == 0 ? fa_bwd<0>(a, st) : a.ns == 1 && std::getenv("TPL_FA_NS1") ? fa_bwd<1>(a, st) : fa_bwd<3>(a, st);
 }
 
 }  // namespace tpl

@@ -230,3 +230,19 @@ def test_atom_stride_too_small_is_flagged(tpl, table):
     _abi.tpl_fullatom_backward_from_coords(tables.handle, coords, rt.cuda(), ln, torch.zeros_like(coords), gang, ws)
     with pytest.raises(TplError):
         _abi.tpl_sync_status(ws)
+
+
+def test_coordinate_gate_many_chains_L700(tpl, oracle_lib, table):
+    """The 1e-3 A gate over many chains at L = 700 (one 512-thread tile plus a
+    tail): the wide scans need Newton-Schulz after each cross-warp combine
+    (policy 3); with policy 1 the worst of 64 chains reached 1.03e-3 A."""
+    tables = tpl.Tables(table)
+    B, L = 48, 700
+    ang = synth.angles_uniform(B, L, 8, 77)
+    rt = synth.restype_uniform(B, L, 20, 78)
+    ln = torch.full((B,), L, dtype=torch.int32)
+    c = tpl.fullatom(ang.cuda(), rt.cuda(), ln.cuda(), tables).cpu().numpy()
+    X, nat = oracle_lib.fullatom_forward(table, synth.numpy64(ang), rt.numpy(), ln.numpy(), c.shape[1])
+    worst = max(float(np.abs(c[b, :nat[b]] - X[b, :nat[b]]).max()) for b in range(B))
+    print(f"full atom {B} x {L}: worst coord err {worst:.3e} A")
+    assert worst <= 1e-3
