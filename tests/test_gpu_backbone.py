@@ -335,3 +335,21 @@ def test_decoupled_more_items_than_resident_ctas(tpl, oracle_lib):
     lnn = ln.numpy()
     sample = sorted({int(np.argmax(lnn)), int(np.argmin(lnn)), 7, 150})
     _check(oracle_lib, ang, ln, grad, coords, gang, chains=sample, coord_tol=2e-3)
+
+
+def test_coordinate_gate_L1000_many_chains(tpl, oracle_lib):
+    """The 1e-3 A gate at its longest stated length (L = 1000, two forward tiles),
+    over every chain of a 128-chain batch."""
+    from paper_1812_01108_b200 import _abi
+
+    B, L = 128, 1000
+    ang = synth.angles_uniform(B, L, 3, 9901)
+    ln = torch.full((B,), L, dtype=torch.int32)
+    coords = torch.empty(B, 3 * L, 3, device="cuda")
+    ws = torch.zeros(_abi.tpl_workspace_bytes(0, B, L), dtype=torch.uint8, device="cuda")
+    _abi.tpl_backbone_forward(ang.cuda(), ln.cuda(), coords, ws)
+    _abi.tpl_sync_status(ws)
+    X = oracle_lib.backbone_forward(synth.numpy64(ang), ln.numpy())
+    worst = float(np.abs(coords.cpu().numpy() - X).max())
+    print(f"backbone {B} x {L}: worst coord err {worst:.3e} A")
+    assert worst <= 1e-3
