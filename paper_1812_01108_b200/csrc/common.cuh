@@ -271,7 +271,7 @@ __device__ __forceinline__ Aff load_aff(const float* s) {
 // visible after the call).  scratch: NT/32 * 12 floats of smem.
 // Newton-Schulz policy kNS: 0 = never, 1 = on the returned prefix and the
 // total only, 2 = after every combine as well, 3 = as 1 plus after each
-// cross-warp combine (wide blocks: up to NW - 1 sequential composes).
+// cross-warp combine.  scratch: NW * 12 floats (NW <= 4) or 2 * NW * 12.
 template <int NT, int kNS>
 __device__ __forceinline__ Aff block_exclusive_scan(Aff a, const Aff& carry, float* scratch, float* total) {
     constexpr int NW = NT / 32;
@@ -289,13 +289,38 @@ __device__ __forceinline__ Aff block_exclusive_scan(Aff a, const Aff& carry, flo
     Aff ex = shfl_up_aff(a, 1);
     if (lane == 0) ex = aff_identity();
     __syncthreads();
-    // prefix over the warp totals of warps < warp, starting at the carry
-    Aff p = carry;
+    Aff p;
+    if (NW > 4) {
+        // wide blocks: warp 0 scans the NW warp totals in log2(NW) steps (instead of
+        // up to NW - 1 sequential composes) and leaves each warp's prefix, carry
+        // included, in scratch[NW + w]; needs 2 * NW * 12 floats of scratch
+        if (warp == 0) {
+            Aff t = lane < NW ? load_aff(scratch + 12 * lane) : aff_identity();
 #pragma unroll
-    for (int w = 0; w < NW - 1; ++w) {
-        if (w < warp) {
-            p = aff_compose(p, load_aff(scratch + 12 * w));
-            if (kNS >= 2) aff_orthonormalize(p);
+            for (int d = 1; d < NW; d <<= 1) {
+                const Aff o = shfl_up_aff(t, d);
+                if (lane >= d) {
+                    t = aff_compose(o, t);
+                    if (kNS >= 2) aff_orthonormalize(t);
+                }
+            }
+            Aff e = shfl_up_aff(t, 1);
+            if (lane == 0) e = aff_identity();
+            Aff pw = aff_compose(carry, e);
+            if (kNS >= 2) aff_orthonormalize(pw);
+            if (lane < NW) store_aff(scratch + 12 * (NW + lane), pw);
+        }
+        __syncthreads();
+        p = load_aff(scratch + 12 * (NW + warp));
+    } else {
+        // prefix over the warp totals of warps < warp, starting at the carry
+        p = carry;
+#pragma unroll
+        for (int w = 0; w < NW - 1; ++w) {
+            if (w < warp) {
+                p = aff_compose(p, load_aff(scratch + 12 * w));
+                if (kNS >= 2) aff_orthonormalize(p);
+            }
         }
     }
     Aff res = aff_compose(p, ex);

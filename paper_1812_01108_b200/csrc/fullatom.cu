@@ -35,8 +35,8 @@ template <int NT>
 struct FASmem {
     static constexpr int NW = NT / 32;
     static constexpr int kBar = 0;
-    static constexpr int kScan = 16;                         // NW*12 floats
-    static constexpr int kSuf = kScan + NW * 12 * 4;         // NW*6 floats
+    static constexpr int kScan = 16;                         // 2*NW*12 floats
+    static constexpr int kSuf = kScan + 2 * NW * 12 * 4;     // NW*6 floats
     static constexpr int kInt = kSuf + NW * 6 * 4;           // NW ints
     static constexpr int kTotal = r16(kInt + NW * 4);        // 12 floats
     static constexpr int kMisc = kTotal + 48;                // 16 floats / ints
