@@ -17,7 +17,7 @@
  *             copies but is not required.
  * Padding     Entries of a chain past lengths[b] are neither read nor written.
  * Errors      Host-detectable problems (NULL, B < 1, Lmax < 1, workspace too
- *             small, atom_stride too small, bad table) return a status BEFORE
+ *             small, atom_stride < 1, bad table) return a status BEFORE
  *             any launch and set tpl_last_error().  Device-detectable
  *             problems (lengths[b] outside [1, Lmax], a restype >= n_types,
  *             a chain with more atoms than atom_stride) set a flag in the
@@ -28,6 +28,12 @@
  * Workspace   Device buffer of tpl_workspace_bytes(model, B, Lmax) bytes,
  *             ZERO-INITIALISED before first use; reusable across calls on
  *             the same stream; one workspace per concurrently used stream.
+ *             It holds the error word, a launch epoch and per-(chain, tile)
+ *             carry slots: for few long chains the backbone kernels split a
+ *             chain over co-resident CTAs that exchange their carries there
+ *             (waiting only on earlier work items, so they always finish,
+ *             given the grid's CTAs are not starved by a never-ending
+ *             concurrent kernel).
  * Determinism Bitwise identical results for identical inputs on one build
  *             and device: no float atomics, fixed association order.
  * Precision   fp32 arithmetic with FMA contraction, accurate sincosf (no
@@ -92,7 +98,7 @@ TPL_API const char* tpl_last_error(void);
 TPL_API int tpl_abi_version(void);
 
 /* Device workspace bytes needed by any fwd/bwd call of `model` with these
- * B and Lmax (error word + per-tile prefix carries of long chains). */
+ * B and Lmax (header words + per-(chain, tile) carry slots). */
 TPL_API size_t tpl_workspace_bytes(int32_t model, int32_t B, int32_t Lmax);
 
 /* Synchronise `stream`, then read and clear the device error flags of
