@@ -1,11 +1,16 @@
-"""User-facing API: differentiable backbone / full-atom layers (§2, §3).
+"""User-facing API: differentiable backbone / full-atom layers (§2, §3)
+and the LRMSD loss (§4).
 
-    coords = backbone(angles, lengths)                      # [B, 3*Lmax, 3]
-    tables = Tables.from_json(synth.load_residue_table())   # or Tables(dict)
-    coords = fullatom(angles, restype, lengths, tables)     # [B, atom_stride, 3]
+    coords = backbone(angles, lengths)                  # [B, 3*Lmax, 3]
+    tables = Tables(synth.load_residue_table())         # 20 residue types
+    coords = fullatom(angles, restype, lengths, tables) # [B, atom_stride, 3]
+    loss = lrmsd(coords, target)                        # [B]
+    loss, coords = backbone_lrmsd(angles, target)       # fused forward + LRMSD (f1)
 
-Both are ``torch.autograd.Function``s running on the current CUDA stream;
-backward recomputes from the angles (nothing but the inputs is saved).
+All are ``torch.autograd.Function``s running on the current CUDA stream.  The
+layers save their output coordinates and back-propagate from them (the rotation
+axes are bond vectors); a table without origin atoms falls back to recomputing
+from the angles.  Argument marshalling only: every step runs in libtpl.so.
 """
 import ctypes
 
