@@ -26,6 +26,9 @@
 //             carried); from coordinates, tiles last to first only.
 // Few long chains (f4): the *_dl_kernel variants put the tiles of a chain on
 // different CTAs that exchange their aggregates through workspace slots.
+// Fewer chains than about 1.4 x SMs of 641-1536 residues: the *_cl_kernel
+// variants split each chain over a 2-CTA thread-block cluster that exchanges the
+// part aggregates through distributed shared memory.
 // Variants of the chain-serial kernels: chain segments over ranks (f4,
 // segment.cu) and the fused LRMSD loss (f1, kLoss).
 #include <cstdio>
@@ -384,6 +387,137 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
     // dependent's griddepcontrol.wait) covers visibility of the global writes.
     if (tid == 0) bulk_wait_read_all();
     TPL_STAMP(9);
+}
+
+// Cluster-split forward: one cluster of CL CTAs per chain, CTA rank c takes
+// the residues [c h, (c + 1) h) with h = ceil(L / CL).  Every CTA scans its
+// part from the identity; its aggregate A_c goes to the shared memory of each
+// later CTA of the cluster (st.shared::cluster + a remote mbarrier arrival),
+// and CTA r places its part with C_r = N(..N(A_0 A_1)..A_{r-1}) composed in
+// rank order (deterministic).  Halves (CL = 2) the serial pass-1 chain of a
+// chain-per-CTA launch when chains are about as many as SMs.  Chains up to
+// CL * NT * RPT residues.
+template <int NT, int RPT, int CL, int kNS>
+__global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_cl_kernel(const float* __restrict__ angles,
+                                                           const int* __restrict__ lengths, int B, int Lmax,
+                                                           float* __restrict__ coords, unsigned* __restrict__ err) {
+    constexpr int TILE = NT * RPT;
+    constexpr int ANG = round16(16 + 12 * (TILE + 1));
+    constexpr int SLOTS = round16(48 * CL);
+    using S = BBSmem<NT>;
+    extern __shared__ __align__(16) char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);  // [0] angles TMA, [1] carries
+    float* scratch = reinterpret_cast<float*>(smem + S::kScratch);
+    float* s_total = reinterpret_cast<float*>(smem + S::kTotal);
+    float* s_slots = reinterpret_cast<float*>(smem + S::kData);  // A_c of earlier ranks c
+    char* s_ang_base = smem + S::kData + SLOTS;
+    char* s_out_base = s_ang_base + ANG;
+
+    const int tid = threadIdx.x;
+    const unsigned rank = cluster_ctarank();
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, rank > 0 ? rank : 1);
+        fence_mbarrier_init_cluster();
+    }
+    __syncthreads();
+    cluster_arrive_relaxed();  // the carry barriers are initialised
+    pdl_wait();
+    const int b = blockIdx.x / CL;
+    const int L = b < B ? __ldg(lengths + b) : 0;
+    if (L < 1 || L > Lmax) {
+        if (tid == 0 && rank == 0 && b < B) atomicOr(err, ERR_LENGTH);
+        return;
+    }
+    const int h = (L + CL - 1) / CL, r0 = int(rank) * h, n = min(h, L - r0);
+    if (n <= 0) return;  // no earlier CTA sends to an empty part
+    const int pre = r0 > 0 ? 1 : 0;
+    const Span sa = make_span(angles + ((size_t)b * Lmax + r0 - pre) * 3, (n + pre) * 12);
+    if (tid == 0) {
+        mbar_arrive_expect_tx(bar, unsigned(sa.mid));
+        span_load_bulk(sa, s_ang_base, bar);
+    }
+    span_load_edges_f32(sa, s_ang_base);
+    const Span so = make_span(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3, n * 36);
+    float* s_out = reinterpret_cast<float*>(s_out_base + so.mis());
+    mbar_wait(bar, 0);
+    __syncthreads();
+    // every CTA of the cluster has initialised its carry barrier (they arrived
+    // right after the init, so this wait is short).  All threads, warp-aligned:
+    // a lone thread's non-aligned barrier.cluster.wait in a divergent branch hung.
+    cluster_wait_aligned();
+    const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 3 * pre;
+
+    // ---- pass 1 (as bb_forward_kernel)
+    const int rl0 = tid * RPT;
+    Aff M;
+    const int nq = max(0, min(RPT, n - rl0));
+    float px[3 * RPT], py[3 * RPT], pz[3 * RPT];
+    float maxabs = 0.f;
+    auto pass1 = [&](auto slow) {
+        constexpr bool kSlow = decltype(slow)::value;
+        M = aff_identity();
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            if (q < nq) {
+                const int rl = rl0 + q;
+                float c[3], s[3];
+                bb_residue_trig<kSlow>(s_ang, rl, r0 + rl, c, s, &maxabs);
+                if (r0 + rl > 0) aff_bond_bb<0>(M, c[0], s[0]);
+                px[3 * q] = M.t0; py[3 * q] = M.t1; pz[3 * q] = M.t2;
+                aff_bond_bb<1>(M, c[1], s[1]);
+                px[3 * q + 1] = M.t0; py[3 * q + 1] = M.t1; pz[3 * q + 1] = M.t2;
+                aff_bond_bb<2>(M, c[2], s[2]);
+                px[3 * q + 2] = M.t0; py[3 * q + 2] = M.t1; pz[3 * q + 2] = M.t2;
+            }
+        }
+    };
+    pass1(std::false_type{});
+    if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
+    if (kNS >= 1) aff_orthonormalize(M);
+    Aff P = block_exclusive_scan<NT, kNS>(M, aff_identity(), scratch, s_total);  // part-local prefix
+    // ---- exchange: A_rank to every later non-empty part of the chain
+    if (tid == 0 && r0 + n < L) {
+        const float* A = s_total;
+        for (int r = int(rank) + 1; r < CL && r * h < L; ++r) {
+            const uint32_t dst = mapa_shared(smem_u32(s_slots + 12 * rank), unsigned(r));
+            st_cluster_v4(dst, A[0], A[1], A[2], A[3]);
+            st_cluster_v4(dst + 16, A[4], A[5], A[6], A[7]);
+            st_cluster_v4(dst + 32, A[8], A[9], A[10], A[11]);
+            mbar_arrive_remote(mapa_shared(smem_u32(bar + 1), unsigned(r)));
+        }
+    }
+    if (rank > 0) {
+        mbar_wait_cluster(bar + 1, 0);
+        Aff C = load_aff(s_slots);
+        for (int c = 1; c < int(rank); ++c) {
+            C = aff_compose(C, load_aff(s_slots + 12 * c));
+            if (kNS >= 1) aff_orthonormalize(C);
+        }
+        P = aff_compose(C, P);
+        if (kNS >= 1) aff_orthonormalize(P);
+    }
+    pdl_trigger();
+    // ---- pass 2
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        if (q < nq) {
+            float* o = s_out + 9 * (rl0 + q);
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk) {
+                const int a = 3 * q + kk;
+                apply(P, px[a], py[a], pz[a], o[3 * kk], o[3 * kk + 1], o[3 * kk + 2]);
+            }
+        }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+        span_store_bulk(so, s_out_base);
+        bulk_commit();
+    }
+    span_store_edges_f32(so, s_out_base);
+    if (tid == 0) bulk_wait_read_all();
 }
 
 // Decoupled forward: each (chain, tile) item scans its tile from the identity,
@@ -991,6 +1125,175 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
     TPL_STAMP(10);
 }
 
+// Cluster-split coordinate backward: one cluster of CL CTAs per chain, parts as
+// bb_forward_cl_kernel.  Each CTA reduces its part's (S, T) about its first atom
+// c_r and sends (S, T, c_r) to the shared memory of every earlier CTA; CTA r adds
+// the later parts' totals (fixed order, moved to the next part's first atom N)
+// to its suffix sums, which also closes omega of its last residue (the same
+// algebra as the f4 segment carry).  Chains up to CL * NT * RPT residues.
+template <int NT, int RPT, int CL>
+__global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_cl_kernel(
+    const float* __restrict__ coords, const int* __restrict__ lengths, int B, int Lmax,
+    const float* __restrict__ grad_coords, float* __restrict__ grad_angles, unsigned* __restrict__ err) {
+    constexpr int TILE = NT * RPT;
+    constexpr int XB = round16(16 + 36 * TILE + 12);  // the previous atom and the part's atoms
+    constexpr int GB = round16(16 + 36 * TILE);
+    constexpr int SLOTS = round16(48 * CL);
+    using S = BBSmem<NT>;
+    extern __shared__ __align__(16) char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);  // [0] TMA, [1] later parts' totals
+    float* s_suf = reinterpret_cast<float*>(smem + S::kSuf);
+    float* s_slots = reinterpret_cast<float*>(smem + S::kData);  // (S, T, c) of later ranks
+    char* s_x_base = smem + S::kData + SLOTS;
+    char* s_g_base = s_x_base + XB;
+    char* s_go_base = s_g_base + GB;
+
+    const int tid = threadIdx.x;
+    const unsigned rank = cluster_ctarank();
+    pdl_wait();
+    const int b = blockIdx.x / CL;
+    const int L = b < B ? __ldg(lengths + b) : 0;
+    const bool ok = L >= 1 && L <= Lmax;
+    const int h = ok ? (L + CL - 1) / CL : 1, r0 = int(rank) * h, n = ok ? min(h, L - r0) : 0;
+    int nlater = 0;  // later non-empty parts: the arrivals this CTA waits for
+    for (int r = int(rank) + 1; r < CL; ++r) nlater += (ok && r * h < L) ? 1 : 0;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, nlater > 0 ? nlater : 1);
+        fence_mbarrier_init_cluster();
+        fence_barrier_init();
+    }
+    __syncthreads();
+    cluster_arrive_relaxed();
+    if (!ok) {
+        if (tid == 0 && rank == 0 && b < B) atomicOr(err, ERR_LENGTH);
+        return;
+    }
+    if (n <= 0) return;  // no CTA sends to (or waits for) an empty part
+    const int pre = r0 > 0 ? 1 : 0;
+    const size_t base = ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3;
+    const Span sx = make_span(coords + base - 3 * pre, (3 * n + pre) * 12);
+    const Span sg = make_span(grad_coords + base, n * 36);
+    if (tid == 0) {
+        mbar_arrive_expect_tx(bar, unsigned(sx.mid + sg.mid));
+        span_load_bulk(sx, s_x_base, bar);
+        span_load_bulk(sg, s_g_base, bar);
+    }
+    span_load_edges_f32(sx, s_x_base);
+    span_load_edges_f32(sg, s_g_base);
+    mbar_wait(bar, 0);
+    __syncthreads();
+    cluster_wait_aligned();  // every CTA's barriers are initialised (see bb_forward_cl_kernel)
+    const float* s_x = reinterpret_cast<const float*>(s_x_base + sx.mis()) + 3 * pre;  // atom 0 of the part
+    const float* s_g = reinterpret_cast<const float*>(s_g_base + sg.mis());
+    const float cx = s_x[0], cy = s_x[1], cz = s_x[2];
+    const int rl0 = tid * RPT;
+    const int nq = max(0, min(RPT, n - rl0));
+
+    // pass 1 (as bb_backward_xyz_kernel)
+    constexpr int APT = 3 * RPT;
+    float Px[APT], Py[APT], Pz[APT], Gx[APT], Gy[APT], Gz[APT], Ex[APT], Ey[APT], Ez[APT];
+    float sum6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < APT; ++a) {
+        Px[a] = Py[a] = Pz[a] = Gx[a] = Gy[a] = Gz[a] = Ex[a] = Ey[a] = Ez[a] = 0.f;
+        if (a / 3 < nq) {
+            const float* x = s_x + 9 * rl0 + 3 * a;
+            const float* g = s_g + 9 * rl0 + 3 * a;
+            const float x0 = x[0], x1 = x[1], x2 = x[2];
+            Px[a] = x0 - cx; Py[a] = x1 - cy; Pz[a] = x2 - cz;
+            Gx[a] = g[0]; Gy[a] = g[1]; Gz[a] = g[2];
+            if (r0 + rl0 + a / 3 > 0 || a % 3 > 0) {  // atom 0 of the chain carries no angle
+                const float ux = x0 - x[-3], uy = x1 - x[-2], uz = x2 - x[-1];
+                const float inv = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
+                Ex[a] = ux * inv; Ey[a] = uy * inv; Ez[a] = uz * inv;
+            }
+            sum6[0] += Gx[a]; sum6[1] += Gy[a]; sum6[2] += Gz[a];
+            sum6[3] += fmaf(Py[a], Gz[a], -Pz[a] * Gy[a]);
+            sum6[4] += fmaf(Pz[a], Gx[a], -Px[a] * Gz[a]);
+            sum6[5] += fmaf(Px[a], Gy[a], -Py[a] * Gx[a]);
+        }
+    }
+    const float zero6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float su[6], tot6[6];
+    block_exclusive_suffix6<NT>(sum6, zero6, s_suf, su, tot6);
+    // ---- exchange: this part's (S, T about c_r, c_r) to every earlier CTA
+    if (tid == 0) {
+        for (int r = 0; r < int(rank); ++r) {
+            const uint32_t dst = mapa_shared(smem_u32(s_slots + 12 * rank), unsigned(r));
+            st_cluster_v4(dst, tot6[0], tot6[1], tot6[2], tot6[3]);
+            st_cluster_v4(dst + 16, tot6[4], tot6[5], cx, cy);
+            st_cluster_v2(dst + 32, cz, 0.f);
+            mbar_arrive_remote(mapa_shared(smem_u32(bar + 1), unsigned(r)));
+        }
+    }
+    float ext[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, cnx = 0.f, cny = 0.f, cnz = 0.f;
+    if (nlater > 0) {  // later parts, last to first, about the next part's first atom N
+        mbar_wait_cluster(bar + 1, 0);
+        const float* n0 = s_slots + 12 * (rank + 1);
+        cnx = n0[6]; cny = n0[7]; cnz = n0[8];
+        for (int r = int(rank) + nlater; r > int(rank); --r) {
+            const float* tr = s_slots + 12 * r;
+            const float S0 = tr[0], S1 = tr[1], S2 = tr[2];
+            const float dx = tr[6] - cnx, dy = tr[7] - cny, dz = tr[8] - cnz;
+            ext[0] += S0; ext[1] += S1; ext[2] += S2;
+            ext[3] += tr[3] + fmaf(dy, S2, -dz * S1);
+            ext[4] += tr[4] + fmaf(dz, S0, -dx * S2);
+            ext[5] += tr[5] + fmaf(dx, S1, -dy * S0);
+        }
+        const float dx = cnx - cx, dy = cny - cy, dz = cnz - cz;  // to this part's reference
+        su[0] += ext[0]; su[1] += ext[1]; su[2] += ext[2];
+        su[3] += ext[3] + fmaf(dy, ext[2], -dz * ext[1]);
+        su[4] += ext[4] + fmaf(dz, ext[0], -dx * ext[2]);
+        su[5] += ext[5] + fmaf(dx, ext[1], -dy * ext[0]);
+    }
+    pdl_trigger();
+
+    // pass 2: atoms last to first
+    const Span so = make_span(grad_angles + ((size_t)b * Lmax + r0) * 3, n * 12);
+    float* s_go = reinterpret_cast<float*>(s_go_base + so.mis());
+#pragma unroll
+    for (int q = RPT - 1; q >= 0; --q) {
+        if (q < nq) {
+            const int rl = rl0 + q;
+            float ga[3];
+#pragma unroll
+            for (int kk = 2; kk >= 0; --kk) {
+                const int a = 3 * q + kk;
+                const float px = Px[a], py = Py[a], pz = Pz[a], gx = Gx[a], gy = Gy[a], gz = Gz[a];
+                const float c0 = su[3] - fmaf(py, su[2], -pz * su[1]);
+                const float c1 = su[4] - fmaf(pz, su[0], -px * su[2]);
+                const float c2 = su[5] - fmaf(px, su[1], -py * su[0]);
+                ga[kk] = fmaf(Ex[a], c0, fmaf(Ey[a], c1, Ez[a] * c2));
+                su[0] += gx; su[1] += gy; su[2] += gz;
+                su[3] += fmaf(py, gz, -pz * gy);
+                su[4] += fmaf(pz, gx, -px * gz);
+                su[5] += fmaf(px, gy, -py * gx);
+            }
+            s_go[3 * rl + 0] = ga[1];                      // phi_j
+            s_go[3 * rl + 1] = ga[2];                      // psi_j
+            if (rl > 0) s_go[3 * (rl - 1) + 2] = ga[0];  // omega_{j-1} (the previous part computes its own)
+        }
+    }
+    if (tid == 0) {  // omega of the part's last residue: e . T_N of the later parts (0 at the chain end)
+        float w = 0.f;
+        if (nlater > 0) {
+            const float* xc = s_x + 3 * (3 * n - 1);
+            const float ux = cnx - xc[0], uy = cny - xc[1], uz = cnz - xc[2];
+            w = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * fmaf(ux, ext[3], fmaf(uy, ext[4], uz * ext[5]));
+        }
+        s_go[3 * (n - 1) + 2] = w;
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+        span_store_bulk(so, s_go_base);
+        bulk_commit();
+    }
+    span_store_edges_f32(so, s_go_base);
+    if (tid == 0) bulk_wait_read_all();
+}
+
 // Decoupled coordinate backward: every (chain, tile) item sums its tile, publishes
 // (S_t, T_t about c_t, c_t) unless it is the chain's first tile, and adds the
 // later tiles' totals (fixed order, moved to its own reference) as its carry.
@@ -1188,6 +1491,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_dl_
 struct BBShape {
     int nt, rpt;
 };
+struct BBClShape {
+    int nt, rpt, cl;
+};
 static int bb_nt_env() {  // TPL_BB_NT=32|128|256 forces the block size (tuning); 0 = default
     static int v = -1;
     if (v < 0) {
@@ -1346,6 +1652,36 @@ static BBShape bbx_dl_shape(int B, int Lmax);
 template <int NT, int RPT>
 static cudaError_t launch_bwd_xyz_dl(const BBArgs& a, cudaStream_t st);
 
+// Cluster-split coordinate backward (TPL_BBXC=NTxRPTxCL forces a shape; "0" disables).
+template <int NT, int RPT, int CL>
+static cudaError_t launch_bwd_xyz_cl(const BBArgs& a, cudaStream_t st) {
+    auto k = bb_backward_xyz_cl_kernel<NT, RPT, CL>;
+    const int tile = NT * RPT;
+    const size_t sm = BBSmem<NT>::kData + round16(48 * CL) + round16(16 + 36 * tile + 12) + round16(16 + 36 * tile) +
+                      round16(16 + 12 * tile);
+    static LaunchCfg cfg;
+    cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
+    if (e != cudaSuccess) return e;
+    return launch_cluster(k, a.B * CL, CL, NT, sm, st, static_cast<const float*>(a.coords), a.lengths, a.B, a.Lmax,
+                          a.grad_coords, a.grad_angles, a.err);
+}
+static BBClShape bbxc_shape(int B, int Lmax) {
+    static const BBClShape env = [] {
+        BBClShape s{0, 0, 0};
+        const char* e = std::getenv("TPL_BBXC");
+        if (e && std::sscanf(e, "%dx%dx%d", &s.nt, &s.rpt, &s.cl) != 3) s = {-1, 0, 0};
+        return s;
+    }();
+    if (env.nt < 0) return {0, 0, 0};
+    if (env.nt > 0) return env.cl * env.nt * env.rpt >= Lmax ? env : BBClShape{0, 0, 0};
+    // measured (tools/gpu_clx_probe.sh): the backward has no trig in pass 1, so the
+    // split only pays where the chain-per-CTA kernel needs a second tile and the
+    // chains leave SMs idle -- 128 x 1000 8.1 -> 7.2 us; 64 x 700 (4.9 vs 5.5 us),
+    // 256 x 700 and 256 x 1000 stay chain-per-CTA
+    if (Lmax > 768 && Lmax <= 1536 && B <= sm_count()) return {256, 3, 2};
+    return {0, 0, 0};
+}
+
 cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
     if (a.loss_state) {  // f1 fused LRMSD: chain-serial shapes
         const BBShape l = bbx_shape(a.B, a.Lmax);
@@ -1362,6 +1698,13 @@ cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
         if (d.nt == 128 && d.rpt == 5) return launch_bwd_xyz_dl<128, 5>(a, st);
         if (d.nt == 256 && d.rpt == 3) return launch_bwd_xyz_dl<256, 3>(a, st);
         return cudaErrorInvalidConfiguration;
+    }
+    if (!a.seg_totals) {
+        const BBClShape c = bbxc_shape(a.B, a.Lmax);
+        if (c.nt == 128 && c.rpt == 3 && c.cl == 2) return launch_bwd_xyz_cl<128, 3, 2>(a, st);
+        if (c.nt == 128 && c.rpt == 5 && c.cl == 2) return launch_bwd_xyz_cl<128, 5, 2>(a, st);
+        if (c.nt == 256 && c.rpt == 3 && c.cl == 2) return launch_bwd_xyz_cl<256, 3, 2>(a, st);
+        if (c.nt > 0) return cudaErrorInvalidConfiguration;
     }
     // one 768-residue tile per chain and at most ~3 chains per SM: single-buffered
     // 256 x 3 (65 KB, 3 CTAs/SM) keeps every chain resident with 8 warps each
@@ -1477,10 +1820,55 @@ static cudaError_t dispatch_fwd_loss(const BBArgs& a, cudaStream_t st) {  // f1:
     return launch_fwd<128, 7, NS, true>(a, st);
 }
 
+// Cluster-split forward shapes (TPL_BBFC=NTxRPTxCL forces one; "0" disables).
+template <int NT, int RPT, int CL, int NS>
+static cudaError_t launch_fwd_cl(const BBArgs& a, cudaStream_t st) {
+    auto k = bb_forward_cl_kernel<NT, RPT, CL, NS>;
+    const size_t sm = BBSmem<NT>::kData + round16(48 * CL) + round16(16 + 12 * (NT * RPT + 1)) +
+                      round16(16 + 36 * NT * RPT);
+    static LaunchCfg cfg;
+    cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
+    if (e != cudaSuccess) return e;
+    return launch_cluster(k, a.B * CL, CL, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err);
+}
+static BBClShape bbfc_shape(int B, int Lmax) {
+    static const BBClShape env = [] {
+        BBClShape s{0, 0, 0};
+        const char* e = std::getenv("TPL_BBFC");
+        if (e && std::sscanf(e, "%dx%dx%d", &s.nt, &s.rpt, &s.cl) != 3) s = {-1, 0, 0};
+        return s;
+    }();
+    if (env.nt < 0) return {0, 0, 0};
+    if (env.nt > 0) return env.cl * env.nt * env.rpt >= Lmax ? env : BBClShape{0, 0, 0};
+    // measured (tools/gpu_cl_sweep.sh, fwd at 1 B200): the split pays where the
+    // chain-per-CTA forward needs 7 residues per thread or a second tile and the
+    // chains do not already fill the SMs twice -- 64 x 700 5.9 -> 5.0 us,
+    // 128 x 1000 10.4 -> 6.8 us, 256 x 900 10.0 -> 8.4 us; 256 x 700 (7.2 vs
+    // 7.4 us), 148 x 600 and 512 x 1000 stay chain-per-CTA
+    const int sms = sm_count();
+    if (Lmax > 640 && Lmax <= 768 && 10 * B <= 14 * sms) return {128, 3, 2};
+    if (Lmax > 768 && Lmax <= 1024 && (10 * B <= 14 * sms || (Lmax > 896 && B <= 2 * sms))) return {128, 5, 2};
+    return {0, 0, 0};
+}
+template <int NS>
+static cudaError_t dispatch_fwd_cl(const BBArgs& a, BBClShape s, cudaStream_t st) {
+#define TPL_BB_CL(NT_, R_, C_) \
+    if (s.nt == NT_ && s.rpt == R_ && s.cl == C_) return launch_fwd_cl<NT_, R_, C_, NS>(a, st);
+    TPL_BB_CL(128, 3, 2) TPL_BB_CL(128, 5, 2) TPL_BB_CL(128, 7, 2)
+#undef TPL_BB_CL
+    return cudaErrorInvalidConfiguration;
+}
+
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st) {
     if (a.loss_out) return a.ns == 0 ? dispatch_fwd_loss<0>(a, st) : dispatch_fwd_loss<1>(a, st);
+    if (a.ns == 2) return dispatch<true, 2>(a, st);  // TPL_ORTHO=2/3: chain-per-CTA shapes only
+    if (a.ns == 3) return dispatch<true, 3>(a, st);
     if (!a.seg_agg_out && dl_enabled(a.B, a.Lmax))
         return a.ns == 0 ? dispatch_fwd_dl<0>(a, st) : dispatch_fwd_dl<1>(a, st);
+    if (!a.seg_agg_out) {
+        const BBClShape cs = bbfc_shape(a.B, a.Lmax);
+        if (cs.nt > 0) return a.ns == 0 ? dispatch_fwd_cl<0>(a, cs, st) : dispatch_fwd_cl<1>(a, cs, st);
+    }
     return a.ns == 0 ? dispatch<true, 0>(a, st) : dispatch<true, 1>(a, st);
 }
 cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st) {

@@ -48,13 +48,16 @@ tpl_status cuda_fail(cudaError_t e, const char* where) {
 bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
 
 // Newton-Schulz re-orthonormalisation policy of the affine scan (TPL_ORTHO):
-// 0 = off, 1 = chunk aggregates, scan results and carries (default),
-// 2 = additionally after every combine inside the scan.
+// 0 = off, 1 = chunk aggregates, scan results and carries (backbone default),
+// 2 = additionally after every combine inside the scan, 3 = as 1 plus the warp
+// totals and every cross-warp combine (full-atom default).  Backbone forward at
+// L = 700 (tools/gpu_ortho.sh): helix / strand / extended 4.1e-3 / 6.5e-3 /
+// 1.9e-3 A under 1, 2.5e-4 / 4.9e-4 / 5.1e-4 A under 2, for +0.5 us (256 x 700).
 int ns_policy() {
     static int v = -1;
     if (v < 0) {
         const char* e = std::getenv("TPL_ORTHO");
-        v = (e && (e[0] == '0' || e[0] == '2')) ? e[0] - '0' : 1;
+        v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 1;
     }
     return v;
 }

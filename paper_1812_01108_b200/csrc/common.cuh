@@ -270,8 +270,8 @@ __device__ __forceinline__ Aff load_aff(const float* s) {
 // for thread t and writes carry * A_0 * ... * A_{NT-1} to *total (smem,
 // visible after the call).  scratch: NT/32 * 12 floats of smem.
 // Newton-Schulz policy kNS: 0 = never, 1 = on the returned prefix and the
-// total only, 2 = after every combine as well, 3 = as 1 plus after each
-// cross-warp combine.  scratch: NW * 12 floats (NW <= 4) or 2 * NW * 12.
+// total only, 2 = after every combine as well, 3 = as 1 plus on each warp
+// total and after each cross-warp combine.  scratch: NW * 12 floats (NW <= 4) or 2 * NW * 12.
 template <int NT, int kNS>
 __device__ __forceinline__ Aff block_exclusive_scan(Aff a, const Aff& carry, float* scratch, float* total) {
     constexpr int NW = NT / 32;
@@ -285,7 +285,15 @@ __device__ __forceinline__ Aff block_exclusive_scan(Aff a, const Aff& carry, flo
             if (kNS == 2) aff_orthonormalize(a);
         }
     }
-    if (lane == 31) store_aff(scratch + 12 * warp, a);
+    if (lane == 31) {
+        if (kNS == 3) {  // the warp totals feed the cross-warp combines: orthonormal first
+            Aff w = a;
+            aff_orthonormalize(w);
+            store_aff(scratch + 12 * warp, w);
+        } else {
+            store_aff(scratch + 12 * warp, a);
+        }
+    }
     Aff ex = shfl_up_aff(a, 1);
     if (lane == 0) ex = aff_identity();
     __syncthreads();
@@ -459,6 +467,48 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// Thread-block clusters (the cluster-split kernels): rank, the cluster barrier
+// (arrive by every thread; wait only where a remote access follows), and
+// remote shared-memory stores / mbarrier arrivals through mapa addresses.
+__device__ __forceinline__ unsigned cluster_ctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_aligned() {  // every thread of the CTA, converged
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbarrier_init_cluster() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, unsigned rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void st_cluster_v2(uint32_t addr, float a, float b) {
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "TPL_WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TPL_WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
 // Inter-CTA publication (decoupled tile carries): payload with plain stores,
 // then a release store of the flag; the reader acquires the flag and reads the
 // payload through L2 (.cg: L1 is not coherent across SMs).
@@ -548,6 +598,27 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, siz
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+// Cluster launch (cluster dimension cl along x), PDL attribute as launch_pdl.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_cluster(void (*kernel)(KArgs...), int grid, int cl, int block, size_t smem,
+                                  cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = unsigned(cl);
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 

@@ -121,6 +121,35 @@ def test_parity_ragged_tiles(tpl, oracle_lib, Lmax, lengths):
 
 
 @pytest.mark.parametrize("Lmax,lengths", [
+    (700, [700, 699, 641, 351, 350, 2, 1]),  # cluster split 128 x 3 x 2: odd halves, an empty second part
+    (1000, [1000, 999, 769, 513, 3, 1]),     # 128 x 5 x 2
+])
+def test_cluster_split_forward_parity(tpl, oracle_lib, Lmax, lengths):
+    """Forward with one 2-CTA cluster per chain (few chains of 641-1024 residues):
+    the second CTA's part is placed with the first's aggregate received through
+    distributed shared memory; at Lmax = 1000 the coordinate backward splits too
+    (later part's (S, T) sent to the earlier one).  Parity, untouched padding,
+    bitwise repeatability."""
+    B = len(lengths)
+    ang = synth.angles_uniform(B, Lmax, 3, 4242 + Lmax)
+    grad = synth.grad_normal((B, 3 * Lmax, 3), 4243 + Lmax)
+    ln = torch.tensor(lengths, dtype=torch.int32)
+    coords, gang = _run(tpl, ang, ln, grad)
+    _check(oracle_lib, ang, ln, grad, coords, gang)
+    for b, L in enumerate(lengths):
+        assert np.isnan(coords[b, 3 * L:]).all()
+    again, _ = _run(tpl, ang, ln, grad)
+    np.testing.assert_array_equal(coords, again)
+    # coordinate backward (cluster-split for Lmax in (768, 1536] and few chains)
+    cx, gx = _run(tpl, ang, ln, grad, xyz=True)
+    _check(oracle_lib, ang, ln, grad, cx, gx)
+    for b, L in enumerate(lengths):
+        assert np.isnan(gx[b, L:]).all()
+    _, gx2 = _run(tpl, ang, ln, grad, xyz=True)
+    np.testing.assert_array_equal(gx, gx2)
+
+
+@pytest.mark.parametrize("Lmax,lengths", [
     (16, [16, 1, 2, 3, 4, 7]),
     (300, [300, 1, 255, 256, 257, 299]),
     (700, [700, 650, 512, 3]),

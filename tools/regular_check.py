@@ -1,0 +1,40 @@
+#!/usr/bin/env python3
+"""Backbone forward error on regular structures (helix / strand / extended) at
+L = 700 and 1000 against the fp64 oracle: the worst case for fp32 drift, since
+every residue repeats the same rounding (DESIGN reading Q21).
+
+    TPL_ORTHO=2 python tools/regular_check.py
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402  (test infrastructure)
+import synth  # noqa: E402
+from paper_1812_01108_b200 import _abi  # noqa: E402
+
+
+def main():
+    torch.cuda.set_device(0)
+    oracle.build()
+    for L in (700, 1000):
+        for kind in ("helix", "strand", "extended"):
+            ang = synth.regular_angles(2, L, kind)
+            ln = torch.full((2,), L, dtype=torch.int32)
+            c = torch.empty(2, 3 * L, 3, device="cuda")
+            ws = torch.zeros(_abi.tpl_workspace_bytes(0, 2, L), dtype=torch.uint8, device="cuda")
+            _abi.tpl_backbone_forward(ang.cuda(), ln.cuda(), c, ws)
+            _abi.tpl_sync_status(ws)
+            X = oracle.backbone_forward(synth.numpy64(ang), ln.numpy())
+            err = float(np.abs(c.cpu().numpy() - X).max())
+            ext = float(np.linalg.norm(X, axis=2).max())
+            print(f"ORTHO={os.environ.get('TPL_ORTHO', '1')} L={L} {kind:9s} max err {err:.3e} A  extent {ext:.0f} A")
+
+
+if __name__ == "__main__":
+    main()
