@@ -26,7 +26,7 @@
 //             carried); from coordinates, tiles last to first only.
 // Few long chains (f4): the *_dl_kernel variants put the tiles of a chain on
 // different CTAs that exchange their aggregates through workspace slots.
-// Fewer chains than about 1.4 x SMs of 641-1536 residues: the *_cl_kernel
+// Fewer chains than about 1.4 x SMs of 641-1024 residues: the *_cl_kernel
 // variants split each chain over a 2-CTA thread-block cluster that exchanges the
 // part aggregates through distributed shared memory.
 // Variants of the chain-serial kernels: chain segments over ranks (f4,
