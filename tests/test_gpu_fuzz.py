@@ -89,11 +89,13 @@ def test_huge_angles_fullatom(abi, oracle_lib, table):
         assert np.abs(a.grad[b].cpu().numpy() - G[b]).max() / np.abs(G[b]).max() <= 1e-3
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(10))
 def test_random_shapes_backbone(abi, oracle_lib, seed):
+    """Lmax values straddle the launchers' switch points: tile sizes, the 2-CTA
+    cluster split (641-1024) and the decoupled kernels (> 1024 for few chains)."""
     rng = np.random.default_rng(9600 + seed)
     B = int(rng.integers(1, 24))
-    Lmax = int(rng.choice([1, 2, 7, 96, 129, 383, 385, 700, 769, 897, 1025, 1800, 2600]))
+    Lmax = int(rng.choice([1, 2, 7, 96, 129, 383, 385, 640, 641, 700, 768, 769, 897, 1024, 1025, 1800, 2600]))
     lengths = rng.integers(1, Lmax + 1, size=B)
     lengths[rng.integers(0, B)] = Lmax
     ang = synth.angles_uniform(B, Lmax, 3, 9700 + seed)
