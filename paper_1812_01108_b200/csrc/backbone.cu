@@ -242,25 +242,40 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
     }
     unsigned tphase = 0;
     pdl_wait();
+    // Speculative first load: when every chain fits one tile, the CTA's first
+    // chain is bulk-loaded whole (Lmax residues) before its length arrives, so
+    // the lengths load no longer precedes the TMA on the critical path.
+    const bool spec = !kLoss && Lmax <= TILE && int(blockIdx.x) < B;
+    if (tid == 0 && spec) {
+        const Span s0 = make_span(angles + (size_t)blockIdx.x * Lmax * 3, Lmax * 12);
+        mbar_arrive_expect_tx(bar, unsigned(s0.mid));
+        span_load_bulk(s0, s_ang_buf, bar);
+    }
     BBIter it{lengths, B, Lmax, TILE, int(gridDim.x), true, err, false};
     it.init();
     TPL_STAMP(1);
     __syncthreads();
-    if (tid == 0 && it.valid) bb_issue(it, angles, nullptr, s_ang_buf, nullptr, bar);
+    const bool spec_hit = spec && it.valid && it.b == int(blockIdx.x);
+    unsigned phases = 0;  // bit k = parity of buffer k
+    if (spec && !spec_hit) {  // first chain invalid: drain the speculative copy
+        if (tid == 0) mbar_wait(bar, 0);
+        phases ^= 1u;
+    }
+    if (tid == 0 && it.valid && !spec_hit) bb_issue(it, angles, nullptr, s_ang_buf, nullptr, bar);
 
     Aff carry = aff_identity();
-    unsigned phases = 0;  // bit k = parity of buffer k
     const int rl0 = tid * RPT;
     for (int k = 0; it.valid; ++k) {
         const int buf = k & 1;
         const int b = it.b, L = it.L, r0 = it.r0(), n = it.n(), pre = r0 > 0 ? 1 : 0;
+        const int nl = (k == 0 && spec_hit) ? Lmax : n;  // residues the copy covers
         if (r0 == 0) carry = aff_identity();
         BBIter nx = it;
         nx.advance();
         if (tid == 0 && nx.valid) bb_issue(nx, angles, nullptr, s_ang_buf + (buf ^ 1) * ANG, nullptr, bar + (buf ^ 1));
         // ---- angles [r0-pre, r0+n): bulk part by TMA, <16-byte edges by threads
         char* s_ang_base = s_ang_buf + buf * ANG;
-        const Span sa = make_span(angles + ((size_t)b * Lmax + r0 - pre) * 3, (n + pre) * 12);
+        const Span sa = make_span(angles + ((size_t)b * Lmax + r0 - pre) * 3, (nl + pre) * 12);
         span_load_edges_f32(sa, s_ang_base);
         const Span so = make_span(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3, n * 36);
         float* s_out = reinterpret_cast<float*>(s_out_base + so.mis());
@@ -945,6 +960,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
     if (tid == 0 && it.valid) bbx_issue(it, coords, grad_coords, s_x_buf, s_g_buf, bar);
 
     unsigned phases = 0;
+
     const int rl0 = tid * RPT;
     float carry6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // (S, T) of the later tiles, about c_prev
     float cpx = 0.f, cpy = 0.f, cpz = 0.f;              // reference point of the later tile
