@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
         pass1(std::false_type{});
         if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
         if (kNS >= 1) aff_orthonormalize(M);
-        if (tid == 0) bulk_wait_read_all();  // the output staging is free again
+        if ((tid & 31) == 0) bulk_wait_read_all();  // the output staging is free again (per-warp groups)
         TPL_STAMP(4);
         const Aff P = block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
         carry = load_aff(s_total);
@@ -350,13 +350,37 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
         }
         TPL_STAMP(6);
         fence_proxy_async_smem();
-        __syncthreads();
-        TPL_STAMP(7);
-        if (tid == 0) {
-            span_store_bulk(so, s_out_base);
-            bulk_commit();
+        if (kLoss) {
+            __syncthreads();
+            if (tid == 0) {
+                span_store_bulk(so, s_out_base);
+                bulk_commit();
+            }
+            span_store_edges_f32(so, s_out_base);
+        } else {
+            // per-warp stores: a warp's residues are contiguous, so each warp sends its
+            // own chunk as soon as its lanes are done (no block barrier); the chunk
+            // starts 36 * 32 * RPT bytes apart, so shared and global keep the same
+            // 16-byte phase
+            __syncwarp();
+            const int lane = tid & 31, w0 = (tid >> 5) * 32 * RPT, wn = min(32 * RPT, n - w0);
+            if (wn > 0) {
+                const Span sw = make_span(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)(r0 + w0)) * 3, wn * 36);
+                const float* src = s_out + 9 * w0;
+                if (lane == 0 && sw.mid > 0) {
+                    bulk_s2g(const_cast<char*>(sw.g) + sw.head, reinterpret_cast<const char*>(src) + sw.head,
+                             unsigned(sw.mid));
+                    bulk_commit();
+                }
+                float* g = reinterpret_cast<float*>(const_cast<char*>(sw.g));
+                const int nh = sw.head >> 2, ntl = sw.tail() >> 2, off_t = (sw.head + sw.mid) >> 2;
+                for (int e = lane; e < nh + ntl; e += 32) {
+                    const int idx = e < nh ? e : off_t + (e - nh);
+                    g[idx] = src[idx];
+                }
+            }
         }
-        span_store_edges_f32(so, s_out_base);
+        TPL_STAMP(7);
         if (kLoss) {  // moments of (x, y) over the tile's atoms, fp64
             mbar_wait(bar_t, tphase);
             tphase ^= 1u;
@@ -400,7 +424,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
     TPL_STAMP(8);
     // Only the shared-memory source must outlive the CTA; grid completion (and the
     // dependent's griddepcontrol.wait) covers visibility of the global writes.
-    if (tid == 0) bulk_wait_read_all();
+    if ((tid & 31) == 0) bulk_wait_read_all();
     TPL_STAMP(9);
 }
 
