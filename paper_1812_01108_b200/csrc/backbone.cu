@@ -314,11 +314,11 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(c
                     const int rl = rl0 + q;
                     float c[3], s[3];
                     bb_residue_trig<kSlow>(s_ang, rl, r0 + rl, c, s, &maxabs, om0);
-                    if (r0 + rl > 0 || seg0) aff_bond_bb<0>(M, c[0], s[0]);
+                    if (r0 + rl > 0 || seg0) aff_bond_bb_x2<0>(M, c[0], s[0]);
                     px[3 * q] = M.t0; py[3 * q] = M.t1; pz[3 * q] = M.t2;
-                    aff_bond_bb<1>(M, c[1], s[1]);
+                    aff_bond_bb_x2<1>(M, c[1], s[1]);
                     px[3 * q + 1] = M.t0; py[3 * q + 1] = M.t1; pz[3 * q + 1] = M.t2;
-                    aff_bond_bb<2>(M, c[2], s[2]);
+                    aff_bond_bb_x2<2>(M, c[2], s[2]);
                     px[3 * q + 2] = M.t0; py[3 * q + 2] = M.t1; pz[3 * q + 2] = M.t2;
                 }
             }
