@@ -62,21 +62,23 @@ __device__ __forceinline__ Aff aff_compose(const Aff& A, const Aff& B) {
 //   m0' = u,  m1' = ca m1 + sa w,  m2' = ca w - sa m1,  t' = t + d u
 // where m0, m1, m2 are the columns of M's rotation block.
 __device__ __forceinline__ void aff_bond(Aff& M, float ca, float sa, const BondC& b) {
-    float u0 = fmaf(b.ct, M.r00, -b.st * M.r02);
-    float u1 = fmaf(b.ct, M.r10, -b.st * M.r12);
-    float u2 = fmaf(b.ct, M.r20, -b.st * M.r22);
-    float w0 = fmaf(b.st, M.r00, b.ct * M.r02);
-    float w1 = fmaf(b.st, M.r10, b.ct * M.r12);
-    float w2 = fmaf(b.st, M.r20, b.ct * M.r22);
-    float n01 = fmaf(ca, M.r01, sa * w0), n02 = fmaf(ca, w0, -sa * M.r01);
-    float n11 = fmaf(ca, M.r11, sa * w1), n12 = fmaf(ca, w1, -sa * M.r11);
-    float n21 = fmaf(ca, M.r21, sa * w2), n22 = fmaf(ca, w2, -sa * M.r21);
-    M.t0 = fmaf(b.d, u0, M.t0);
-    M.t1 = fmaf(b.d, u1, M.t1);
+    // rows 0 and 1 packed (fma.rn.f32x2 / mul.rn.f32x2): per-element roundings as the scalar form
+    const float2 c2 = make_float2(b.ct, b.ct), s2 = make_float2(b.st, b.st), ms2 = make_float2(-b.st, -b.st);
+    const float2 ca2 = make_float2(ca, ca), sa2 = make_float2(sa, sa), msa2 = make_float2(-sa, -sa);
+    const float2 m0 = make_float2(M.r00, M.r10), m1 = make_float2(M.r01, M.r11), m2 = make_float2(M.r02, M.r12);
+    const float2 u = __ffma2_rn(c2, m0, __fmul2_rn(ms2, m2));
+    const float2 w = __ffma2_rn(s2, m0, __fmul2_rn(c2, m2));
+    const float2 n1 = __ffma2_rn(ca2, m1, __fmul2_rn(sa2, w));
+    const float2 n2 = __ffma2_rn(ca2, w, __fmul2_rn(msa2, m1));
+    const float2 t = __ffma2_rn(make_float2(b.d, b.d), u, make_float2(M.t0, M.t1));
+    const float u2 = fmaf(b.ct, M.r20, -b.st * M.r22);
+    const float w2 = fmaf(b.st, M.r20, b.ct * M.r22);
+    const float n21 = fmaf(ca, M.r21, sa * w2), n22 = fmaf(ca, w2, -sa * M.r21);
     M.t2 = fmaf(b.d, u2, M.t2);
-    M.r00 = u0; M.r10 = u1; M.r20 = u2;
-    M.r01 = n01; M.r11 = n11; M.r21 = n21;
-    M.r02 = n02; M.r12 = n12; M.r22 = n22;
+    M.t0 = t.x; M.t1 = t.y;
+    M.r00 = u.x; M.r10 = u.y; M.r20 = u2;
+    M.r01 = n1.x; M.r11 = n1.y; M.r21 = n21;
+    M.r02 = n2.x; M.r12 = n2.y; M.r22 = n22;
 }
 
 // aff_bond with the backbone constants of transform kind k as immediates.
