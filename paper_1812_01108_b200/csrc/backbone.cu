@@ -1587,17 +1587,19 @@ static int sm_count() { return device_sm_count(); }
 
 
 // Grid of the chain-serial kernels: the co-resident CTAs, each walking chains
-// b, b + grid, ...  TPL_GRID=<m> uses m x that (0: one CTA per chain, which lets
-// the block scheduler balance ragged batches: config 4 214 -> 187 us, but 4096 x
-// 700 108 -> 117 us; dynamic chain claiming through a workspace counter cost
-// more in atomics than it saved).
-static int chain_grid(int B, int cap) {
+// b, b + grid, ...; for rows longer than 1024 residues one CTA per chain, which
+// lets the block scheduler balance ragged batches (config 4, 4096 x U[50, 2000]:
+// 212 -> 185 us; uniform 1024-4096 x 1000-2000 within +-1.6%), while shorter
+// rows keep the persistent grid (one CTA per chain costs 4096 x 700 8%; dynamic
+// chain claiming through a workspace counter cost more in atomics than it saved).
+// TPL_GRID=<m> forces m x the co-resident grid (0: one CTA per chain).
+static int chain_grid(int B, int cap, int Lmax) {
     static const int mult = [] {
         const char* e = std::getenv("TPL_GRID");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : -1;
     }();
-    if (mult <= 0) return B;
-    const long g = long(mult) * cap;
+    if (mult == 0 || (mult < 0 && Lmax > 1024)) return B;
+    const long g = long(mult > 0 ? mult : 1) * cap;
     return B < g ? B : int(g);
 }
 
@@ -1609,7 +1611,7 @@ static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
     const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
-    const int grid = chain_grid(a.B, grid_cap);
+    const int grid = chain_grid(a.B, grid_cap, a.Lmax);
     return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err,
                       static_cast<const float*>(a.seg_omega_prev), a.seg_agg_out, a.loss_target, a.loss_out,
                       a.loss_state_out);
@@ -1622,7 +1624,7 @@ static cudaError_t launch_bwd(const BBArgs& a, cudaStream_t st) {
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
     const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
-    const int grid = chain_grid(a.B, grid_cap);
+    const int grid = chain_grid(a.B, grid_cap, a.Lmax);
     return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.grad_coords, a.grad_angles, a.err,
                       a.ws_prefix, a.max_tiles);
 }
@@ -1658,7 +1660,7 @@ static cudaError_t launch_bwd_xyz(const BBArgs& a, cudaStream_t st) {
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
     const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
-    const int grid = chain_grid(a.B, grid_cap);
+    const int grid = chain_grid(a.B, grid_cap, a.Lmax);
     return launch_pdl(k, grid, NT, sm, st, static_cast<const float*>(a.coords), a.lengths, a.B, a.Lmax,
                       LOSS ? a.loss_target : a.grad_coords, a.grad_angles, a.err, a.seg_totals, a.n_seg, a.seg,
                       a.loss_state, a.loss_grad);
