@@ -1750,8 +1750,12 @@ cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
     }
     // one 768-residue tile per chain and at most ~3 chains per SM: single-buffered
     // 256 x 3 (65 KB, 3 CTAs/SM) keeps every chain resident with 8 warps each
-    if (!std::getenv("TPL_BBX") && a.Lmax <= 768 && a.B <= 3 * sm_count())
-        return launch_bwd_xyz<256, 3, false, false>(a, st);
+    const bool env_shape = std::getenv("TPL_BBX") != nullptr;
+    if (!env_shape && a.Lmax <= 768 && a.B <= 3 * sm_count()) return launch_bwd_xyz<256, 3, false, false>(a, st);
+    // more chains than SMs: single-buffered 128 x 3 (twice the resident CTAs of the
+    // double-buffered shape; measured, tools/gpu_bbxs.sh: 4096 x 700 56.0 -> 50.9 us,
+    // 512 x 1000 18.2 -> 13.5 us, config 4 96.6 -> 86.2 us)
+    if (!env_shape && a.B > sm_count() && a.Lmax > 128) return launch_bwd_xyz<128, 3, false, false>(a, st);
     const BBShape s = bbx_shape(a.B, a.Lmax);
 #define TPL_BBX(NT_, R_) \
     if (s.nt == NT_ && s.rpt == R_) return launch_bwd_xyz<NT_, R_>(a, st);
