@@ -463,23 +463,42 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_cl_kerne
     cluster_arrive_relaxed();  // the carry barriers are initialised
     pdl_wait();
     const int b = blockIdx.x / CL;
+    // speculative part load assuming L = Lmax (uniform batches), issued before the
+    // length arrives; it is used whenever it covers the actual part
+    const int hs = (Lmax + CL - 1) / CL, r0s = int(rank) * hs, ns = min(hs, Lmax - r0s), pres = r0s > 0 ? 1 : 0;
+    const bool spec = ns > 0 && b < B;
+    const Span ss = make_span(angles + ((size_t)b * Lmax + r0s - pres) * 3, (ns + pres) * 12);
+    if (tid == 0 && spec) {
+        mbar_arrive_expect_tx(bar, unsigned(ss.mid));
+        span_load_bulk(ss, s_ang_base, bar);
+    }
     const int L = b < B ? __ldg(lengths + b) : 0;
     if (L < 1 || L > Lmax) {
         if (tid == 0 && rank == 0 && b < B) atomicOr(err, ERR_LENGTH);
+        if (tid == 0 && spec) mbar_wait(bar, 0);  // no bulk copy may outlive the CTA
         return;
     }
     const int h = (L + CL - 1) / CL, r0 = int(rank) * h, n = min(h, L - r0);
-    if (n <= 0) return;  // no earlier CTA sends to an empty part
+    if (n <= 0) {  // no earlier CTA sends to an empty part
+        if (tid == 0 && spec) mbar_wait(bar, 0);
+        return;
+    }
     const int pre = r0 > 0 ? 1 : 0;
-    const Span sa = make_span(angles + ((size_t)b * Lmax + r0 - pre) * 3, (n + pre) * 12);
-    if (tid == 0) {
-        mbar_arrive_expect_tx(bar, unsigned(sa.mid));
-        span_load_bulk(sa, s_ang_base, bar);
+    const bool hit = spec && r0 == r0s && n <= ns;
+    unsigned ph = 0;
+    const Span sa = hit ? ss : make_span(angles + ((size_t)b * Lmax + r0 - pre) * 3, (n + pre) * 12);
+    if (!hit) {
+        if (tid == 0) {
+            if (spec) mbar_wait(bar, 0);  // drain the speculative copy before refilling the buffer
+            mbar_arrive_expect_tx(bar, unsigned(sa.mid));
+            span_load_bulk(sa, s_ang_base, bar);
+        }
+        if (spec) ph = 1;
     }
     span_load_edges_f32(sa, s_ang_base);
     const Span so = make_span(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3, n * 36);
     float* s_out = reinterpret_cast<float*>(s_out_base + so.mis());
-    mbar_wait(bar, 0);
+    mbar_wait(bar, ph);
     __syncthreads();
     // every CTA of the cluster has initialised its carry barrier (they arrived
     // right after the init, so this wait is short).  All threads, warp-aligned:
@@ -550,13 +569,26 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_cl_kerne
         }
     }
     fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-        span_store_bulk(so, s_out_base);
-        bulk_commit();
+    __syncwarp();
+    {  // per-warp stores (as bb_forward_kernel)
+        const int lane = tid & 31, w0 = (tid >> 5) * 32 * RPT, wn = min(32 * RPT, n - w0);
+        if (wn > 0) {
+            const Span sw = make_span(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)(r0 + w0)) * 3, wn * 36);
+            const float* src = s_out + 9 * w0;
+            if (lane == 0 && sw.mid > 0) {
+                bulk_s2g(const_cast<char*>(sw.g) + sw.head, reinterpret_cast<const char*>(src) + sw.head,
+                         unsigned(sw.mid));
+                bulk_commit();
+            }
+            float* g = reinterpret_cast<float*>(const_cast<char*>(sw.g));
+            const int nh = sw.head >> 2, ntl = sw.tail() >> 2, off_t = (sw.head + sw.mid) >> 2;
+            for (int e = lane; e < nh + ntl; e += 32) {
+                const int idx = e < nh ? e : off_t + (e - nh);
+                g[idx] = src[idx];
+            }
+        }
+        if (lane == 0) bulk_wait_read_all();
     }
-    span_store_edges_f32(so, s_out_base);
-    if (tid == 0) bulk_wait_read_all();
 }
 
 // Decoupled forward: each (chain, tile) item scans its tile from the identity,
