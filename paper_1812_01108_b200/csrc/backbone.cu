@@ -208,8 +208,10 @@ __device__ __forceinline__ void bb_issue(const It& it, const float* angles, cons
 // chain's raw fp64 moments (sum x, sum y, sum x y^T, sum |x|^2, sum |y|^2; PAPER
 // §4 step 1) are reduced over its tiles, and at the chain's end thread
 // 0 solves steps 2-3 (lrmsd_math.cuh) into loss_out[b] and loss_state[b][16].
+// The kLoss variant is compiled for 2 CTAs/SM (up to 255 registers): capped at
+// 128 it spilled the 17 fp64 moment accumulators (fused step 25.0 -> 20.5 us).
 template <int NT, int RPT, int kNS, bool kLoss = false>
-__global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_kernel(const float* __restrict__ angles,
+__global__ void __launch_bounds__(NT, kLoss ? 2 : kMinBlocks128Regs(NT)) bb_forward_kernel(const float* __restrict__ angles,
                                                         const int* __restrict__ lengths, int B, int Lmax,
                                                         float* __restrict__ coords, unsigned* __restrict__ err,
                                                         const float* __restrict__ omega_prev,
