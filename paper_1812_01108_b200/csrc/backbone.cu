@@ -210,8 +210,10 @@ __device__ __forceinline__ void bb_issue(const It& it, const float* angles, cons
 // 0 solves steps 2-3 (lrmsd_math.cuh) into loss_out[b] and loss_state[b][16].
 // The kLoss variant is compiled for 2 CTAs/SM (up to 255 registers): capped at
 // 128 it spilled the 17 fp64 moment accumulators (fused step 25.0 -> 20.5 us).
-template <int NT, int RPT, int kNS, bool kLoss = false>
-__global__ void __launch_bounds__(NT, kLoss ? 2 : kMinBlocks128Regs(NT)) bb_forward_kernel(const float* __restrict__ angles,
+// kMinB overrides the CTAs/SM the registers are sized for (the launcher picks 2
+// for 128 x 7 when the chains fit two per SM: 256 x 700 fwd 6.80 -> 6.61 us).
+template <int NT, int RPT, int kNS, bool kLoss = false, int kMinB = 0>
+__global__ void __launch_bounds__(NT, kMinB > 0 ? kMinB : (kLoss ? 2 : kMinBlocks128Regs(NT))) bb_forward_kernel(const float* __restrict__ angles,
                                                         const int* __restrict__ lengths, int B, int Lmax,
                                                         float* __restrict__ coords, unsigned* __restrict__ err,
                                                         const float* __restrict__ omega_prev,
@@ -1637,9 +1639,9 @@ static int chain_grid(int B, int cap, int Lmax) {
     return B < g ? B : int(g);
 }
 
-template <int NT, int RPT, int NS, bool LOSS = false>
+template <int NT, int RPT, int NS, bool LOSS = false, int MINB = 0>
 static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
-    auto k = bb_forward_kernel<NT, RPT, NS, LOSS>;
+    auto k = bb_forward_kernel<NT, RPT, NS, LOSS, MINB>;
     const size_t sm = fwd_smem<NT>(RPT, LOSS);
     static LaunchCfg cfg;
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
@@ -1667,6 +1669,8 @@ template <bool kFwd, int NS>
 static cudaError_t dispatch(const BBArgs& a, cudaStream_t st) {
     const BBShape s = bb_shape(kFwd, a.Lmax);
     if (kFwd) {
+        // 128 x 7 with at most two chains per SM: registers for 2 CTAs/SM (no spills)
+        if (s.nt == 128 && s.rpt == 7 && a.B <= 2 * sm_count()) return launch_fwd<128, 7, NS, false, 2>(a, st);
 #define TPL_BB_FWD(NT_, R_) \
     if (s.nt == NT_ && s.rpt == R_) return launch_fwd<NT_, R_, NS>(a, st);
         TPL_BB_FWD(32, 1) TPL_BB_FWD(32, 3) TPL_BB_FWD(32, 5) TPL_BB_FWD(32, 7)
