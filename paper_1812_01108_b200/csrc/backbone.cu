@@ -1786,8 +1786,8 @@ cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
         if (c.nt == 256 && c.rpt == 3 && c.cl == 2) return launch_bwd_xyz_cl<256, 3, 2>(a, st);
         if (c.nt > 0) return cudaErrorInvalidConfiguration;
     }
-    // one 768-residue tile per chain and at most ~3 chains per SM: single-buffered
-    // 256 x 3 (65 KB, 3 CTAs/SM) keeps every chain resident with 8 warps each
+    // one 768-residue tile per chain and at most ~3 chains per SM (two resident): single-buffered
+    // 256 x 3 (65 KB; 2 CTAs/SM at 128 registers) keeps every chain resident with 8 warps each
     const bool env_shape = std::getenv("TPL_BBX") != nullptr;
     if (!env_shape && a.Lmax <= 768 && a.B <= 3 * sm_count()) return launch_bwd_xyz<256, 3, false, false>(a, st);
     // more chains than SMs: single-buffered 128 x 3 (twice the resident CTAs of the
