@@ -46,8 +46,8 @@ struct BBSmem {
     static constexpr int NW = NT / 32;
     static constexpr int kBar = 0;                         // 2 uint64 mbarriers (one per buffer)
     static constexpr int kScratch = 16;                    // 2*NW*12 floats (affine scan)
-    static constexpr int kSuf = kScratch + 2 * NW * 12 * 4;  // NW*6 floats (suffix scan)
-    static constexpr int kTotal = kSuf + NW * 6 * 4;       // 12 floats
+    static constexpr int kSuf = kScratch + 2 * NW * 12 * 4;  // 2*NW*6 + 8 floats (suffix scan)
+    static constexpr int kTotal = kSuf + (2 * NW * 6 + 8) * 4;  // 12 floats
     static constexpr int kMisc = kTotal + 48;              // 16 floats of misc
     static constexpr int kData = ((kMisc + 64 + 15) / 16) * 16;
 };

@@ -368,7 +368,7 @@ __device__ __forceinline__ Aff block_exclusive_scan(Aff a, const Aff& carry, flo
 }
 
 // Block-wide EXCLUSIVE suffix sum of a 6-vector (sum over threads > t) plus a
-// carry (sum over later tiles).  scratch: NT/32 * 6 floats.
+// carry (sum over later tiles).  scratch: (2 * NT/32 * 6 + 8) floats.
 template <int NT>
 __device__ __forceinline__ void block_exclusive_suffix6(float v[6], const float carry[6], float* scratch,
                                                         float out[6], float total[6]) {
@@ -396,6 +396,38 @@ __device__ __forceinline__ void block_exclusive_suffix6(float v[6], const float 
         ex[k] = lane == 31 ? 0.f : o;
     }
     __syncthreads();
+    if (NW > 4) {
+        // wide blocks: warp 0 suffix-scans the NW warp totals in log2(NW) steps and
+        // leaves each warp's later sum (carry included) and the block total in
+        // scratch, instead of every thread re-adding up to 2 NW totals
+        if (warp == 0) {
+            float t[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) t[k] = lane < NW ? scratch[6 * lane + k] : 0.f;
+#pragma unroll
+            for (int d = 1; d < NW; d <<= 1) {
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    const float o = __shfl_down_sync(0xffffffffu, t[k], d);
+                    if (lane + d < NW) t[k] += o;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                const float o = __shfl_down_sync(0xffffffffu, t[k], 1);
+                if (lane < NW) scratch[6 * NW + 6 * lane + k] = carry[k] + (lane + 1 < NW ? o : 0.f);
+                if (lane == 0) scratch[12 * NW + k] = carry[k] + t[k];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            out[k] = scratch[6 * NW + 6 * warp + k] + ex[k];
+            total[k] = scratch[12 * NW + k];
+        }
+        __syncthreads();
+        return;
+    }
     float later[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) later[k] = carry[k];

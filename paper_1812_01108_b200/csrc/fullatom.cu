@@ -36,8 +36,8 @@ struct FASmem {
     static constexpr int NW = NT / 32;
     static constexpr int kBar = 0;
     static constexpr int kScan = 16;                         // 2*NW*12 floats
-    static constexpr int kSuf = kScan + 2 * NW * 12 * 4;     // NW*6 floats
-    static constexpr int kInt = kSuf + NW * 6 * 4;           // NW ints
+    static constexpr int kSuf = kScan + 2 * NW * 12 * 4;     // 2*NW*6 + 8 floats
+    static constexpr int kInt = kSuf + (2 * NW * 6 + 8) * 4;  // NW ints
     static constexpr int kTotal = r16(kInt + NW * 4);        // 12 floats
     static constexpr int kMisc = kTotal + 48;                // 16 floats / ints
     static constexpr int kTable = r16(kMisc + 64);           // n_types * sizeof(FAType)
@@ -625,8 +625,8 @@ template <int NT>
 struct FAXSmem {
     static constexpr int NW = NT / 32;
     static constexpr int kBar = 0;                   // 4 mbarriers: 2 tile buffers, table, chain restype
-    static constexpr int kSuf = 32;                  // NW*6 floats
-    static constexpr int kInt = kSuf + NW * 6 * 4;   // NW ints
+    static constexpr int kSuf = 32;                         // 2*NW*6 + 8 floats
+    static constexpr int kInt = kSuf + (2 * NW * 6 + 8) * 4;  // NW ints
     static constexpr int kTable = r16(kInt + NW * 4);
 };
 
