@@ -12,8 +12,9 @@ arrays into it, plus the LRMSD oracle in ``lrmsd.py``.
 
 Parity status: every function here is pinned by ``tests/test_oracle_*.py``
 against values and properties fixed by the paper and by geometry (DESIGN.md
-"Oracle pins").  Absolute side-chain geometry is data (the residue table),
-"parity unpinned" beyond self-consistency (reading Q8).
+"Oracle pins").  Absolute side-chain geometry is data (the residue table,
+reading Q8), pinned against textbook covalent geometry (Engh & Huber bond
+lengths and angles, connectivity, ring planarity; V16).
 """
 import ctypes
 import os

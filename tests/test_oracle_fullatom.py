@@ -180,3 +180,95 @@ def test_input_validation(oracle_lib, table):
         oracle_lib.fullatom_forward(table, ang, np.zeros((1, 3), dtype=np.uint8), [0])
     with pytest.raises(ValueError):
         oracle_lib.fullatom_forward(table, ang, np.zeros((1, 3), dtype=np.uint8), [3], atom_stride=10)
+
+
+# Textbook covalent radii (Å) of the heavy elements in the 20 residues; a bond is a
+# pair closer than r1 + r2 + 0.25 Å.  Independent of the table generator (reading Q8).
+_COV = {"C": 0.76, "N": 0.71, "O": 0.66, "S": 1.05}
+
+
+def _element(atom_name):
+    return atom_name[0]
+
+
+def _bond_angles(R, bond):
+    out = {}
+    for k in range(len(R)):
+        nbr = np.nonzero(bond[k])[0]
+        for i1 in range(len(nbr)):
+            for i2 in range(i1 + 1, len(nbr)):
+                u, v = R[nbr[i1]] - R[k], R[nbr[i2]] - R[k]
+                out[(nbr[i1], k, nbr[i2])] = math.degrees(
+                    math.acos(np.dot(u, v) / np.linalg.norm(u) / np.linalg.norm(v)))
+    return out
+
+
+def test_side_chain_covalent_geometry(oracle_lib, table):
+    """Reading Q8 pin against chemistry rather than the table itself: the placed side
+    chains have the standard covalent geometry (Engh & Huber 1991).
+
+    At the all-trans rotamer (every χ = π, random φ/ψ/ω) the bond graph (pairs closer
+    than the sum of covalent radii + 0.25 Å) over N, CA, side chain, C, O is
+    connected; bonds are 1.2-1.9 Å; bond angles are 100-135° (5-ring exocyclic angles
+    reach 131°); 1-3 pairs are 2.1-2.9 Å apart (carboxylate O-O 2.19 Å, CA-SG 2.8 Å),
+    farther pairs > 1.9 Å except with O (ψ is random: O may clash with the side chain); CA-CB = 1.53 Å; N-CA-CB = 110.5° (PRO 103.0°); PHE/TYR
+    rings are planar.  C-CA-CB follows from the paper's N-CA-C (reading Q7) and is
+    skipped.  Under random χ every bond length and bond angle is unchanged (torsions
+    move no covalent geometry)."""
+    rng = np.random.default_rng(11)
+    B, L = 3, 20
+    ang, rt = _rand(rng, B, L)
+    rt[0, :] = np.arange(20)
+    trans = ang.copy()
+    trans[..., 3:] = math.pi
+    X0, _ = oracle_lib.fullatom_forward(table, trans, rt, np.full(B, L))
+    X1, _ = oracle_lib.fullatom_forward(table, ang, rt, np.full(B, L))
+    checked = set()
+    for b in range(B):
+        off = _offsets(table, rt[b], L)
+        for j in range(L):
+            ty = table["types"][rt[b, j]]
+            names = [a["name"] for a in ty["atoms"]]
+            n = len(names)
+            R = X0[b, off[j]: off[j + 1]]
+            pos = dict(zip(names, R))
+            D = np.linalg.norm(R[:, None] - R[None], axis=-1)
+            cut = np.array([[_COV[_element(a)] + _COV[_element(c)] + 0.25 for c in names] for a in names])
+            bond = (D < cut) & ~np.eye(n, dtype=bool)
+            assert np.all((D[bond] > 1.2) & (D[bond] < 1.9)), (ty["name"], D[bond])
+            # bond-graph distances (BFS from every atom); the graph is connected
+            hops = np.full((n, n), -1)
+            for s0 in range(n):
+                hops[s0, s0], todo = 0, [s0]
+                while todo:
+                    k = todo.pop(0)
+                    for m in np.nonzero(bond[k])[0]:
+                        if hops[s0, m] < 0:
+                            hops[s0, m] = hops[s0, k] + 1
+                            todo.append(m)
+            assert np.all(hops >= 0), (ty["name"], [names[k] for k in range(n) if hops[0, k] < 0])
+            assert np.all((D[hops == 2] > 2.1) & (D[hops == 2] < 2.9)), (ty["name"], sorted(D[hops == 2]))
+            far = (hops >= 3) & ~np.isin(np.array(names), ["O"])[:, None] & ~np.isin(np.array(names), ["O"])[None]
+            assert np.all(D[far] > 1.9), (ty["name"], [(names[p], names[q], D[p, q]) for p, q in zip(*np.nonzero(far & (D <= 1.9)))])
+            ba = _bond_angles(R, bond)
+            for (i, k, m), a in ba.items():
+                if names[k] == "CA" and "C" in (names[i], names[m]):
+                    continue  # fixed by the paper's backbone constants (reading Q7)
+                assert 100.0 < a < 135.0, (ty["name"], names[i], names[k], names[m], a)
+            if "CB" in pos:
+                assert abs(np.linalg.norm(pos["CB"] - pos["CA"]) - 1.53) < 0.03, ty["name"]
+                u, v = pos["N"] - pos["CA"], pos["CB"] - pos["CA"]
+                a = math.degrees(math.acos(np.dot(u, v) / np.linalg.norm(u) / np.linalg.norm(v)))
+                assert abs(a - (103.0 if ty["name"] == "PRO" else 110.5)) < 2.0, (ty["name"], a)
+            if ty["name"] in ("PHE", "TYR"):
+                P = np.array([pos[a] for a in ("CG", "CD1", "CD2", "CE1", "CE2", "CZ")])
+                assert np.linalg.svd(P - P.mean(0), compute_uv=False)[-1] < 0.02, ty["name"]
+            # random chi: the same covalent geometry
+            R1 = X1[b, off[j]: off[j + 1]]
+            D1 = np.linalg.norm(R1[:, None] - R1[None], axis=-1)
+            np.testing.assert_allclose(D1[bond], D[bond], atol=1e-9)
+            ba1 = _bond_angles(R1, bond)
+            for key, a in ba.items():
+                assert abs(ba1[key] - a) < 1e-6, (ty["name"], key)
+            checked.add(ty["name"])
+    assert len(checked) == 20
