@@ -104,3 +104,40 @@ def test_random_shapes_backbone(abi, oracle_lib, seed):
     c, ga, gx = _bb(abi, ang, ln, grad)
     chains = sorted(set(rng.choice(B, size=min(B, 4), replace=False).tolist()) | {int(np.argmax(lengths))})
     _check_bb(oracle_lib, ang, ln, grad, c, ga, gx, chains)
+
+
+_FA_SHAPES = [(1, 1), (20, 3), (2, 127), (3, 257), (2, 511), (17, 700), (147, 1100), (149, 256), (149, 513),
+              (297, 127), (300, 700), (300, 255)]
+
+
+@pytest.mark.parametrize("seed", range(len(_FA_SHAPES)))
+def test_random_shapes_fullatom(abi, oracle_lib, table, seed):
+    """Full-atom forward + backward (PAPER §2, Eq. 1) on random ragged batches whose
+    B and Lmax straddle the launchers' switch points (B <= 148 / <= 296 / more;
+    Lmax around 256 and the 128/256/512-residue tiles); sampled chains vs the oracle."""
+    import paper_1812_01108_b200 as tpl
+
+    rng = np.random.default_rng(9900 + seed)
+    B, Lmax = _FA_SHAPES[seed]
+    lengths = rng.integers(1, Lmax + 1, size=B)
+    lengths[rng.integers(0, B)] = Lmax
+    ang = synth.angles_uniform(B, Lmax, 8, 9910 + seed)
+    rt = synth.restype_uniform(B, Lmax, 20, 9920 + seed)
+    ln = torch.tensor(lengths, dtype=torch.int32)
+    tables = tpl.Tables(table)
+    a = ang.cuda().requires_grad_(True)
+    coords = tpl.fullatom(a, rt.cuda(), ln.cuda(), tables)
+    grad = synth.grad_normal(tuple(coords.shape), 9930 + seed)
+    (coords * grad.cuda()).sum().backward()
+    c, ga = coords.detach().cpu().numpy(), a.grad.cpu().numpy()
+    chains = sorted(set(rng.choice(B, size=min(B, 3), replace=False).tolist()) | {int(np.argmax(lengths))})
+    idx = np.array(chains)
+    a64, g64 = synth.numpy64(ang)[idx], synth.numpy64(grad)[idx]
+    X, nat = oracle_lib.fullatom_forward(table, a64, rt.numpy()[idx], lengths[idx], coords.shape[1])
+    G = oracle_lib.fullatom_backward(table, a64, rt.numpy()[idx], lengths[idx], g64)
+    for n, b in enumerate(idx):
+        L, na = int(lengths[b]), int(nat[n])
+        tol = 1e-3 if L <= 1000 else 5e-3  # north_star's coordinate gate holds for L <= 1000
+        assert np.abs(c[b, :na] - X[n, :na]).max() <= tol, (B, Lmax, b, L)
+        ref = G[n, :L]
+        assert np.abs(ga[b, :L] - ref).max() / max(np.abs(ref).max(), 1e-30) <= 1e-3, (B, Lmax, b, L)
