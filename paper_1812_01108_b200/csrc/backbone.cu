@@ -984,7 +984,10 @@ __device__ __forceinline__ void bbx_issue(const BBIter& it, const float* coords,
 // kDB: two staging buffers (the next item's tiles load during this one); without
 // it one buffer, refilled after the walk -- for grids where every CTA owns one
 // item, so that twice the threads fit per SM.
-template <int NT, int RPT, bool kLoss = false, bool kDB = true>
+// kPW: every thread closes omega of its own last residue from its exclusive suffix
+// (the lever arm of N_{j+1} about itself is zero) and each warp bulk-stores its own
+// residues as soon as its lanes are done (no block barrier before the store).
+template <int NT, int RPT, bool kLoss = false, bool kDB = true, bool kPW = false>
 __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_kernel(const float* __restrict__ coords,
                                                              const int* __restrict__ lengths, int B, int Lmax,
                                                              const float* __restrict__ grad_coords,
@@ -1128,7 +1131,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
                 sum6[5] += fmaf(Px[a], Gy[a], -Py[a] * Gx[a]);
             }
         }
-        if (tid == 0) bulk_wait_read_all();  // the output staging is free again
+        if (kPW ? (tid & 31) == 0 : tid == 0) bulk_wait_read_all();  // the output staging is free again
         if (k < 2) TPL_STAMP(3 + 4 * k);
         float su[6], tot6[6];
         block_exclusive_suffix6<NT>(sum6, carry6, s_suf, su, tot6);
@@ -1145,6 +1148,31 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
         // pass 2: atoms last to first
         const Span so = make_span(grad_angles + ((size_t)b * Lmax + r0) * 3, n * 12);
         float* s_go = reinterpret_cast<float*>(s_go_base + so.mis());
+        float w_last = 0.f;  // kPW: omega of this thread's last residue, e . (T - p_N x S) about N_{j+1}
+        if (kPW && nq > 0) {
+            const int an = 3 * (rl0 + nq);  // atom index of N_{j+1} in the tile
+            float nx_ = 0.f, ny_ = 0.f, nz_ = 0.f;
+            bool has_n = true;
+            if (rl0 + nq < n) {
+                nx_ = s_x[3 * an]; ny_ = s_x[3 * an + 1]; nz_ = s_x[3 * an + 2];
+            } else if (!last_tile) {
+                const float* gn = coords + ((size_t)b * 3 * Lmax + 3 * (size_t)(r0 + n)) * 3;
+                nx_ = __ldg(gn); ny_ = __ldg(gn + 1); nz_ = __ldg(gn + 2);
+            } else if (has_ext) {
+                nx_ = cnx; ny_ = cny; nz_ = cnz;
+            } else {
+                has_n = false;  // omega_{L-1} is a structural zero
+            }
+            if (has_n) {
+                const float* xc = s_x + 3 * (an - 1);
+                const float ux = nx_ - xc[0], uy = ny_ - xc[1], uz = nz_ - xc[2];
+                const float px = nx_ - cx, py = ny_ - cy, pz = nz_ - cz;
+                const float c0 = su[3] - fmaf(py, su[2], -pz * su[1]);
+                const float c1 = su[4] - fmaf(pz, su[0], -px * su[2]);
+                const float c2 = su[5] - fmaf(px, su[1], -py * su[0]);
+                w_last = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * fmaf(ux, c0, fmaf(uy, c1, uz * c2));
+            }
+        }
 #pragma unroll
         for (int q = RPT - 1; q >= 0; --q) {
             if (q < nq) {
@@ -1166,13 +1194,44 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
                 }
                 s_go[3 * rl + 0] = ga[1];  // phi_j
                 s_go[3 * rl + 1] = ga[2];  // psi_j
-                if (j > 0) {               // omega_{j-1}
+                if (kPW) {
+                    if (q > 0) s_go[3 * (rl - 1) + 2] = ga[0];  // omega_{j-1}, this thread's residue
+                    if (q == nq - 1) s_go[3 * rl + 2] = w_last;
+                } else if (j > 0) {  // omega_{j-1}
                     if (rl > 0) s_go[3 * (rl - 1) + 2] = ga[0];
                     else s_misc[0] = ga[0];  // belongs to the previous tile
                 }
             }
         }
         if (k < 2) TPL_STAMP(11 + k);
+        if constexpr (kPW) {
+            // per-warp stores (as bb_forward_kernel): a warp's residues are contiguous and
+            // start 12 * 32 * RPT bytes apart, so shared and global keep the same 16-byte phase
+            fence_proxy_async_smem();
+            __syncwarp();
+            const int lane = tid & 31, w0 = (tid >> 5) * 32 * RPT, wn = min(32 * RPT, n - w0);
+            if (wn > 0) {
+                const Span sw = make_span(grad_angles + ((size_t)b * Lmax + r0 + w0) * 3, wn * 12);
+                const float* src = s_go + 3 * w0;
+                if (lane == 0 && sw.mid > 0) {
+                    bulk_s2g(const_cast<char*>(sw.g) + sw.head, reinterpret_cast<const char*>(src) + sw.head,
+                             unsigned(sw.mid));
+                    bulk_commit();
+                }
+                float* g = reinterpret_cast<float*>(const_cast<char*>(sw.g));
+                const int nh = sw.head >> 2, ntl = sw.tail() >> 2, off_t = (sw.head + sw.mid) >> 2;
+                for (int e = lane; e < nh + ntl; e += 32) {
+                    const int idx = e < nh ? e : off_t + (e - nh);
+                    g[idx] = src[idx];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 6; ++q) carry6[q] = tot6[q];
+            __syncthreads();  // s_x, s_g and the scan scratch are free again
+            if (!kDB && tid == 0 && nx.valid) bbx_issue(nx, coords, grad_coords, s_x_buf, s_g_buf, bar);
+            it = nx;
+            continue;
+        }
         if (tid == 0) {
             float w = last_tile ? 0.f : omega_next;
             if (last_tile && has_ext) {  // omega_{L-1} = e . T_n (the later segments about their N)
@@ -1197,7 +1256,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
         __syncthreads();
         it = nx;
     }
-    if (tid == 0) bulk_wait_read_all();
+    if (kPW ? (tid & 31) == 0 : tid == 0) bulk_wait_read_all();
     TPL_STAMP(10);
 }
 
@@ -1687,9 +1746,9 @@ static cudaError_t dispatch(const BBArgs& a, cudaStream_t st) {
     return cudaErrorInvalidConfiguration;
 }
 
-template <int NT, int RPT, bool LOSS = false, bool DB = true>
+template <int NT, int RPT, bool LOSS = false, bool DB = true, bool PW = false>
 static cudaError_t launch_bwd_xyz(const BBArgs& a, cudaStream_t st) {
-    auto k = bb_backward_xyz_kernel<NT, RPT, LOSS, DB>;
+    auto k = bb_backward_xyz_kernel<NT, RPT, LOSS, DB, PW>;
     const int tile = NT * RPT;
     const int nb = DB ? 2 : 1;
     const size_t sm = BBSmem<NT>::kData + nb * round16(16 + 36 * tile + 12) + nb * round16(16 + 36 * tile) +
@@ -1789,11 +1848,17 @@ cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
     // one 768-residue tile per chain and at most ~3 chains per SM (two resident): single-buffered
     // 256 x 3 (65 KB; 2 CTAs/SM at 128 registers) keeps every chain resident with 8 warps each
     const bool env_shape = std::getenv("TPL_BBX") != nullptr;
-    if (!env_shape && a.Lmax <= 768 && a.B <= 3 * sm_count()) return launch_bwd_xyz<256, 3, false, false>(a, st);
+    static const bool pw = [] {
+        const char* e = std::getenv("TPL_BBX_PW");
+        return e != nullptr && e[0] == '1';
+    }();
+    if (!env_shape && a.Lmax <= 768 && a.B <= 3 * sm_count())
+        return pw ? launch_bwd_xyz<256, 3, false, false, true>(a, st) : launch_bwd_xyz<256, 3, false, false>(a, st);
     // more chains than SMs: single-buffered 128 x 3 (twice the resident CTAs of the
     // double-buffered shape; measured, tools/gpu_bbxs.sh: 4096 x 700 56.0 -> 50.9 us,
     // 512 x 1000 18.2 -> 13.5 us, config 4 96.6 -> 86.2 us)
-    if (!env_shape && a.B > sm_count() && a.Lmax > 128) return launch_bwd_xyz<128, 3, false, false>(a, st);
+    if (!env_shape && a.B > sm_count() && a.Lmax > 128)
+        return pw ? launch_bwd_xyz<128, 3, false, false, true>(a, st) : launch_bwd_xyz<128, 3, false, false>(a, st);
     const BBShape s = bbx_shape(a.B, a.Lmax);
 #define TPL_BBX(NT_, R_) \
     if (s.nt == NT_ && s.rpt == R_) return launch_bwd_xyz<NT_, R_>(a, st);
