@@ -141,3 +141,18 @@ def test_random_shapes_fullatom(abi, oracle_lib, table, seed):
         assert np.abs(c[b, :na] - X[n, :na]).max() <= tol, (B, Lmax, b, L)
         ref = G[n, :L]
         assert np.abs(ga[b, :L] - ref).max() / max(np.abs(ref).max(), 1e-30) <= 1e-3, (B, Lmax, b, L)
+
+
+def test_per_warp_store_variant_parity(abi):
+    """The opt-in coordinate backward with per-warp stores (TPL_BBX_PW=1, read once
+    per process) passes the same randomised backbone parity in a fresh process."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, TPL_BBX_PW="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_fuzz.py"), "-k", "random_shapes_backbone"],
+                       env=env, cwd=os.path.dirname(here), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
