@@ -328,7 +328,9 @@ __global__ void __launch_bounds__(NT, kMinB > 0 ? kMinB : (kLoss ? 2 : kMinBlock
             }
         };
         pass1(std::false_type{});
-        if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
+        // rare: huge angles.  pass 1 is thread-local, so the redo is decided per warp (a
+        // warp-uniform branch, no block barrier: the block scan below synchronises)
+        if (__any_sync(0xffffffffu, maxabs > kSinCosFastMax)) pass1(std::true_type{});
         if (kNS >= 1) aff_orthonormalize(M);
         if ((tid & 31) == 0) bulk_wait_read_all();  // the output staging is free again (per-warp groups)
         TPL_STAMP(4);
