@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_cl_kerne
         }
     };
     pass1(std::false_type{});
-    if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
+    if (__any_sync(0xffffffffu, maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles (per warp)
     if (kNS >= 1) aff_orthonormalize(M);
     Aff P = block_exclusive_scan<NT, kNS>(M, aff_identity(), scratch, s_total);  // part-local prefix
     // ---- exchange: A_rank to every later non-empty part of the chain
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_forward_dl_kerne
             }
         };
         pass1(std::false_type{});
-        if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
+        if (__any_sync(0xffffffffu, maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles (per warp)
         if (kNS >= 1) aff_orthonormalize(M);
         if (tid == 0) bulk_wait_read_all();  // the output staging is free again
         Aff P = block_exclusive_scan<NT, kNS>(M, aff_identity(), scratch, s_total);  // tile-local prefix
@@ -862,7 +862,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_kernel(
             }
         };
         pass1(std::false_type{});
-        if (__syncthreads_or(maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
+        if (__any_sync(0xffffffffu, maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles (per warp)
         if (kNS >= 1) aff_orthonormalize(M);
         if (tid == 0) bulk_wait_read_all();  // the gradient staging is free again
         const Aff P = block_exclusive_scan<NT, kNS>(M, carry, scratch, s_total);
