@@ -28,6 +28,10 @@
 #include "kernels.h"
 
 namespace tpl {
+// added to a thread's atom count when its residue type is out of range: far above any
+// tile's atom count (< 2^16), and 512 threads x 2^21 stay below 2^31, so the tile's
+// total (block total minus the carry) flags it without overflow
+constexpr int kBadRestype = 1 << 21;
 
 __host__ __device__ constexpr int r16(int x) { return (x + 15) & ~15; }
 
@@ -191,15 +195,17 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
                 }
             }
         }
-        if (__syncthreads_or(bad)) {
+        // a bad restype rides in the atom-count scan (kBadRestype >> any tile's atom count), so
+        // the block-uniform early return needs no barrier of its own
+        int tile_end_atoms;
+        const int off0 = block_exclusive_sum_int<NT>(cnt + (bad ? kBadRestype : 0), carry_atoms, s_int, &tile_end_atoms);
+        if (tile_end_atoms - carry_atoms >= kBadRestype) {
             if (tid == 0) {
                 atomicOr(a.err, ERR_RESTYPE);
                 bulk_wait_all();
             }
             return;
         }
-        int tile_end_atoms;
-        const int off0 = block_exclusive_sum_int<NT>(cnt, carry_atoms, s_int, &tile_end_atoms);
         if (tile_end_atoms > a.atom_stride) {  // the chain's atoms do not fit its row: flag, skip
             if (tid == 0) {
                 atomicOr(a.err, ERR_STRIDE);
@@ -473,15 +479,15 @@ __global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_
                 }
             }
         }
-        if (__syncthreads_or(bad)) {
+        int tile_end;  // a bad restype rides in the scan (as the forward)
+        const int off0 = block_exclusive_sum_int<NT>(cnt + (bad ? kBadRestype : 0), carry_atoms, s_int, &tile_end);
+        if (tile_end - carry_atoms >= kBadRestype) {
             if (tid == 0) {
                 atomicOr(a.err, ERR_RESTYPE);
                 bulk_wait_all();
             }
             return;
         }
-        int tile_end;
-        const int off0 = block_exclusive_sum_int<NT>(cnt, carry_atoms, s_int, &tile_end);
         if (tile_end > a.atom_stride) {
             if (tid == 0) {
                 atomicOr(a.err, ERR_STRIDE);
