@@ -56,6 +56,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds of the cpu_baseline sample")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-parity", action="store_true", help="skip the oracle parity leg (A/B timing runs only)")
     p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                    help="weak: every rank runs the config's batch; strong: the batch is split (LPT)")
     return p.parse_args()
@@ -561,6 +562,10 @@ def run_ours(args):
             "step_GB/s": (ab["fwd"] + ab["bwd"]) / (ms_step * 1e-3) / 1e9,
             "step_frac": (ab["fwd"] + ab["bwd"]) / (ms_step * 1e-3) / 1e9 / peak}
 
+    parity = None
+    if not args.no_parity:
+        parity = parity_leg(work, sets[0], c, dist)
+
     cpu = None
     # the oracle's O(L^2) backward makes a 20000-residue chain a minute of CPU: no sample for "long";
     # the loss config's oracle would time the same backbone work as the metric config
@@ -579,14 +584,98 @@ def run_ours(args):
                "ms_per_step": ms_step, "ms_per_step_ci95": ci95, "higher_is_better": True,
                "scaling": args.scaling, "vs_baseline": None,
                "dtype": "f32", "data": "synthetic (seeded uniform angles, N(0,1) dL/dr)", "config": cfgd,
-               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": work.launches_per_step * K,
+               "roofline": roof, "parity": parity, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": work.launches_per_step * K,
                "impl": "paper_gpu_design" if args.impl == "paper" else "ours"}
         print(json.dumps(out))
     if dist is not None:
         dist.destroy_process_group()
 
 
-# --------------------------------------------------------------- CPU oracle
+# --------------------------------------------------------------- oracle legs
+def parity_chains(work, cfg_name):
+    """every chain for the small configs, else 64 seeded chains including the longest."""
+    B = work.B
+    ln = work.host["lengths"].numpy()
+    if cfg_name in ("metric", "lrmsd", "long", 1, 2, 3) or B <= 64:
+        return np.arange(B)
+    rng = np.random.default_rng(6000 + synth.config_id(cfg_name))
+    pick = set(rng.choice(B, size=63, replace=False).tolist())
+    pick.add(int(np.argmax(ln)))
+    return np.array(sorted(pick))[:64]
+
+
+def parity_leg(work, s, cfg_name, dist):
+    """The bench's own correctness check: one more fwd+bwd on
+    the first buffer set -- the inputs the timed region used -- compared element by
+    element with the fp64 oracle on a bounded set of chains.  Gates (north_star):
+    coordinates <= 1e-3 A for L <= 1000 (5e-3 A beyond, reading Q21), per-chain
+    norm-wise gradient error <= 1e-3 (reading Q18).  MAX over ranks."""
+    import oracle
+
+    oracle.build()
+    work.fwd(s)
+    work.bwd(s)
+    torch.cuda.synchronize()
+    idx = parity_chains(work, cfg_name)
+    h = work.host
+    a64 = synth.numpy64(h["angles"])[idx]
+    ln = h["lengths"].numpy()[idx]
+    coords = s["coords"].cpu().numpy()[idx]
+    gang = s["gang"].cpu().numpy()[idx]
+    check_grad = int(ln.max()) <= 5000  # the O(L^2) oracle backward of one 20000-residue chain is minutes
+    coord_err, grad_err, coord_err_long = 0.0, 0.0, 0.0
+    loss_err = None
+    if work.model == "backbone":
+        X = oracle.backbone_forward(a64, ln)
+        if isinstance(work, LossBackboneWork):
+            from oracle import lrmsd as olr
+
+            tgt = synth.numpy64(h["target"])[idx]
+            vals, dldr = olr.batch(X, tgt, 3 * ln)
+            loss = s["loss"].cpu().numpy()[idx]
+            loss_err = float(np.max(np.abs(loss - vals) / np.maximum(np.abs(vals), 1e-12)))
+            G = oracle.backbone_backward(a64, ln, dldr) if check_grad else None
+        else:
+            G = oracle.backbone_backward(a64, ln, synth.numpy64(h["grad"])[idx]) if check_grad else None
+        for k, L in enumerate(ln):
+            e = float(np.abs(coords[k, : 3 * L] - X[k, : 3 * L]).max())
+            if L <= 1000:
+                coord_err = max(coord_err, e)
+            else:
+                coord_err_long = max(coord_err_long, e)
+    else:
+        rt = h["restype"].numpy()[idx]
+        X, nat = oracle.fullatom_forward(work.table, a64, rt, ln, work.stride)
+        G = oracle.fullatom_backward(work.table, a64, rt, ln, synth.numpy64(h["grad"])[idx]) if check_grad else None
+        for k, L in enumerate(ln):
+            e = float(np.abs(coords[k, : nat[k]] - X[k, : nat[k]]).max())
+            if L <= 1000:
+                coord_err = max(coord_err, e)
+            else:
+                coord_err_long = max(coord_err_long, e)
+    if G is not None:
+        for k in range(len(idx)):
+            den = float(np.abs(G[k]).max())
+            if den > 0:
+                grad_err = max(grad_err, float(np.abs(gang[k] - G[k]).max()) / den)
+    vals = [coord_err, coord_err_long, grad_err, loss_err or 0.0, float(len(idx))]
+    if dist is not None:
+        t = torch.tensor(vals[:4], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        n = torch.tensor([vals[4]], dtype=torch.float64, device="cuda")
+        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+        vals = t.tolist() + n.tolist()
+    ok = vals[0] <= 1e-3 and vals[1] <= 5e-3 and (G is None or vals[2] <= 1e-3) and (loss_err is None or vals[3] <= 1e-4)
+    out = {"chains": int(vals[4]), "max_coord_err_A": vals[0], "max_grad_rel_err": vals[2] if G is not None else None,
+           "ok": bool(ok), "gate": "coords <= 1e-3 A (L <= 1000), grad <= 1e-3 per-chain norm-wise (Q18)",
+           "inputs": "the timed region's first buffer set, vs the fp64 oracle"}
+    if coord_err_long or int(ln.max()) > 1000:
+        out["max_coord_err_A_L_gt_1000"] = vals[1]
+    if loss_err is not None:
+        out["max_loss_rel_err"] = vals[3]
+    return out
+
+
 def cpu_baseline(work, seconds):
     """The fp64 oracle as it stands (paper-literal O(L^2) backward, OpenMP over
     chains) on this host's cores, on a bounded sample of the same workload."""

@@ -147,6 +147,23 @@ def _stream(stream):
     return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
 
 
+def _on_device(fn):
+    """Run the C call with the device of its first CUDA tensor argument current, so
+    that the default stream (current_stream()) and the library's per-device launch
+    state belong to the device the pointers live on."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        for a in list(args) + list(kwargs.values()):
+            if isinstance(a, torch.Tensor) and a.is_cuda:
+                with torch.cuda.device(a.device):
+                    return fn(*args, **kwargs)
+        return fn(*args, **kwargs)
+
+    return wrapper
+
+
 def tpl_abi_version():
     return int(lib.tpl_abi_version())
 
@@ -159,10 +176,12 @@ def tpl_backbone_atoms(L):
     return int(lib.tpl_backbone_atoms(int(L)))
 
 
+@_on_device
 def tpl_sync_status(workspace, stream=None):
     _check(lib.tpl_sync_status(_stream(stream), _dev(workspace, torch.uint8, "workspace")))
 
 
+@_on_device
 def tpl_backbone_forward(angles, lengths, coords, workspace, stream=None):
     B, Lmax, three = angles.shape
     if three != BB_SLOTS or tuple(coords.shape) != (B, 3 * Lmax, 3) or tuple(lengths.shape) != (B,):
@@ -172,6 +191,7 @@ def tpl_backbone_forward(angles, lengths, coords, workspace, stream=None):
                                     _dev(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream)))
 
 
+@_on_device
 def tpl_backbone_backward(angles, lengths, grad_coords, grad_angles, workspace, stream=None):
     B, Lmax, three = angles.shape
     if (three != BB_SLOTS or tuple(grad_coords.shape) != (B, 3 * Lmax, 3)
@@ -184,6 +204,7 @@ def tpl_backbone_backward(angles, lengths, grad_coords, grad_angles, workspace, 
                                      _stream(stream)))
 
 
+@_on_device
 def tpl_backbone_backward_from_coords(coords, lengths, grad_coords, grad_angles, workspace, stream=None):
     B, Lmax, three = grad_angles.shape
     if (three != BB_SLOTS or tuple(coords.shape) != (B, 3 * Lmax, 3) or tuple(grad_coords.shape) != (B, 3 * Lmax, 3)
@@ -225,6 +246,7 @@ def tpl_fullatom_atoms(handle, restype_host, lengths_host):
     return apc, int(stride.value)
 
 
+@_on_device
 def tpl_fullatom_forward(handle, angles, restype, lengths, coords, workspace, stream=None):
     B, Lmax, slots = angles.shape
     if slots != FA_SLOTS or tuple(restype.shape) != (B, Lmax) or coords.dim() != 3 or coords.shape[0] != B:
@@ -235,6 +257,7 @@ def tpl_fullatom_forward(handle, angles, restype, lengths, coords, workspace, st
                                     _dev(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream)))
 
 
+@_on_device
 def tpl_fullatom_backward(handle, angles, restype, lengths, grad_coords, grad_angles, workspace, stream=None):
     B, Lmax, slots = angles.shape
     if slots != FA_SLOTS or tuple(grad_angles.shape) != (B, Lmax, FA_SLOTS) or grad_coords.shape[0] != B:
@@ -246,6 +269,7 @@ def tpl_fullatom_backward(handle, angles, restype, lengths, grad_coords, grad_an
                                      _dev(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream)))
 
 
+@_on_device
 def tpl_fullatom_backward_from_coords(handle, coords, restype, lengths, grad_coords, grad_angles, workspace,
                                       stream=None):
     B, Lmax, slots = grad_angles.shape
@@ -265,6 +289,7 @@ def tpl_tables_backward_from_coords_ok(handle):
     return bool(lib.tpl_tables_backward_from_coords_ok(ctypes.c_void_p(handle)))
 
 
+@_on_device
 def tpl_backbone_forward_precise(angles, lengths, coords, workspace, stream=None):
     """f2: the backbone forward computed in fp64 internally (coords rounded to fp32)."""
     B, Lmax, three = angles.shape
@@ -277,6 +302,7 @@ def tpl_backbone_forward_precise(angles, lengths, coords, workspace, stream=None
                                             _stream(stream)))
 
 
+@_on_device
 def tpl_backbone_lrmsd_forward(angles, lengths, target, coords, lrmsd, state, workspace, stream=None):
     """f1: backbone forward + LRMSD against target, fused (per-chain loss over the 3L backbone atoms)."""
     B, Lmax, three = angles.shape
@@ -291,6 +317,7 @@ def tpl_backbone_lrmsd_forward(angles, lengths, target, coords, lrmsd, state, wo
                                           _stream(stream)))
 
 
+@_on_device
 def tpl_backbone_lrmsd_backward(coords, lengths, target, state, grad_lrmsd, grad_angles, workspace, stream=None):
     B, atoms, _ = coords.shape
     if (tuple(target.shape) != tuple(coords.shape) or tuple(grad_angles.shape) != (B, atoms // 3, 3)
@@ -305,6 +332,7 @@ def tpl_backbone_lrmsd_backward(coords, lengths, target, state, grad_lrmsd, grad
                                            _stream(stream)))
 
 
+@_on_device
 def tpl_backbone_segment_forward(angles, lengths, omega_prev, coords, aggregate, workspace, stream=None):
     B, Lmax, three = angles.shape
     if three != BB_SLOTS or tuple(coords.shape) != (B, 3 * Lmax, 3) or aggregate.numel() != 12 * B:
@@ -318,6 +346,7 @@ def tpl_backbone_segment_forward(angles, lengths, omega_prev, coords, aggregate,
                                             _stream(stream)))
 
 
+@_on_device
 def tpl_backbone_segment_place(coords, lengths, aggregates, seg, workspace, stream=None):
     B, atoms, _ = coords.shape
     n_seg = aggregates.numel() // (12 * B)
@@ -327,6 +356,7 @@ def tpl_backbone_segment_place(coords, lengths, aggregates, seg, workspace, stre
                                           _stream(stream)))
 
 
+@_on_device
 def tpl_backbone_segment_totals(coords, lengths, grad_coords, totals, workspace, stream=None):
     B, atoms, _ = coords.shape
     if tuple(grad_coords.shape) != tuple(coords.shape) or totals.numel() != 12 * B:
@@ -339,6 +369,7 @@ def tpl_backbone_segment_totals(coords, lengths, grad_coords, totals, workspace,
                                            _stream(stream)))
 
 
+@_on_device
 def tpl_backbone_segment_backward(coords, lengths, grad_coords, totals, seg, grad_angles, workspace, stream=None):
     B, atoms, _ = coords.shape
     n_seg = totals.numel() // (12 * B)
@@ -357,6 +388,7 @@ def tpl_paper_backbone_saved_floats(B, Lmax):
     return int(lib.tpl_paper_backbone_saved_floats(int(B), int(Lmax)))
 
 
+@_on_device
 def tpl_paper_backbone_forward(angles, lengths, coords, saved_M, workspace, stream=None):
     """the paper's GPU design (saves M_i, 64 B/atom) -- a comparison point."""
     B, Lmax, three = angles.shape
@@ -370,6 +402,7 @@ def tpl_paper_backbone_forward(angles, lengths, coords, saved_M, workspace, stre
                                           _stream(stream)))
 
 
+@_on_device
 def tpl_paper_backbone_backward(angles, lengths, saved_M, grad_coords, grad_angles, workspace, stream=None):
     """O(L^2) per-angle sums without a reduction."""
     B, Lmax, three = angles.shape
@@ -385,6 +418,7 @@ def tpl_paper_backbone_backward(angles, lengths, saved_M, grad_coords, grad_angl
                                            _stream(stream)))
 
 
+@_on_device
 def tpl_lrmsd_forward(x, y, n_atoms, lrmsd, state, workspace, stream=None):
     B, S, three = x.shape
     if three != 3 or tuple(y.shape) != (B, S, 3) or tuple(lrmsd.shape) != (B,) or tuple(state.shape) != (B, 16):
@@ -395,6 +429,7 @@ def tpl_lrmsd_forward(x, y, n_atoms, lrmsd, state, workspace, stream=None):
                                  workspace.numel(), _stream(stream)))
 
 
+@_on_device
 def tpl_lrmsd_backward(x, y, n_atoms, state, grad_lrmsd, grad_x, workspace, stream=None):
     B, S, three = x.shape
     if three != 3 or tuple(grad_x.shape) != (B, S, 3) or tuple(grad_lrmsd.shape) != (B,):

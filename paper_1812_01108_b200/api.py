@@ -4,15 +4,22 @@ and the LRMSD loss (§4).
     coords = backbone(angles, lengths)                  # [B, 3*Lmax, 3]
     tables = Tables(synth.load_residue_table())         # 20 residue types
     coords = fullatom(angles, restype, lengths, tables) # [B, atom_stride, 3]
-    loss = lrmsd(coords, target)                        # [B]
+    loss = lrmsd(coords, target, 3 * lengths)           # [B] (n_atoms: the chains' true atom counts)
+    coords, n_atoms = fullatom(angles, restype, lengths, tables, return_atoms=True)
+    loss = lrmsd(coords, target, n_atoms)               # full atom: padded width != atom count
     loss, coords = backbone_lrmsd(angles, target)       # fused forward + LRMSD (f1)
 
-All are ``torch.autograd.Function``s running on the current CUDA stream.  The
+All are ``torch.autograd.Function``s running on the current CUDA stream of the
+inputs' device.  Output entries past a chain's length (padding) are 0.  A chain
+with a bad length or residue type is skipped on the device and flagged in the
+workspace error word: ``default_workspace().check()`` raises on it, and with
+``TPL_CHECK=1`` (or ``api.CHECK_INPUTS = True``) every call checks (a sync).  The
 layers save their output coordinates and back-propagate from them (the rotation
 axes are bond vectors); a table without origin atoms falls back to recomputing
 from the angles.  Argument marshalling only: every step runs in libtpl.so.
 """
 import ctypes
+import os
 
 import torch
 
@@ -40,6 +47,13 @@ class Workspace:
 
 
 _workspaces = {}
+
+CHECK_INPUTS = os.environ.get("TPL_CHECK", "0") == "1"  # debug: sync + raise on flagged inputs after each call
+
+
+def _maybe_check(device):
+    if CHECK_INPUTS:
+        default_workspace(device).check()
 
 
 def default_workspace(device=None):
@@ -103,6 +117,8 @@ class Tables:
 def _lengths_for(angles, lengths):
     if lengths is None:
         return torch.full((angles.shape[0],), angles.shape[1], dtype=torch.int32, device=angles.device)
+    if not lengths.is_cuda and lengths.numel() and (int(lengths.min()) < 1 or int(lengths.max()) > angles.shape[1]):
+        raise ValueError(f"lengths must lie in [1, {angles.shape[1]}] (host check)")
     return lengths.to(device=angles.device, dtype=torch.int32).contiguous()
 
 
@@ -111,9 +127,11 @@ class BackboneFunction(torch.autograd.Function):
     def forward(ctx, angles, lengths):
         angles = angles.contiguous()
         B, Lmax, _ = angles.shape
-        coords = torch.empty((B, 3 * Lmax, 3), dtype=torch.float32, device=angles.device)
-        ws = default_workspace(angles.device).get(MODEL_BACKBONE, B, Lmax)
-        _abi.tpl_backbone_forward(angles, lengths, coords, ws)
+        coords = torch.zeros((B, 3 * Lmax, 3), dtype=torch.float32, device=angles.device)  # pads stay 0
+        with torch.cuda.device(angles.device):
+            ws = default_workspace(angles.device).get(MODEL_BACKBONE, B, Lmax)
+            _abi.tpl_backbone_forward(angles, lengths, coords, ws)
+            _maybe_check(angles.device)
         # the backward needs only the output (rotation axes are bond vectors)
         ctx.save_for_backward(coords, lengths)
         ctx.mark_non_differentiable(lengths)
@@ -124,8 +142,10 @@ class BackboneFunction(torch.autograd.Function):
         coords, lengths = ctx.saved_tensors
         B, Lmax = coords.shape[0], coords.shape[1] // 3
         grad_angles = torch.zeros((B, Lmax, 3), dtype=torch.float32, device=coords.device)  # pads stay 0
-        ws = default_workspace(coords.device).get(MODEL_BACKBONE, B, Lmax)
-        _abi.tpl_backbone_backward_from_coords(coords, lengths, grad_coords.contiguous(), grad_angles, ws)
+        with torch.cuda.device(coords.device):
+            ws = default_workspace(coords.device).get(MODEL_BACKBONE, B, Lmax)
+            _abi.tpl_backbone_backward_from_coords(coords, lengths, grad_coords.contiguous(), grad_angles, ws)
+            _maybe_check(coords.device)
         return grad_angles, None
 
 
@@ -135,8 +155,10 @@ class FullAtomFunction(torch.autograd.Function):
         angles = angles.contiguous()
         B, Lmax, _ = angles.shape
         coords = torch.zeros((B, atom_stride, 3), dtype=torch.float32, device=angles.device)
-        ws = default_workspace(angles.device).get(MODEL_FULLATOM, B, Lmax)
-        _abi.tpl_fullatom_forward(tables.handle, angles, restype, lengths, coords, ws)
+        with torch.cuda.device(angles.device):
+            ws = default_workspace(angles.device).get(MODEL_FULLATOM, B, Lmax)
+            _abi.tpl_fullatom_forward(tables.handle, angles, restype, lengths, coords, ws)
+            _maybe_check(angles.device)
         # tables with an atom at every frame origin back-propagate from the output
         ctx.from_coords = tables.backward_from_coords
         ctx.save_for_backward(coords if ctx.from_coords else angles, restype, lengths)
@@ -149,13 +171,15 @@ class FullAtomFunction(torch.autograd.Function):
         saved, restype, lengths = ctx.saved_tensors
         B, Lmax = restype.shape[0], ctx.Lmax
         grad_angles = torch.zeros((B, Lmax, _abi.FA_SLOTS), dtype=torch.float32, device=saved.device)
-        ws = default_workspace(saved.device).get(MODEL_FULLATOM, B, Lmax)
-        if ctx.from_coords:
-            _abi.tpl_fullatom_backward_from_coords(ctx.tables.handle, saved, restype, lengths,
-                                                   grad_coords.contiguous(), grad_angles, ws)
-        else:
-            _abi.tpl_fullatom_backward(ctx.tables.handle, saved, restype, lengths, grad_coords.contiguous(),
-                                       grad_angles, ws)
+        with torch.cuda.device(saved.device):
+            ws = default_workspace(saved.device).get(MODEL_FULLATOM, B, Lmax)
+            if ctx.from_coords:
+                _abi.tpl_fullatom_backward_from_coords(ctx.tables.handle, saved, restype, lengths,
+                                                       grad_coords.contiguous(), grad_angles, ws)
+            else:
+                _abi.tpl_fullatom_backward(ctx.tables.handle, saved, restype, lengths, grad_coords.contiguous(),
+                                           grad_angles, ws)
+            _maybe_check(saved.device)
         return grad_angles, None, None, None, None
 
 
@@ -164,14 +188,19 @@ def backbone(angles, lengths=None):
     return BackboneFunction.apply(angles, _lengths_for(angles, lengths))
 
 
-def fullatom(angles, restype, lengths, tables, atom_stride=None):
+def fullatom(angles, restype, lengths, tables, atom_stride=None, return_atoms=False):
     """angles [B, Lmax, 8], restype [B, Lmax] uint8 -> packed coords [B, atom_stride, 3].
-    atom_stride defaults to tables.atoms(...) (a host round trip); pass it to avoid the sync."""
+    atom_stride defaults to tables.atoms(...) (a host round trip); pass it to avoid the sync.
+    return_atoms=True also returns the atoms of each chain (int32 [B] on the device) -- the
+    n_atoms an LRMSD of the packed output needs (the width is padded to atom_stride)."""
     lengths = _lengths_for(angles, lengths)
     restype = restype.to(device=angles.device, dtype=torch.uint8).contiguous()
-    if atom_stride is None:
-        _, atom_stride = tables.atoms(restype, lengths)
-    return FullAtomFunction.apply(angles, restype, lengths, tables, int(atom_stride))
+    apc = None
+    if atom_stride is None or return_atoms:
+        apc, stride = tables.atoms(restype, lengths)
+        atom_stride = stride if atom_stride is None else atom_stride
+    coords = FullAtomFunction.apply(angles, restype, lengths, tables, int(atom_stride))
+    return (coords, apc.to(angles.device)) if return_atoms else coords
 
 
 class BackboneLRMSDFunction(torch.autograd.Function):
@@ -182,11 +211,13 @@ class BackboneLRMSDFunction(torch.autograd.Function):
     def forward(ctx, angles, target, lengths):
         angles, target = angles.contiguous(), target.contiguous()
         B, Lmax, _ = angles.shape
-        coords = torch.empty((B, 3 * Lmax, 3), dtype=torch.float32, device=angles.device)
-        out = torch.empty(B, dtype=torch.float32, device=angles.device)
-        state = torch.empty((B, 16), dtype=torch.float32, device=angles.device)
-        ws = default_workspace(angles.device).get(MODEL_BACKBONE, B, Lmax)
-        _abi.tpl_backbone_lrmsd_forward(angles, lengths, target, coords, out, state, ws)
+        coords = torch.zeros((B, 3 * Lmax, 3), dtype=torch.float32, device=angles.device)  # pads stay 0
+        out = torch.zeros(B, dtype=torch.float32, device=angles.device)
+        state = torch.zeros((B, 16), dtype=torch.float32, device=angles.device)
+        with torch.cuda.device(angles.device):
+            ws = default_workspace(angles.device).get(MODEL_BACKBONE, B, Lmax)
+            _abi.tpl_backbone_lrmsd_forward(angles, lengths, target, coords, out, state, ws)
+            _maybe_check(angles.device)
         ctx.save_for_backward(coords, target, lengths, state)
         ctx.mark_non_differentiable(coords)
         return out, coords
@@ -196,8 +227,10 @@ class BackboneLRMSDFunction(torch.autograd.Function):
         coords, target, lengths, state = ctx.saved_tensors
         B, Lmax = coords.shape[0], coords.shape[1] // 3
         grad_angles = torch.zeros((B, Lmax, 3), dtype=torch.float32, device=coords.device)
-        ws = default_workspace(coords.device).get(MODEL_BACKBONE, B, Lmax)
-        _abi.tpl_backbone_lrmsd_backward(coords, lengths, target, state, grad_out.contiguous(), grad_angles, ws)
+        with torch.cuda.device(coords.device):
+            ws = default_workspace(coords.device).get(MODEL_BACKBONE, B, Lmax)
+            _abi.tpl_backbone_lrmsd_backward(coords, lengths, target, state, grad_out.contiguous(), grad_angles, ws)
+            _maybe_check(coords.device)
         return grad_angles, None, None
 
 
@@ -214,10 +247,12 @@ class LRMSDFunction(torch.autograd.Function):
     def forward(ctx, x, y, n_atoms):
         x, y = x.contiguous(), y.contiguous()
         B = x.shape[0]
-        out = torch.empty(B, dtype=torch.float32, device=x.device)
-        state = torch.empty(B, 16, dtype=torch.float32, device=x.device)
-        ws = default_workspace(x.device).buf
-        _abi.tpl_lrmsd_forward(x, y, n_atoms, out, state, ws)
+        out = torch.zeros(B, dtype=torch.float32, device=x.device)
+        state = torch.zeros(B, 16, dtype=torch.float32, device=x.device)
+        with torch.cuda.device(x.device):
+            ws = default_workspace(x.device).buf
+            _abi.tpl_lrmsd_forward(x, y, n_atoms, out, state, ws)
+            _maybe_check(x.device)
         ctx.save_for_backward(x, y, n_atoms, state)
         ctx.mark_non_differentiable(n_atoms)
         return out
@@ -226,13 +261,18 @@ class LRMSDFunction(torch.autograd.Function):
     def backward(ctx, grad_out):
         x, y, n_atoms, state = ctx.saved_tensors
         grad_x = torch.zeros_like(x)
-        ws = default_workspace(x.device).buf
-        _abi.tpl_lrmsd_backward(x, y, n_atoms, state, grad_out.contiguous(), grad_x, ws)
+        with torch.cuda.device(x.device):
+            ws = default_workspace(x.device).buf
+            _abi.tpl_lrmsd_backward(x, y, n_atoms, state, grad_out.contiguous(), grad_x, ws)
+            _maybe_check(x.device)
         return grad_x, None, None
 
 
 def lrmsd(x, y, n_atoms=None):
-    """x, y [B, stride, 3] fp32 CUDA -> LRMSD [B]; differentiable in x."""
+    """x, y [B, stride, 3] fp32 CUDA -> LRMSD [B] over the first n_atoms[b] atoms; differentiable in x.
+    n_atoms defaults to the full width x.shape[1] -- right for unpadded backbone coordinates only:
+    full-atom output is padded to atom_stride (pass fullatom(..., return_atoms=True)'s counts) and
+    ragged backbone batches need 3 * lengths, or the pads enter the centroid and the rotation."""
     if n_atoms is None:
         n_atoms = torch.full((x.shape[0],), x.shape[1], dtype=torch.int32, device=x.device)
     return LRMSDFunction.apply(x, y.to(x.device), n_atoms.to(device=x.device, dtype=torch.int32).contiguous())

@@ -1707,7 +1707,7 @@ static cudaError_t launch_fwd(const BBArgs& a, cudaStream_t st) {
     static LaunchCfg cfg;
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
-    const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
+    const int grid_cap = cfg.cap_now();
     const int grid = chain_grid(a.B, grid_cap, a.Lmax);
     return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err,
                       static_cast<const float*>(a.seg_omega_prev), a.seg_agg_out, a.loss_target, a.loss_out,
@@ -1720,7 +1720,7 @@ static cudaError_t launch_bwd(const BBArgs& a, cudaStream_t st) {
     static LaunchCfg cfg;
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
-    const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
+    const int grid_cap = cfg.cap_now();
     const int grid = chain_grid(a.B, grid_cap, a.Lmax);
     return launch_pdl(k, grid, NT, sm, st, a.angles, a.lengths, a.B, a.Lmax, a.grad_coords, a.grad_angles, a.err,
                       a.ws_prefix, a.max_tiles);
@@ -1758,7 +1758,7 @@ static cudaError_t launch_bwd_xyz(const BBArgs& a, cudaStream_t st) {
     static LaunchCfg cfg;
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
-    const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
+    const int grid_cap = cfg.cap_now();
     const int grid = chain_grid(a.B, grid_cap, a.Lmax);
     return launch_pdl(k, grid, NT, sm, st, static_cast<const float*>(a.coords), a.lengths, a.B, a.Lmax,
                       LOSS ? a.loss_target : a.grad_coords, a.grad_angles, a.err, a.seg_totals, a.n_seg, a.seg,
@@ -1824,6 +1824,7 @@ static BBClShape bbxc_shape(int B, int Lmax) {
 }
 
 cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
+    if (!a.loss_state && !a.seg_totals && bbp_enabled() && bbp_backward_xyz_ok(a)) return bbp_backward_xyz_launch(a, st);
     if (a.loss_state) {  // f1 fused LRMSD: chain-serial shapes
         const BBShape l = bbx_shape(a.B, a.Lmax);
 #define TPL_BBXL(NT_, R_) \
@@ -1918,7 +1919,7 @@ static cudaError_t launch_fwd_dl(const BBArgs& a, cudaStream_t st) {
     static LaunchCfg cfg;
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
-    const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
+    const int grid_cap = cfg.cap_now();
     const int max_tiles = (a.Lmax + NT * RPT - 1) / (NT * RPT);
     const long items = long(a.B) * max_tiles;
     const int grid = int(items < grid_cap ? items : grid_cap);  // co-resident: waits only on smaller items
@@ -1934,7 +1935,7 @@ static cudaError_t launch_bwd_xyz_dl(const BBArgs& a, cudaStream_t st) {
     static LaunchCfg cfg;
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
-    const int grid_cap = cfg.cap.load(std::memory_order_relaxed);
+    const int grid_cap = cfg.cap_now();
     const int max_tiles = (a.Lmax + tile - 1) / tile;
     const long items = long(a.B) * max_tiles;
     const int grid = int(items < grid_cap ? items : grid_cap);
@@ -2011,6 +2012,8 @@ static cudaError_t dispatch_fwd_cl(const BBArgs& a, BBClShape s, cudaStream_t st
 }
 
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st) {
+    if (!a.loss_out && !a.seg_agg_out && !a.seg_omega_prev && bbp_enabled() && a.Lmax <= bbp_forward_max_L())
+        return bbp_forward_launch(a, st);
     if (a.loss_out) return a.ns == 0 ? dispatch_fwd_loss<0>(a, st) : dispatch_fwd_loss<1>(a, st);
     if (a.ns == 2) return dispatch<true, 2>(a, st);  // TPL_ORTHO=2/3: chain-per-CTA shapes only
     if (a.ns == 3) return dispatch<true, 3>(a, st);

@@ -606,39 +606,52 @@ __device__ __forceinline__ void finish_epoch(unsigned* hdr) {  // call once per 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// Host: launch with programmatic stream serialization (TPL_PDL=0 disables).
-// SMs of the current device (cached once per process).
+// Host: per-device launch state.  Everything below is keyed by the current
+// device (the C ABI enqueues on the caller's stream of the current device), so a
+// process driving several GPUs sets attributes and reads occupancy per device.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev >= 0 && dev < kMaxDevices ? dev : 0;
+}
+// SMs of the current device (cached per device).
 inline int device_sm_count() {
-    static const int sms = [] {
-        int dev = 0, n = 0;
-        cudaGetDevice(&dev);
+    static std::atomic<int> sms[kMaxDevices] = {};
+    const int dev = current_device();
+    int n = sms[dev].load(std::memory_order_relaxed);
+    if (n == 0) {
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        return n > 0 ? n : 148;
-    }();
-    return sms;
+        if (n <= 0) n = 148;
+        sms[dev].store(n, std::memory_order_relaxed);
+    }
+    return n;
 }
 
-// Per kernel instance: the dynamic shared-memory opt-in, raised monotonically to
-// the largest size requested so far, and the co-resident grid (resident CTAs per
-// SM x SMs) at that size for the persistent kernels.  Thread-safe; the attribute
-// call happens on first use of a size (outside graph capture in practice).
+// Per kernel instance and device: the dynamic shared-memory opt-in, raised
+// monotonically to the largest size requested so far, and the co-resident grid
+// (resident CTAs per SM x SMs) at that size for the persistent kernels.
+// Thread-safe; the attribute call happens on first use of a size on a device
+// (outside graph capture in practice).
 struct LaunchCfg {
-    std::atomic<size_t> smem{0};
-    std::atomic<int> cap{0};
+    std::atomic<size_t> smem[kMaxDevices] = {};
+    std::atomic<int> cap_[kMaxDevices] = {};
     std::mutex m;
+    int cap_now() const { return cap_[current_device()].load(std::memory_order_relaxed); }
 };
 template <typename K>
 inline cudaError_t ensure_launch_cfg(LaunchCfg& c, K kernel, int block, size_t smem) {
-    if (c.smem.load(std::memory_order_acquire) >= smem && smem > 0) return cudaSuccess;
+    const int dev = current_device();
+    if (c.smem[dev].load(std::memory_order_acquire) >= smem && smem > 0) return cudaSuccess;
     std::lock_guard<std::mutex> g(c.m);
-    if (c.smem.load(std::memory_order_relaxed) >= smem && smem > 0) return cudaSuccess;
+    if (c.smem[dev].load(std::memory_order_relaxed) >= smem && smem > 0) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
-    c.cap.store(per_sm * device_sm_count(), std::memory_order_relaxed);
-    c.smem.store(smem, std::memory_order_release);
+    c.cap_[dev].store(per_sm * device_sm_count(), std::memory_order_relaxed);
+    c.smem[dev].store(smem, std::memory_order_release);
     return cudaSuccess;
 }
 

@@ -59,6 +59,12 @@ bool pdl_enabled();  // capi.cu: programmatic dependent launch on (TPL_PDL != 0)
 int bb_rpt_for(int Lmax);
 int bb_tile_for(int Lmax);
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st);
+// packed.cu: two residue runs per thread in f32x2 lanes, one CTA per chain (Lmax <= bbp_forward_max_L())
+bool bbp_enabled();
+int bbp_forward_max_L();
+cudaError_t bbp_forward_launch(const BBArgs& a, cudaStream_t st);
+bool bbp_backward_xyz_ok(const BBArgs& a);
+cudaError_t bbp_backward_xyz_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st);  // a.coords is the input
 int bb_dl_max_tiles(int Lmax);

@@ -1,0 +1,711 @@
+// packed.cu -- backbone kernels with two residue runs per thread in the two
+// lanes of packed fp32 pairs (sm_100a fma.rn.f32x2 / mul.rn.f32x2), for chains
+// that fit one CTA tile (§3).
+//
+// Forward (M_i = M_{i-1} R_i): thread t owns residues
+// [2Rt, 2Rt + 2R) as two runs of R, run A = [2Rt, 2Rt + R) in the .x lanes and
+// run B = [2Rt + R, 2Rt + 2R) in the .y lanes.  Both runs are composed from the
+// identity at once -- every bond update R(alpha, theta, d) (the printed matrix
+// P:149-155, 27 flops) and every sincos is one packed instruction stream for
+// the pair, so a thread's serial chain is R residues while the block scan sees
+// 2R residues per thread.  The thread's aggregate A B enters the block-wide
+// exclusive scan of 3x4 affines (common.cuh); run A is placed with the prefix P,
+// run B with P A.  Each element keeps the rounding of the scalar kernels
+// (same operations per element, FMA contraction as written).
+//
+// Latency cuts for few chains (the 256 x 700 headline has <= 2 chains per SM):
+// the tile is bulk-loaded for Lmax residues before the chain's length is known
+// (residues past the length only influence later residues, which are never
+// stored), so the length load overlaps the whole computation; each warp
+// bulk-stores its own contiguous residues.
+#include <cstdio>
+#include <cstdlib>
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tpl {
+
+// ---------------------------------------------------------------------------
+// Packed pair of 3x4 affines (.x = run A, .y = run B).
+struct Aff2 {
+    float2 r00, r01, r02, t0;
+    float2 r10, r11, r12, t1;
+    float2 r20, r21, r22, t2;
+};
+
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// One row of M <- M R(alpha, theta, d) (common.cuh aff_bond_bb, per lane).
+template <int k>
+__device__ __forceinline__ void row_bond2(float2& m0, float2& m1, float2& m2, float2& t, float2 ca, float2 sa,
+                                          float2 msa) {
+    constexpr float ct = kBBct[k], st = kBBst[k], d = kBBd[k];
+    const float2 u = __ffma2_rn(f2(ct), m0, __fmul2_rn(f2(-st), m2));
+    const float2 w = __ffma2_rn(f2(st), m0, __fmul2_rn(f2(ct), m2));
+    const float2 n1 = __ffma2_rn(ca, m1, __fmul2_rn(sa, w));
+    const float2 n2 = __ffma2_rn(ca, w, __fmul2_rn(msa, m1));
+    t = __ffma2_rn(f2(d), u, t);
+    m0 = u;
+    m1 = n1;
+    m2 = n2;
+}
+
+template <int k>
+__device__ __forceinline__ void aff2_bond(Aff2& M, float2 ca, float2 sa) {
+    const float2 msa = make_float2(-sa.x, -sa.y);
+    row_bond2<k>(M.r00, M.r01, M.r02, M.t0, ca, sa, msa);
+    row_bond2<k>(M.r10, M.r11, M.r12, M.t1, ca, sa, msa);
+    row_bond2<k>(M.r20, M.r21, M.r22, M.t2, ca, sa, msa);
+}
+
+// M = R(alpha, theta_k, d_k) itself: the bond update applied to the identity,
+// with the same per-element results (products of one rounding each).
+template <int k>
+__device__ __forceinline__ void aff2_from_bond(Aff2& M, float2 ca, float2 sa) {
+    constexpr float ct = kBBct[k], st = kBBst[k], d = kBBd[k];
+    M.r00 = f2(ct);
+    M.r10 = f2(0.f);
+    M.r20 = f2(-st);
+    M.r01 = __fmul2_rn(sa, f2(st));
+    M.r11 = ca;
+    M.r21 = __fmul2_rn(sa, f2(ct));
+    M.r02 = __fmul2_rn(ca, f2(st));
+    M.r12 = make_float2(-sa.x, -sa.y);
+    M.r22 = __fmul2_rn(ca, f2(ct));
+    M.t0 = f2(d * ct);
+    M.t1 = f2(0.f);
+    M.t2 = f2(-(d * st));
+}
+
+__device__ __forceinline__ Aff lane_x(const Aff2& M) {
+    return Aff{M.r00.x, M.r01.x, M.r02.x, M.t0.x, M.r10.x, M.r11.x, M.r12.x, M.t1.x, M.r20.x, M.r21.x, M.r22.x, M.t2.x};
+}
+__device__ __forceinline__ Aff lane_y(const Aff2& M) {
+    return Aff{M.r00.y, M.r01.y, M.r02.y, M.t0.y, M.r10.y, M.r11.y, M.r12.y, M.t1.y, M.r20.y, M.r21.y, M.r22.y, M.t2.y};
+}
+__device__ __forceinline__ void set_lane_x(Aff2& M, const Aff& a) {
+    M.r00.x = a.r00; M.r01.x = a.r01; M.r02.x = a.r02; M.t0.x = a.t0;
+    M.r10.x = a.r10; M.r11.x = a.r11; M.r12.x = a.r12; M.t1.x = a.t1;
+    M.r20.x = a.r20; M.r21.x = a.r21; M.r22.x = a.r22; M.t2.x = a.t2;
+}
+__device__ __forceinline__ Aff2 pack2(const Aff& a, const Aff& b) {
+    Aff2 M;
+    M.r00 = make_float2(a.r00, b.r00); M.r01 = make_float2(a.r01, b.r01);
+    M.r02 = make_float2(a.r02, b.r02); M.t0 = make_float2(a.t0, b.t0);
+    M.r10 = make_float2(a.r10, b.r10); M.r11 = make_float2(a.r11, b.r11);
+    M.r12 = make_float2(a.r12, b.r12); M.t1 = make_float2(a.t1, b.t1);
+    M.r20 = make_float2(a.r20, b.r20); M.r21 = make_float2(a.r21, b.r21);
+    M.r22 = make_float2(a.r22, b.r22); M.t2 = make_float2(a.t2, b.t2);
+    return M;
+}
+
+// (x, y, z) <- M (x, y, z, 1) per lane (common.cuh apply).
+__device__ __forceinline__ void apply2(const Aff2& M, float2 x, float2 y, float2 z, float2& ox, float2& oy,
+                                       float2& oz) {
+    ox = __ffma2_rn(M.r00, x, __ffma2_rn(M.r01, y, __ffma2_rn(M.r02, z, M.t0)));
+    oy = __ffma2_rn(M.r10, x, __ffma2_rn(M.r11, y, __ffma2_rn(M.r12, z, M.t1)));
+    oz = __ffma2_rn(M.r20, x, __ffma2_rn(M.r21, y, __ffma2_rn(M.r22, z, M.t2)));
+}
+
+// Packed fast sincos: tpl_sincos_fast per lane (common.cuh), the reduction and
+// both polynomials as f32x2 operations, the quadrant fix-up per lane.
+__device__ __forceinline__ void sincos2_fast(float2 x, float2& s, float2& c, float& maxabs) {
+    const float2 jm = __ffma2_rn(x, f2(0.636619772f), f2(12582912.0f));
+    const int qx = __float_as_int(jm.x), qy = __float_as_int(jm.y);
+    const float2 j = __fadd2_rn(jm, f2(-12582912.0f));
+    float2 r = __ffma2_rn(j, f2(-1.570796371e+00f), x);
+    r = __ffma2_rn(j, f2(4.371138829e-08f), r);
+    r = __ffma2_rn(j, f2(1.715124510e-15f), r);
+    const float2 r2 = __fmul2_rn(r, r);
+    float2 sp = __ffma2_rn(__ffma2_rn(f2(-1.95152959e-4f), r2, f2(8.33216087e-3f)), r2, f2(-1.66666546e-1f));
+    sp = __ffma2_rn(__fmul2_rn(sp, r2), r, r);
+    float2 cp = __ffma2_rn(__ffma2_rn(f2(2.44331571e-5f), r2, f2(-1.38873163e-3f)), r2, f2(4.16666457e-2f));
+    cp = __ffma2_rn(__ffma2_rn(cp, r2, f2(-0.5f)), r2, f2(1.0f));
+    float snx = (qx & 1) ? cp.x : sp.x, csx = (qx & 1) ? sp.x : cp.x;
+    float sny = (qy & 1) ? cp.y : sp.y, csy = (qy & 1) ? sp.y : cp.y;
+    // sign flips as sign-bit xors (quadrant bits 1 of q and q + 1)
+    snx = __int_as_float(__float_as_int(snx) ^ ((qx & 2) << 30));
+    csx = __int_as_float(__float_as_int(csx) ^ (((qx + 1) & 2) << 30));
+    sny = __int_as_float(__float_as_int(sny) ^ ((qy & 2) << 30));
+    csy = __int_as_float(__float_as_int(csy) ^ (((qy + 1) & 2) << 30));
+    s = make_float2(snx, sny);
+    c = make_float2(csx, csy);
+    maxabs = fmaxf(maxabs, fmaxf(fabsf(x.x), fabsf(x.y)));
+}
+__device__ __forceinline__ void sincos2_slow(float2 x, float2& s, float2& c) {
+    float xs[2] = {x.x, x.y}, ss[2], cc[2];
+    tpl_sincos_n<2>(xs, ss, cc);
+    s = make_float2(ss[0], ss[1]);
+    c = make_float2(cc[0], cc[1]);
+}
+
+// N consecutive floats between registers and shared memory, as 8-byte accesses
+// where the address allows (a thread's runs sit 216 R bytes apart: 64-bit accesses
+// of a half-warp then hit distinct bank pairs).
+template <int N>
+__device__ __forceinline__ void sts_run(float* p, const float (&v)[N]) {
+    if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+#pragma unroll
+        for (int i = 0; i + 1 < N; i += 2) *reinterpret_cast<float2*>(p + i) = make_float2(v[i], v[i + 1]);
+        if (N & 1) p[N - 1] = v[N - 1];
+    } else {
+        p[0] = v[0];
+#pragma unroll
+        for (int i = 1; i + 1 < N; i += 2) *reinterpret_cast<float2*>(p + i) = make_float2(v[i], v[i + 1]);
+        if (!(N & 1)) p[N - 1] = v[N - 1];
+    }
+}
+template <int N>
+__device__ __forceinline__ void lds_run(const float* p, float (&v)[N]) {
+    if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+#pragma unroll
+        for (int i = 0; i + 1 < N; i += 2) {
+            const float2 t = *reinterpret_cast<const float2*>(p + i);
+            v[i] = t.x;
+            v[i + 1] = t.y;
+        }
+        if (N & 1) v[N - 1] = p[N - 1];
+    } else {
+        v[0] = p[0];
+#pragma unroll
+        for (int i = 1; i + 1 < N; i += 2) {
+            const float2 t = *reinterpret_cast<const float2*>(p + i);
+            v[i] = t.x;
+            v[i + 1] = t.y;
+        }
+        if (!(N & 1)) v[N - 1] = p[N - 1];
+    }
+}
+
+// Head/tail bytes of a span with plain loads by the 32 lanes of one warp.
+__device__ __forceinline__ void span_load_edges_warp(const Span& s, char* sbase, int lane) {
+    float* d = reinterpret_cast<float*>(sbase + s.mis());
+    const float* g = reinterpret_cast<const float*>(s.g);
+    const int nh = s.head >> 2, nt = s.tail() >> 2, off_t = (s.head + s.mid) >> 2;
+    for (int k = lane; k < nh + nt; k += 32) {
+        const int idx = k < nh ? k : off_t + (k - nh);
+        d[idx] = __ldg(g + idx);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Forward, one CTA per chain, NT threads x 2R residues (tile TILE = 2 R NT >= Lmax).
+template <int NT, int R, int kNS>
+__global__ void __launch_bounds__(NT, R >= 4 ? 384 / NT : 512 / NT) bbp_forward_kernel(const float* __restrict__ angles,
+                                                                             const int* __restrict__ lengths, int B,
+                                                                             int Lmax, float* __restrict__ coords,
+                                                                             unsigned* __restrict__ err) {
+    constexpr int TILE = 2 * R * NT;
+    constexpr int NW = NT / 32;
+    extern __shared__ __align__(16) char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    float* scratch = reinterpret_cast<float*>(smem + 16);             // 2 NW 12 floats
+    float* s_total = scratch + 2 * NW * 12;                            // 12 floats
+    char* s_ang_base = smem + 16 + (2 * NW * 12 + 16) * 4;             // 16 + 12 TILE bytes (+ head slack)
+    char* s_out_base = s_ang_base + ((16 + 12 * TILE + 16 + 15) & ~15);  // 16 + 36 TILE bytes
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int b = blockIdx.x;
+    TPL_STAMP(0);
+    const Span sa = make_span(angles + (size_t)b * Lmax * 3, Lmax * 12);
+    pdl_wait();     // programmatic dependent launch: nothing global is read before this
+    pdl_trigger();  // every CTA is resident: the next kernel may start launching
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_barrier_init();
+        mbar_arrive_expect_tx(bar, unsigned(sa.mid));
+        span_load_bulk(sa, s_ang_base, bar);
+    }
+    const int L = __ldg(lengths + b);  // consumed only by the store
+    span_load_edges_f32(sa, s_ang_base);
+    __syncthreads();  // barrier initialised, edges in place
+    TPL_STAMP(1);
+    mbar_wait(bar, 0);
+    TPL_STAMP(2);
+    const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis());
+
+    // ---- pass 1: runs A (.x) and B (.y) from the identity; atom positions kept
+    const int j0 = 2 * R * tid;  // first residue of run A; run B starts at j0 + R
+    float2 px[3 * R], py[3 * R], pz[3 * R];
+    Aff2 M;
+    float maxabs = 0.f;
+    auto angle = [&](int j, int k) -> float {  // omega_{j-1} (k=0), phi_j (1), psi_j (2); 0 past Lmax
+        const int idx = 3 * j + k - 1;
+        return (j < Lmax && idx >= 0) ? s_ang[idx] : 0.f;
+    };
+    auto pass1 = [&](auto slow) {
+        constexpr bool kSlow = decltype(slow)::value;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int ja = j0 + q, jb = j0 + R + q;
+            float2 c[3], s[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float2 x = make_float2(angle(ja, k), angle(jb, k));
+                if (kSlow) sincos2_slow(x, s[k], c[k]);
+                else sincos2_fast(x, s[k], c[k], maxabs);
+            }
+            if (q == 0) {
+                aff2_from_bond<0>(M, c[0], s[0]);
+                if (tid == 0) set_lane_x(M, aff_identity());  // R_0 = I (reading Q1)
+            } else {
+                aff2_bond<0>(M, c[0], s[0]);
+            }
+            px[3 * q] = M.t0; py[3 * q] = M.t1; pz[3 * q] = M.t2;
+            aff2_bond<1>(M, c[1], s[1]);
+            px[3 * q + 1] = M.t0; py[3 * q + 1] = M.t1; pz[3 * q + 1] = M.t2;
+            aff2_bond<2>(M, c[2], s[2]);
+            px[3 * q + 2] = M.t0; py[3 * q + 2] = M.t1; pz[3 * q + 2] = M.t2;
+        }
+    };
+    pass1(std::false_type{});
+    if (__any_sync(0xffffffffu, maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
+    const Aff A = lane_x(M);
+    Aff agg = aff_compose(A, lane_y(M));
+    if (kNS >= 1) aff_orthonormalize(agg);
+    TPL_STAMP(3);
+
+    // ---- block scan of the thread aggregates (carry: identity, one tile)
+    const Aff P = block_exclusive_scan<NT, kNS>(agg, aff_identity(), scratch, s_total);
+    const Aff PB = aff_compose(P, A);
+    const Aff2 P2 = pack2(P, PB);
+    TPL_STAMP(4);
+
+    // ---- pass 2: positions to the output staging (run A then run B)
+    const int ok = L >= 1 && L <= Lmax;
+    const Span so = make_span(coords + (size_t)b * 3 * Lmax * 3, (ok ? L : 0) * 36);
+    float* s_out = reinterpret_cast<float*>(s_out_base + so.mis());
+    {
+        float fa[9 * R], fb[9 * R];
+#pragma unroll
+        for (int a = 0; a < 3 * R; ++a) {
+            float2 ox, oy, oz;
+            apply2(P2, px[a], py[a], pz[a], ox, oy, oz);
+            fa[3 * a] = ox.x; fa[3 * a + 1] = oy.x; fa[3 * a + 2] = oz.x;
+            fb[3 * a] = ox.y; fb[3 * a + 1] = oy.y; fb[3 * a + 2] = oz.y;
+        }
+        sts_run<9 * R>(s_out + 9 * j0, fa);
+        sts_run<9 * R>(s_out + 9 * j0 + 9 * R, fb);
+    }
+    TPL_STAMP(5);
+    if (!ok) {
+        if (tid == 0) atomicOr(err, ERR_LENGTH);
+        return;
+    }
+    // ---- per-warp bulk stores of the warp's contiguous residues (same 16-byte phase in
+    //      shared and global memory: a warp's chunk starts 36 * 64 * R bytes apart)
+    fence_proxy_async_smem();
+    __syncwarp();
+    const int w0 = warp * 64 * R, wn = min(64 * R, L - w0);
+    if (wn > 0) {
+        const Span sw = make_span(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)w0) * 3, wn * 36);
+        const float* src = s_out + 9 * w0;
+        if (lane == 0 && sw.mid > 0) {
+            bulk_s2g(const_cast<char*>(sw.g) + sw.head, reinterpret_cast<const char*>(src) + sw.head,
+                     unsigned(sw.mid));
+            bulk_commit();
+        }
+        float* g = reinterpret_cast<float*>(const_cast<char*>(sw.g));
+        const int nh = sw.head >> 2, ntl = sw.tail() >> 2, off_t = (sw.head + sw.mid) >> 2;
+        for (int e = lane; e < nh + ntl; e += 32) {
+            const int idx = e < nh ? e : off_t + (e - nh);
+            g[idx] = src[idx];
+        }
+        TPL_STAMP(6);
+        if (lane == 0) bulk_wait_read_all();
+    }
+    TPL_STAMP(7);
+    (void)B;
+    (void)NW;
+}
+
+template <int NT, int R>
+static size_t bbp_fwd_smem() {
+    constexpr int TILE = 2 * R * NT, NW = NT / 32;
+    return 16 + (2 * NW * 12 + 16) * 4 + ((16 + 12 * TILE + 16 + 15) & ~15) + 16 + 36 * TILE + 16;
+}
+
+// TPL_BBP_MINSMEM=<bytes>: pad the packed kernels' shared memory (tuning: caps the
+// CTAs per SM, e.g. to keep early-launched dependents from piling onto idle SMs)
+static size_t bbp_min_smem() {
+    static long v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("TPL_BBP_MINSMEM");
+        v = e ? std::atol(e) : 0;
+    }
+    return size_t(v);
+}
+
+// Launch policy of the packed kernels.  With at most 2 chains per SM the step is
+// latency-bound and every kernel boundary costs ~0.8 us between the last CTA of one
+// kernel and the first of the next (tools/step_gaps.py).  These kernels are then
+// launched with programmatic stream serialization (each CTA waits on
+// griddepcontrol.wait before its first global access and triggers the next grid
+// at once), so consecutive tpl kernels overlap launch with the previous tail; and
+// their shared memory is padded so that at most ceil(B / SMs) CTAs of either
+// kernel fit on an SM -- otherwise the early-launched dependents pile onto the SMs
+// that finish first (measured: 256 x 700 step 12.4 us without PDL, 13.3 us with
+// PDL unpadded, 11.3 us with PDL padded to 2 CTAs/SM).  TPL_BBP_PDL=0 disables.
+struct BBPLaunch {
+    size_t smem;
+    bool pdl;
+};
+static BBPLaunch bbp_policy(int B, size_t smem) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("TPL_BBP_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    BBPLaunch l{std::max(smem, bbp_min_smem()), false};
+    const int sms = device_sm_count();
+    if (v == 1 && B <= 2 * sms) {
+        const int per_sm = (B + sms - 1) / sms;                         // 1 or 2
+        const size_t cap = per_sm == 1 ? 118 * 1024 : 80 * 1024;        // > 228 KB / (per_sm + 1)
+        l.smem = std::max(l.smem, cap);
+        l.pdl = true;
+    }
+    return l;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_bbp(void (*kernel)(KArgs...), int grid, int block, const BBPLaunch& l, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = l.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = l.pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+template <int NT, int R, int NS>
+static cudaError_t launch_bbp_fwd(const BBArgs& a, cudaStream_t st) {
+    auto k = bbp_forward_kernel<NT, R, NS>;
+    const BBPLaunch l = bbp_policy(a.B, bbp_fwd_smem<NT, R>());
+    static LaunchCfg cfg;
+    cudaError_t e = ensure_launch_cfg(cfg, k, NT, l.smem);
+    if (e != cudaSuccess) return e;
+    return launch_bbp(k, a.B, NT, l, st, a.angles, a.lengths, a.B, a.Lmax, a.coords, a.err);
+}
+
+// TPL_PACKED=0 disables the packed kernels (A/B against the chain-serial ones).
+bool bbp_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("TPL_PACKED");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+int bbp_forward_max_L() { return 2 * 4 * 128; }
+
+template <int NT, int R>
+static cudaError_t launch_bbp_fwd_ns(const BBArgs& a, cudaStream_t st) {
+    if (a.ns == 0) return launch_bbp_fwd<NT, R, 0>(a, st);
+    if (a.ns == 1) return launch_bbp_fwd<NT, R, 1>(a, st);
+    return launch_bbp_fwd<NT, R, 2>(a, st);
+}
+
+cudaError_t bbp_forward_launch(const BBArgs& a, cudaStream_t st) {
+    if (a.ns > 2) return cudaErrorInvalidConfiguration;
+    static int env_nt = -1, env_r = 0;  // TPL_BBP=NTxR forces a shape (tuning)
+    if (env_nt < 0) {
+        env_nt = 0;
+        if (const char* e = std::getenv("TPL_BBP")) {
+            if (std::sscanf(e, "%dx%d", &env_nt, &env_r) != 2) env_nt = 0;
+        }
+    }
+    int nt = 128, r = 4;
+    if (env_nt > 0 && 2 * env_nt * env_r >= a.Lmax) {
+        nt = env_nt;
+        r = env_r;
+    } else {
+        for (int rr = 1; rr <= 4; ++rr)
+            if (2 * 128 * rr >= a.Lmax) { r = rr; break; }
+    }
+#define TPL_BBP(NT_, R_) \
+    if (nt == NT_ && r == R_) return launch_bbp_fwd_ns<NT_, R_>(a, st);
+    TPL_BBP(128, 1) TPL_BBP(128, 2) TPL_BBP(128, 3) TPL_BBP(128, 4)
+#undef TPL_BBP
+    return cudaErrorInvalidConfiguration;
+}
+
+// ---------------------------------------------------------------------------
+// Coordinate backward (Eq. 2, via the rotation-axis identity; reading
+// Q23), one CTA per chain, runs as the forward: thread t owns residues
+// [2Rt, 2Rt + 2R), run A in the .x lanes, run B in the .y lanes.  With atoms
+// a = 3j + k (N, CA, C), S_a = sum_{b>a} g_b and T_a = sum_{b>a} (x_b - c) x g_b
+// about the chain's first atom c,
+//     dL/dalpha_a = e_a . (T_a - (x_a - c) x S_a),   e_a = unit(x_a - x_{a-1}),
+// alpha_{3j+1} = phi_j, alpha_{3j+2} = psi_j, alpha_{3j} = omega_{j-1}.
+// Pass 1 reduces (S, T) of each run (kept: x - c of every atom); one block-wide
+// exclusive suffix sum gives each run the sums of all later atoms; pass 2 walks
+// each run last to first.  omega of a thread's last residue is closed from the
+// next thread's first atom N (its own lever arm about N is zero), so every
+// thread writes only its own residues and each warp bulk-stores its residues
+// without a block barrier.  The tile is loaded in one TMA piece per warp (each
+// warp starts on its own data), for Lmax residues before the length is known;
+// atoms past the length are zeroed in shared memory (they add nothing).
+template <int NT, int R>
+__global__ void __launch_bounds__(NT, R >= 3 ? 3 : 4) bbp_backward_xyz_kernel(const float* __restrict__ coords,
+                                                                        const int* __restrict__ lengths, int B,
+                                                                        int Lmax,
+                                                                        const float* __restrict__ grad_coords,
+                                                                        float* __restrict__ grad_angles,
+                                                                        unsigned* __restrict__ err) {
+    constexpr int TILE = 2 * R * NT;
+    constexpr int NW = NT / 32;
+    constexpr int WRES = 64 * R;                       // residues per warp
+    constexpr int XB = (16 + 36 * TILE + 16 + 15) & ~15;  // coordinate / dL/dr staging (+ slack)
+    extern __shared__ __align__(16) char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);                         // NW barriers
+    float* s_suf = reinterpret_cast<float*>(smem + 8 * NW + 8);                // 2 NW 6 + 8 floats
+    char* s_x_base = smem + ((8 * NW + 8 + (2 * NW * 6 + 8) * 4 + 15) & ~15);
+    char* s_g_base = s_x_base + XB;
+    char* s_go_base = s_g_base + XB;                                            // 16 + 12 TILE bytes
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int b = blockIdx.x;
+    TPL_STAMP(8);
+    const size_t cbase = (size_t)b * 3 * Lmax * 3;
+    const int w0 = warp * WRES;                       // the warp's first residue
+    const int wl = max(0, min(WRES, Lmax - w0));      // residues of the warp's piece (speculative: Lmax)
+    const Span sxw = make_span(coords + cbase + 9 * (size_t)w0, wl * 36);
+    const Span sgw = make_span(grad_coords + cbase + 9 * (size_t)w0, wl * 36);
+    pdl_wait();
+    pdl_trigger();
+    if (tid == 0) {
+        for (int w = 0; w < NW; ++w) mbar_init(bar + w, 1);
+        fence_barrier_init();
+        for (int w = 0; w < NW; ++w) {
+            const int r0 = w * WRES, n = max(0, min(WRES, Lmax - r0));
+            const Span px = make_span(coords + cbase + 9 * (size_t)r0, n * 36);
+            const Span pg = make_span(grad_coords + cbase + 9 * (size_t)r0, n * 36);
+            mbar_arrive_expect_tx(bar + w, unsigned(px.mid + pg.mid));
+            span_load_bulk(px, s_x_base + 36 * r0, bar + w);
+            span_load_bulk(pg, s_g_base + 36 * r0, bar + w);
+        }
+    }
+    const int L = __ldg(lengths + b);
+    const float* c0p = coords + cbase;
+    const float cx = __ldg(c0p), cy = __ldg(c0p + 1), cz = __ldg(c0p + 2);  // reference point: atom 0
+    const int mis = int(reinterpret_cast<uintptr_t>(coords + cbase) & 15);   // same for dL/dr (checked on host)
+    float* s_x = reinterpret_cast<float*>(s_x_base + mis);
+    float* s_g = reinterpret_cast<float*>(s_g_base + mis);
+    span_load_edges_warp(sxw, s_x_base + 36 * w0, lane);
+    span_load_edges_warp(sgw, s_g_base + 36 * w0, lane);
+    __syncthreads();  // barriers initialised
+    const bool ok = L >= 1 && L <= Lmax;
+    const int Lv = ok ? L : 0;
+    TPL_STAMP(9);
+    mbar_wait(bar + warp, 0);
+    // zero the warp's atoms at and past the chain's end (pads and unloaded slack)
+    {
+        const int f0 = 9 * max(Lv, w0), f1 = 9 * (w0 + WRES);
+        for (int f = f0 + lane; f < f1; f += 32) {
+            s_x[f] = 0.f;
+            s_g[f] = 0.f;
+        }
+    }
+    __syncwarp();
+    TPL_STAMP(10);
+
+    // ---- pass 1: (S, T) of runs A and B; P = x - c of every atom kept
+    const int j0 = 2 * R * tid;
+    float2 Px[3 * R], Py[3 * R], Pz[3 * R];
+    float2 S0 = f2(0.f), S1 = f2(0.f), S2 = f2(0.f), T0 = f2(0.f), T1 = f2(0.f), T2 = f2(0.f);
+    {
+        float xa[9 * R], xb[9 * R], ga[9 * R], gb[9 * R];
+        lds_run<9 * R>(s_x + 9 * j0, xa);
+        lds_run<9 * R>(s_x + 9 * j0 + 9 * R, xb);
+        lds_run<9 * R>(s_g + 9 * j0, ga);
+        lds_run<9 * R>(s_g + 9 * j0 + 9 * R, gb);
+        const float2 c2x = f2(cx), c2y = f2(cy), c2z = f2(cz);
+#pragma unroll
+        for (int i = 0; i < 3 * R; ++i) {
+            const float2 px = __fadd2_rn(make_float2(xa[3 * i], xb[3 * i]), make_float2(-c2x.x, -c2x.y));
+            const float2 py = __fadd2_rn(make_float2(xa[3 * i + 1], xb[3 * i + 1]), make_float2(-c2y.x, -c2y.y));
+            const float2 pz = __fadd2_rn(make_float2(xa[3 * i + 2], xb[3 * i + 2]), make_float2(-c2z.x, -c2z.y));
+            const float2 gx = make_float2(ga[3 * i], gb[3 * i]);
+            const float2 gy = make_float2(ga[3 * i + 1], gb[3 * i + 1]);
+            const float2 gz = make_float2(ga[3 * i + 2], gb[3 * i + 2]);
+            Px[i] = px; Py[i] = py; Pz[i] = pz;
+            S0 = __fadd2_rn(S0, gx); S1 = __fadd2_rn(S1, gy); S2 = __fadd2_rn(S2, gz);
+            T0 = __fadd2_rn(T0, __ffma2_rn(py, gz, __fmul2_rn(make_float2(-pz.x, -pz.y), gy)));
+            T1 = __fadd2_rn(T1, __ffma2_rn(pz, gx, __fmul2_rn(make_float2(-px.x, -px.y), gz)));
+            T2 = __fadd2_rn(T2, __ffma2_rn(px, gy, __fmul2_rn(make_float2(-py.x, -py.y), gx)));
+        }
+    }
+    TPL_STAMP(11);
+
+    // ---- block-wide exclusive suffix sum of the thread totals (runs A + B)
+    float v6[6] = {S0.x + S0.y, S1.x + S1.y, S2.x + S2.y, T0.x + T0.y, T1.x + T1.y, T2.x + T2.y};
+    const float zero6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float ext[6], tot6[6];
+    block_exclusive_suffix6<NT>(v6, zero6, s_suf, ext, tot6);
+    // running suffix state: lane y = after run B (= ext), lane x = after run A (= ext + run B)
+    S0 = make_float2(ext[0] + S0.y, ext[0]); S1 = make_float2(ext[1] + S1.y, ext[1]);
+    S2 = make_float2(ext[2] + S2.y, ext[2]); T0 = make_float2(ext[3] + T0.y, ext[3]);
+    T1 = make_float2(ext[4] + T1.y, ext[4]); T2 = make_float2(ext[5] + T2.y, ext[5]);
+    TPL_STAMP(12);
+
+    // ---- pass 2: runs last atom to first
+    const Span so = make_span(grad_angles + (size_t)b * Lmax * 3, Lv * 12);
+    float* s_go = reinterpret_cast<float*>(s_go_base + so.mis());
+    float oa[3 * R], ob[3 * R];  // (phi, psi, omega) of the run's residues
+    {
+        float ga[9 * R], gb[9 * R];
+        lds_run<9 * R>(s_g + 9 * j0, ga);
+        lds_run<9 * R>(s_g + 9 * j0 + 9 * R, gb);
+        // the atom before run A (previous thread's last atom; unused for atom 0 of the chain)
+        const float* xp = s_x + 9 * j0 - 3;
+        const float2 prevA = j0 > 0 ? make_float2(xp[0] - cx, 0.f) : f2(0.f);
+        const float prevAy = j0 > 0 ? xp[1] - cy : 0.f, prevAz = j0 > 0 ? xp[2] - cz : 0.f;
+#pragma unroll
+        for (int i = 3 * R - 1; i >= 0; --i) {
+            const float2 px = Px[i], py = Py[i], pz = Pz[i];
+            float2 qx, qy, qz;  // the previous atom's P
+            if (i > 0) {
+                qx = Px[i - 1]; qy = Py[i - 1]; qz = Pz[i - 1];
+            } else {
+                qx = make_float2(prevA.x, Px[3 * R - 1].x);
+                qy = make_float2(prevAy, Py[3 * R - 1].x);
+                qz = make_float2(prevAz, Pz[3 * R - 1].x);
+            }
+            const float2 ux = __fadd2_rn(px, make_float2(-qx.x, -qx.y));
+            const float2 uy = __fadd2_rn(py, make_float2(-qy.x, -qy.y));
+            const float2 uz = __fadd2_rn(pz, make_float2(-qz.x, -qz.y));
+            // c = T - P x S
+            const float2 c0 = __fadd2_rn(T0, __ffma2_rn(make_float2(-py.x, -py.y), S2, __fmul2_rn(pz, S1)));
+            const float2 c1 = __fadd2_rn(T1, __ffma2_rn(make_float2(-pz.x, -pz.y), S0, __fmul2_rn(px, S2)));
+            const float2 c2 = __fadd2_rn(T2, __ffma2_rn(make_float2(-px.x, -px.y), S1, __fmul2_rn(py, S0)));
+            const float2 uu = __ffma2_rn(ux, ux, __ffma2_rn(uy, uy, __fmul2_rn(uz, uz)));
+            const float2 uc = __ffma2_rn(ux, c0, __ffma2_rn(uy, c1, __fmul2_rn(uz, c2)));
+            const float2 gv = __fmul2_rn(uc, make_float2(rsqrtf(uu.x), rsqrtf(uu.y)));
+            const int q = i / 3, k = i - 3 * q;
+            if (k == 1) { oa[3 * q] = gv.x; ob[3 * q] = gv.y; }            // phi
+            else if (k == 2) { oa[3 * q + 1] = gv.x; ob[3 * q + 1] = gv.y; }  // psi
+            else {                                                            // omega of the residue before
+                if (q > 0) { oa[3 * (q - 1) + 2] = gv.x; ob[3 * (q - 1) + 2] = gv.y; }
+                else oa[3 * (R - 1) + 2] = gv.y;  // run B's first N closes run A's last omega
+            }
+            const float2 gx = make_float2(ga[3 * i], gb[3 * i]);
+            const float2 gy = make_float2(ga[3 * i + 1], gb[3 * i + 1]);
+            const float2 gz = make_float2(ga[3 * i + 2], gb[3 * i + 2]);
+            S0 = __fadd2_rn(S0, gx); S1 = __fadd2_rn(S1, gy); S2 = __fadd2_rn(S2, gz);
+            T0 = __fadd2_rn(T0, __ffma2_rn(py, gz, __fmul2_rn(make_float2(-pz.x, -pz.y), gy)));
+            T1 = __fadd2_rn(T1, __ffma2_rn(pz, gx, __fmul2_rn(make_float2(-px.x, -px.y), gz)));
+            T2 = __fadd2_rn(T2, __ffma2_rn(px, gy, __fmul2_rn(make_float2(-py.x, -py.y), gx)));
+        }
+        // omega of the thread's last residue jl: axis C_jl -> N_{jl+1} (next thread's first atom),
+        // sums over the atoms after the thread (ext); structural zero for the chain's last residue
+        const int jl = j0 + 2 * R - 1;
+        float wl_ = 0.f;
+        if (jl < Lv - 1) {
+            const float* xn = s_x + 9 * (jl + 1);
+            const float nx = xn[0] - cx, ny = xn[1] - cy, nz = xn[2] - cz;
+            const float ux = nx - Px[3 * R - 1].y, uy = ny - Py[3 * R - 1].y, uz = nz - Pz[3 * R - 1].y;
+            const float c0 = ext[3] - fmaf(ny, ext[2], -nz * ext[1]);
+            const float c1 = ext[4] - fmaf(nz, ext[0], -nx * ext[2]);
+            const float c2 = ext[5] - fmaf(nx, ext[1], -ny * ext[0]);
+            wl_ = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * fmaf(ux, c0, fmaf(uy, c1, uz * c2));
+        }
+        ob[3 * (R - 1) + 2] = wl_;
+        // omega_{L-1} is a structural zero wherever the chain ends inside a run
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            if (j0 + q == Lv - 1) oa[3 * q + 2] = 0.f;
+            if (j0 + R + q == Lv - 1) ob[3 * q + 2] = 0.f;
+        }
+    }
+    sts_run<3 * R>(s_go + 3 * j0, oa);
+    sts_run<3 * R>(s_go + 3 * j0 + 3 * R, ob);
+    TPL_STAMP(13);
+    if (!ok) {
+        if (tid == 0) atomicOr(err, ERR_LENGTH);
+        return;
+    }
+    // ---- per-warp bulk stores (a warp's chunk starts 12 * 64 R bytes apart: same 16-byte phase)
+    fence_proxy_async_smem();
+    __syncwarp();
+    const int wn = min(WRES, L - w0);
+    if (wn > 0) {
+        const Span sw = make_span(grad_angles + ((size_t)b * Lmax + w0) * 3, wn * 12);
+        const float* src = s_go + 3 * w0;
+        if (lane == 0 && sw.mid > 0) {
+            bulk_s2g(const_cast<char*>(sw.g) + sw.head, reinterpret_cast<const char*>(src) + sw.head,
+                     unsigned(sw.mid));
+            bulk_commit();
+        }
+        float* g = reinterpret_cast<float*>(const_cast<char*>(sw.g));
+        const int nh = sw.head >> 2, ntl = sw.tail() >> 2, off_t = (sw.head + sw.mid) >> 2;
+        for (int e = lane; e < nh + ntl; e += 32) {
+            const int idx = e < nh ? e : off_t + (e - nh);
+            g[idx] = src[idx];
+        }
+        TPL_STAMP(14);
+        if (lane == 0) bulk_wait_read_all();
+    }
+    TPL_STAMP(15);
+    (void)B;
+    (void)tot6;
+}
+
+template <int NT, int R>
+static size_t bbp_bwd_smem() {
+    constexpr int TILE = 2 * R * NT, NW = NT / 32;
+    constexpr int XB = (16 + 36 * TILE + 16 + 15) & ~15;
+    return ((8 * NW + 8 + (2 * NW * 6 + 8) * 4 + 15) & ~15) + 2 * XB + 16 + 12 * TILE + 16;
+}
+
+template <int NT, int R>
+static cudaError_t launch_bbp_bwd_xyz(const BBArgs& a, cudaStream_t st) {
+    auto k = bbp_backward_xyz_kernel<NT, R>;
+    const BBPLaunch l = bbp_policy(a.B, bbp_bwd_smem<NT, R>());
+    static LaunchCfg cfg;
+    cudaError_t e = ensure_launch_cfg(cfg, k, NT, l.smem);
+    if (e != cudaSuccess) return e;
+    return launch_bbp(k, a.B, NT, l, st, static_cast<const float*>(a.coords), a.lengths, a.B, a.Lmax,
+                      a.grad_coords, a.grad_angles, a.err);
+}
+
+// coords and dL/dr must share their 16-byte phase (the staging mirrors both at one offset)
+bool bbp_backward_xyz_ok(const BBArgs& a) {
+    return a.Lmax <= 2 * 4 * 128 &&
+           ((reinterpret_cast<uintptr_t>(a.coords) ^ reinterpret_cast<uintptr_t>(a.grad_coords)) & 15) == 0 &&
+           (size_t(a.Lmax) * 36) % 16 == 0;
+}
+
+cudaError_t bbp_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
+    static int env_r = -1;  // TPL_BBPX=R forces the residues per run (tuning)
+    if (env_r < 0) {
+        const char* e = std::getenv("TPL_BBPX");
+        env_r = e ? std::atoi(e) : 0;
+    }
+    int r = 4;
+    if (env_r > 0 && 2 * 128 * env_r >= a.Lmax) r = env_r;
+    else
+        for (int rr = 1; rr <= 4; ++rr)
+            if (2 * 128 * rr >= a.Lmax) { r = rr; break; }
+    if (r == 1) return launch_bbp_bwd_xyz<128, 1>(a, st);
+    if (r == 2) return launch_bbp_bwd_xyz<128, 2>(a, st);
+    if (r == 3) return launch_bbp_bwd_xyz<128, 3>(a, st);
+    return launch_bbp_bwd_xyz<128, 4>(a, st);
+}
+
+#ifdef TPL_PROFILE_PHASES
+// the stamp array is per translation unit: this file's copy
+extern "C" __attribute__((visibility("default"))) int tpl_debug_stamps_packed(unsigned long long* host, int n) {
+    return int(cudaMemcpyFromSymbol(host, g_tpl_stamps, sizeof(unsigned long long) * n));
+}
+#endif
+
+}  // namespace tpl

@@ -30,6 +30,7 @@ def main():
     p.add_argument("--B", type=int, default=256)
     p.add_argument("--L", type=int, default=700)
     p.add_argument("--bwd", action="store_true", help="the coordinate backward (two tiles per CTA stamped)")
+    p.add_argument("--packed", action="store_true", help="packed.cu kernels: stamps 0..7 (start, issued, landed, pass1, scan, pass2, store issued, end)")
     a = p.parse_args()
     torch.cuda.set_device(0)
     L = _abi.lib
@@ -56,7 +57,21 @@ def main():
     torch.cuda.synchronize()
     n = min(a.B, 4096)
     buf = (ctypes.c_ulonglong * (n * 16))()
-    L.tpl_debug_stamps(buf, n * 16)
+    if a.packed:
+        L.tpl_debug_stamps_packed(buf, n * 16)
+    else:
+        L.tpl_debug_stamps(buf, n * 16)
+    if a.packed:
+        names = ["start", "issued", "landed", "pass1", "scan", "pass2", "store issued", "end"]
+        st = np.array(buf, dtype=np.int64).reshape(n, 16)[:, 8:16] if a.bwd else np.array(buf, dtype=np.int64).reshape(n, 16)[:, :8]
+        st = st[(st > 0).all(axis=1)]
+        rel = st - st[:, 0].min()
+        print(f"{'bwd' if a.bwd else 'fwd'} B={a.B} L={a.L}: {len(st)} CTAs, span {rel.max() / 1e3:.2f} us")
+        for i, nm in enumerate(names):
+            step = (st[:, i] - st[:, i - 1]) if i else rel[:, 0]
+            print(f"  {nm:13s} at median {np.median(rel[:, i]) / 1e3:6.2f} us, max {rel[:, i].max() / 1e3:6.2f};"
+                  f"  phase median {np.median(step) / 1e3:6.2f} us max {step.max() / 1e3:6.2f}")
+        return
     if a.bwd:
         names = ["start", "tile A landed", "tile A pass1", "tile A scan", "tile A walk", "tile A stored",
                  "tile B landed", "tile B pass1", "tile B scan", "tile B walk", "tile B stored", "end"]
