@@ -227,9 +227,10 @@ class BackboneWork:
 
 class LossBackboneWork(BackboneWork):
     """f1: the step a structure-prediction model takes -- forward, LRMSD against a
-    target (PAPER 4), its gradient, backward -- through the fused pair
-    tpl_backbone_lrmsd_forward / _backward (no dL/dr array)."""
-    launches_per_step = 3  # forward (+ moments), per-chain eigen solve, backward
+    target (PAPER 4), its gradient, backward.  One pass: angles and the
+    target in, LRMSD and dLRMSD/dangles out (tpl_backbone_lrmsd_fused, no coordinate
+    round-trip); the backward is the chain rule's per-chain scale (tpl_chain_scale)."""
+    launches_per_step = 2  # one-pass kernel, per-chain scale
 
     def __init__(self, c, rank, world=1, strong=False):
         super().__init__(c, rank, world, strong)
@@ -241,27 +242,27 @@ class LossBackboneWork(BackboneWork):
         s["loss"] = torch.empty(self.B, device="cuda")
         s["state"] = torch.empty(self.B, 16, device="cuda")
         s["gl"] = torch.ones(self.B, device="cuda")
+        s["dlda"] = torch.zeros((self.B, self.Lmax, 3), device="cuda")
         return s
 
     def footprint(self):
-        return super().footprint() + self.B * self.Lmax * 36
+        return self.B * self.Lmax * (12 + 36 + 12 + 12)
 
     def fwd(self, s, stream=None):
         from paper_1812_01108_b200 import _abi
 
-        _abi.tpl_backbone_lrmsd_forward(s["angles"], s["lengths"], s["target"], s["coords"], s["loss"], s["state"],
-                                        s["ws"], stream)
+        _abi.tpl_backbone_lrmsd_fused(s["angles"], s["lengths"], s["target"], None, s["loss"], s["state"],
+                                      s["dlda"], s["ws"], stream)
 
     def bwd(self, s, stream=None):
         from paper_1812_01108_b200 import _abi
 
-        _abi.tpl_backbone_lrmsd_backward(s["coords"], s["lengths"], s["target"], s["state"], s["gl"], s["gang"],
-                                         s["ws"], stream)
+        _abi.tpl_chain_scale(s["dlda"], s["gl"], s["gang"], stream)
 
     def algo_bytes(self):
-        # the op's own bytes: fwd angles + target in, coords out; bwd angles + target in, dL/dangles out
+        # one pass: angles + target in, dLRMSD/dangles out; backward: read it, write dL/dangles
         r = self.residues
-        return {"fwd": r * (12 + 36 + 36), "bwd": r * (12 + 36 + 12)}
+        return {"fwd": r * (12 + 36 + 12), "bwd": r * (12 + 12)}
 
     def e2e_io(self):
         h = self.host
@@ -269,7 +270,7 @@ class LossBackboneWork(BackboneWork):
 
     def config(self):
         d = super().config()
-        d["workload"] += "; LRMSD loss vs a synthetic target, fused into the forward and backward kernels"
+        d["workload"] += "; LRMSD loss vs a synthetic target, one-pass angles -> LRMSD -> dLRMSD/dangles kernel"
         return d
 
 
@@ -638,6 +639,8 @@ def parity_leg(work, s, cfg_name, dist):
         else:
             G = oracle.backbone_backward(a64, ln, synth.numpy64(h["grad"])[idx]) if check_grad else None
         for k, L in enumerate(ln):
+            if isinstance(work, LossBackboneWork):
+                break  # the one-pass kernel writes no coordinates (checked through the loss and its gradient)
             e = float(np.abs(coords[k, : 3 * L] - X[k, : 3 * L]).max())
             if L <= 1000:
                 coord_err = max(coord_err, e)

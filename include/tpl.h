@@ -153,6 +153,31 @@ TPL_API tpl_status tpl_backbone_forward_precise(const float* angles, const int32
                                         int32_t Lmax, float* coords, void* workspace, size_t ws_bytes,
                                         void* stream);
 
+/* SURVEY f1 in one pass (PAPER §3 P:143-196 + §4, reading Q19):
+ * angles -> backbone coordinates -> LRMSD to the target y -> dLRMSD/dangles,
+ * one kernel, no coordinate round-trip through HBM.  Per chain b (3L atoms):
+ *   lrmsd[b]        the LRMSD of P:204 after optimal superposition
+ *   state[b][16]    U (9, row-major), barycentre of x (3), of y (3), 1/(3L LRMSD)
+ *                   (the layout of tpl_lrmsd_forward)
+ *   grad_angles     [B][Lmax][3] dLRMSD/d(phi, psi, omega) (not yet multiplied by
+ *                   dL/dLRMSD: see tpl_chain_scale); psi_{L-1}, omega_{L-1} = 0;
+ *                   0 for a chain whose LRMSD vanishes (the gradient is undefined)
+ *   coords          [B][3*Lmax][3] fp32 or NULL (written only when non-NULL)
+ * target [B][3*Lmax][3] fp32.  Lmax <= tpl_backbone_lrmsd_fused_max_L() (one CTA
+ * tile per chain), else TPL_ERR_SHAPE (use the two-call pair below).  Entries
+ * past lengths[b] are neither read for the sums nor written.  Device input
+ * errors as tpl_backbone_forward (chain skipped, error word set). */
+TPL_API int32_t tpl_backbone_lrmsd_fused_max_L(void);
+TPL_API tpl_status tpl_backbone_lrmsd_fused(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                            const float* target, float* coords, float* lrmsd, float* state,
+                                            float* grad_angles, void* workspace, size_t ws_bytes, void* stream);
+
+/* y[b * per_chain + i] = x[b * per_chain + i] * scale[b] for b < B, i < per_chain
+ * (device pointers): the chain rule dL/dangles = dL/dLRMSD[b] dLRMSD/dangles of
+ * the fused pass's autograd backward.  x and y may alias. */
+TPL_API tpl_status tpl_chain_scale(const float* x, const float* scale, int32_t B, int32_t per_chain, float* y,
+                                   void* stream);
+
 /* the backbone map and the LRMSD loss (PAPER §4)
  * fused: the forward also reduces, per chain, the moments of (r, y) over the
  * chain's 3L atoms against the reference y [B][3*Lmax][3] and returns

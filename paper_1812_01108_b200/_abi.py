@@ -33,6 +33,7 @@ EXPORTS = [
     "tpl_lrmsd_forward", "tpl_lrmsd_backward",
     "tpl_backbone_forward_precise", "tpl_backbone_lrmsd_forward", "tpl_backbone_lrmsd_backward", "tpl_backbone_segment_forward", "tpl_backbone_segment_place", "tpl_backbone_segment_totals",
     "tpl_backbone_segment_backward", "tpl_paper_backbone_saved_floats", "tpl_paper_backbone_forward", "tpl_paper_backbone_backward",
+    "tpl_backbone_lrmsd_fused_max_L", "tpl_backbone_lrmsd_fused", "tpl_chain_scale",
 ]
 
 
@@ -116,6 +117,12 @@ def _load():
     L.tpl_paper_backbone_forward.argtypes = [vp, vp, i32, i32, vp, vp, vp, sz, vp]
     L.tpl_paper_backbone_backward.restype = ctypes.c_int
     L.tpl_paper_backbone_backward.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, sz, vp]
+    L.tpl_backbone_lrmsd_fused_max_L.restype = i32
+    L.tpl_backbone_lrmsd_fused_max_L.argtypes = []
+    L.tpl_backbone_lrmsd_fused.restype = ctypes.c_int
+    L.tpl_backbone_lrmsd_fused.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.tpl_chain_scale.restype = ctypes.c_int
+    L.tpl_chain_scale.argtypes = [vp, vp, i32, i32, vp, vp]
     L.tpl_lrmsd_forward.restype = ctypes.c_int
     L.tpl_lrmsd_forward.argtypes = [vp, vp, vp, i32, i32, vp, vp, vp, sz, vp]
     L.tpl_lrmsd_backward.restype = ctypes.c_int
@@ -315,6 +322,37 @@ def tpl_backbone_lrmsd_forward(angles, lengths, target, coords, lrmsd, state, wo
                                           _dev(lrmsd, torch.float32, "lrmsd"), _dev(state, torch.float32, "state"),
                                           _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
                                           _stream(stream)))
+
+
+def tpl_backbone_lrmsd_fused_max_L():
+    return int(lib.tpl_backbone_lrmsd_fused_max_L())
+
+
+@_on_device
+def tpl_backbone_lrmsd_fused(angles, lengths, target, coords, lrmsd, state, grad_angles, workspace, stream=None):
+    """f1 in one pass: angles -> coords -> LRMSD -> dLRMSD/dangles (coords may be None)."""
+    B, Lmax, three = angles.shape
+    if (three != BB_SLOTS or tuple(target.shape) != (B, 3 * Lmax, 3) or tuple(lrmsd.shape) != (B,)
+            or tuple(state.shape) != (B, 16) or tuple(grad_angles.shape) != (B, Lmax, 3)
+            or (coords is not None and tuple(coords.shape) != (B, 3 * Lmax, 3))):
+        raise ValueError("shapes: angles/grad_angles [B,Lmax,3], target/coords [B,3*Lmax,3], lrmsd [B], state [B,16]")
+    c = _dev(coords, torch.float32, "coords") if coords is not None else None
+    _check(lib.tpl_backbone_lrmsd_fused(_dev(angles, torch.float32, "angles"), _dev(lengths, torch.int32, "lengths"),
+                                        B, Lmax, _dev(target, torch.float32, "target"), c,
+                                        _dev(lrmsd, torch.float32, "lrmsd"), _dev(state, torch.float32, "state"),
+                                        _dev(grad_angles, torch.float32, "grad_angles"),
+                                        _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                        _stream(stream)))
+
+
+@_on_device
+def tpl_chain_scale(x, scale, y, stream=None):
+    """y[b] = x[b] * scale[b] (per-chain scalar; x, y [B, ...] fp32)."""
+    B = x.shape[0]
+    if tuple(y.shape) != tuple(x.shape) or tuple(scale.shape) != (B,):
+        raise ValueError("shapes: x, y [B, ...], scale [B]")
+    _check(lib.tpl_chain_scale(_dev(x, torch.float32, "x"), _dev(scale, torch.float32, "scale"), B,
+                               x.numel() // max(B, 1), _dev(y, torch.float32, "y"), _stream(stream)))
 
 
 @_on_device

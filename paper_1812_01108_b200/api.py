@@ -204,26 +204,44 @@ def fullatom(angles, restype, lengths, tables, atom_stride=None, return_atoms=Fa
 
 
 class BackboneLRMSDFunction(torch.autograd.Function):
-    """f1: angles -> (LRMSD to target [B], coords) in one fused forward; the backward
-    forms dL/dr from the LRMSD state inside the coordinate backward."""
+    """f1: angles -> (LRMSD to target [B], coords).  Chains that fit one tile
+    (Lmax <= tpl_backbone_lrmsd_fused_max_L()) take the one-pass kernel: the forward
+    already computes dLRMSD/dangles (no coordinate round-trip), the backward only
+    scales it by dL/dLRMSD.  Longer chains: the fused forward + coordinate backward."""
 
     @staticmethod
-    def forward(ctx, angles, target, lengths):
+    def forward(ctx, angles, target, lengths, with_coords):
         angles, target = angles.contiguous(), target.contiguous()
         B, Lmax, _ = angles.shape
-        coords = torch.zeros((B, 3 * Lmax, 3), dtype=torch.float32, device=angles.device)  # pads stay 0
-        out = torch.zeros(B, dtype=torch.float32, device=angles.device)
-        state = torch.zeros((B, 16), dtype=torch.float32, device=angles.device)
-        with torch.cuda.device(angles.device):
-            ws = default_workspace(angles.device).get(MODEL_BACKBONE, B, Lmax)
-            _abi.tpl_backbone_lrmsd_forward(angles, lengths, target, coords, out, state, ws)
-            _maybe_check(angles.device)
-        ctx.save_for_backward(coords, target, lengths, state)
-        ctx.mark_non_differentiable(coords)
+        dev = angles.device
+        coords = torch.zeros((B, 3 * Lmax, 3), dtype=torch.float32, device=dev) if with_coords else None
+        out = torch.zeros(B, dtype=torch.float32, device=dev)
+        state = torch.zeros((B, 16), dtype=torch.float32, device=dev)
+        ctx.one_pass = Lmax <= _abi.tpl_backbone_lrmsd_fused_max_L()
+        with torch.cuda.device(dev):
+            ws = default_workspace(dev).get(MODEL_BACKBONE, B, Lmax)
+            if ctx.one_pass:
+                dlda = torch.zeros((B, Lmax, 3), dtype=torch.float32, device=dev)
+                _abi.tpl_backbone_lrmsd_fused(angles, lengths, target, coords, out, state, dlda, ws)
+                ctx.save_for_backward(dlda)
+            else:
+                if coords is None:
+                    coords = torch.zeros((B, 3 * Lmax, 3), dtype=torch.float32, device=dev)
+                _abi.tpl_backbone_lrmsd_forward(angles, lengths, target, coords, out, state, ws)
+                ctx.save_for_backward(coords, target, lengths, state)
+            _maybe_check(dev)
+        if coords is not None:
+            ctx.mark_non_differentiable(coords)
         return out, coords
 
     @staticmethod
     def backward(ctx, grad_out, _grad_coords):
+        if ctx.one_pass:
+            (dlda,) = ctx.saved_tensors
+            grad_angles = torch.empty_like(dlda)
+            with torch.cuda.device(dlda.device):
+                _abi.tpl_chain_scale(dlda, grad_out.contiguous(), grad_angles)
+            return grad_angles, None, None, None
         coords, target, lengths, state = ctx.saved_tensors
         B, Lmax = coords.shape[0], coords.shape[1] // 3
         grad_angles = torch.zeros((B, Lmax, 3), dtype=torch.float32, device=coords.device)
@@ -231,13 +249,15 @@ class BackboneLRMSDFunction(torch.autograd.Function):
             ws = default_workspace(coords.device).get(MODEL_BACKBONE, B, Lmax)
             _abi.tpl_backbone_lrmsd_backward(coords, lengths, target, state, grad_out.contiguous(), grad_angles, ws)
             _maybe_check(coords.device)
-        return grad_angles, None, None
+        return grad_angles, None, None, None
 
 
-def backbone_lrmsd(angles, target, lengths=None):
+def backbone_lrmsd(angles, target, lengths=None, with_coords=True):
     """angles [B, Lmax, 3], target [B, 3*Lmax, 3] -> (LRMSD over each chain's 3L atoms [B],
-    coords [B, 3*Lmax, 3] (not differentiable: the gradient flows through the LRMSD))."""
-    return BackboneLRMSDFunction.apply(angles, target.to(angles.device), _lengths_for(angles, lengths))
+    coords [B, 3*Lmax, 3] or None when with_coords=False (the coordinates are then never
+    written to HBM); coords are not differentiable: the gradient flows through the LRMSD)."""
+    return BackboneLRMSDFunction.apply(angles, target.to(angles.device), _lengths_for(angles, lengths),
+                                       bool(with_coords))
 
 
 class LRMSDFunction(torch.autograd.Function):

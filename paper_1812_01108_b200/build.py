@@ -16,8 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtpl.so")
-SOURCES = ["capi.cu", "backbone.cu", "fullatom.cu", "lrmsd.cu", "paper_baseline.cu", "segment.cu", "precise.cu", "packed.cu"]
-HEADERS = ["common.cuh", "kernels.h", "lrmsd_math.cuh"]
+SOURCES = ["capi.cu", "backbone.cu", "fullatom.cu", "lrmsd.cu", "paper_baseline.cu", "segment.cu", "precise.cu", "packed.cu", "fused_lrmsd.cu"]
+HEADERS = ["common.cuh", "kernels.h", "lrmsd_math.cuh", "packed.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [

@@ -283,6 +283,46 @@ tpl_status tpl_backbone_lrmsd_forward(const float* angles, const int32_t* length
     return TPL_OK;
 }
 
+int32_t tpl_backbone_lrmsd_fused_max_L(void) { return bbp_lrmsd_max_L(); }
+
+tpl_status tpl_backbone_lrmsd_fused(const float* angles, const int32_t* lengths, int32_t B, int32_t Lmax,
+                                    const float* target, float* coords, float* lrmsd, float* state,
+                                    float* grad_angles, void* workspace, size_t ws_bytes, void* stream) {
+    tpl_status s = bb_common(angles, lengths, B, Lmax, workspace, ws_bytes);
+    if (s != TPL_OK) return s;
+    if (!target || !lrmsd || !state || !grad_angles)
+        return fail(TPL_ERR_NULL, "target/lrmsd/state/grad_angles is NULL");
+    if (!aligned4(target) || (coords && !aligned4(coords)) || !aligned4(lrmsd) || !aligned4(state) ||
+        !aligned4(grad_angles))
+        return fail(TPL_ERR_ALIGN, "pointers not 4-byte aligned");
+    if (Lmax > bbp_lrmsd_max_L())
+        return fail(TPL_ERR_SHAPE, "Lmax %d > %d: use tpl_backbone_lrmsd_forward/_backward", Lmax, bbp_lrmsd_max_L());
+    BBArgs a{};
+    a.angles = angles;
+    a.lengths = lengths;
+    a.B = B;
+    a.Lmax = Lmax;
+    a.coords = coords;
+    a.err = static_cast<unsigned*>(workspace);
+    a.ns = ns_policy() >= 1 ? 1 : 0;
+    a.K = backbone_constants();
+    a.loss_target = target;
+    a.loss_out = lrmsd;
+    a.loss_state_out = state;
+    cudaError_t e = bbp_lrmsd_fused_launch(a, grad_angles, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "one-pass backbone+LRMSD launch");
+    return TPL_OK;
+}
+
+tpl_status tpl_chain_scale(const float* x, const float* scale, int32_t B, int32_t per_chain, float* y, void* stream) {
+    if (!x || !scale || !y) return fail(TPL_ERR_NULL, "x/scale/y is NULL");
+    if (B < 0 || per_chain < 0) return fail(TPL_ERR_SHAPE, "B=%d per_chain=%d", B, per_chain);
+    if (!aligned4(x) || !aligned4(scale) || !aligned4(y)) return fail(TPL_ERR_ALIGN, "pointers not 4-byte aligned");
+    cudaError_t e = chain_scale_launch(x, scale, B, per_chain, y, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "chain scale launch");
+    return TPL_OK;
+}
+
 tpl_status tpl_backbone_lrmsd_backward(const float* coords, const int32_t* lengths, int32_t B, int32_t Lmax,
                                        const float* target, const float* state, const float* grad_lrmsd,
                                        float* grad_angles, void* workspace, size_t ws_bytes, void* stream) {

@@ -65,6 +65,10 @@ int bbp_forward_max_L();
 cudaError_t bbp_forward_launch(const BBArgs& a, cudaStream_t st);
 bool bbp_backward_xyz_ok(const BBArgs& a);
 cudaError_t bbp_backward_xyz_launch(const BBArgs& a, cudaStream_t st);
+// fused_lrmsd.cu: angles -> coords -> LRMSD -> dLRMSD/dangles in one kernel
+int bbp_lrmsd_max_L();
+cudaError_t bbp_lrmsd_fused_launch(const BBArgs& a, float* grad_angles, cudaStream_t st);
+cudaError_t chain_scale_launch(const float* x, const float* s, int B, int per_chain, float* y, cudaStream_t st);
 cudaError_t bb_backward_launch(const BBArgs& a, cudaStream_t st);
 cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st);  // a.coords is the input
 int bb_dl_max_tiles(int Lmax);

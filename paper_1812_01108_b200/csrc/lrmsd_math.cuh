@@ -7,6 +7,15 @@
 
 namespace tpl {
 
+// Phase clocks of the solve (tools/micro/solve_cost.cu defines TPL_SOLVE_CLOCKS; the
+// library compiles these to nothing).
+#ifdef TPL_SOLVE_CLOCKS
+__device__ long long g_solve_clk[8];
+#define TPL_SCLK(i) (g_solve_clk[i] = clock64())
+#else
+#define TPL_SCLK(i) ((void)0)
+#endif
+
 // Largest eigenpair of a symmetric 4x4 (fp64, cyclic Jacobi).  Out of line: it is
 // only the fallback for a degenerate pair, and its dynamically indexed arrays
 // must not put the fast path on the stack.
@@ -60,9 +69,65 @@ static __device__ __noinline__ void sym4_max_eigen(double A[4][4], double* lam, 
     for (int i = 0; i < 4; ++i) q[i] = V[i][m] * sg;
 }
 
+// Reciprocals for correction terms and normalisations whose relative error only
+// needs to be small against the quantity they correct: the fp32 correctly rounded
+// reciprocal (MUFU + 2 FMA) and, where a full-precision value is needed, one fp64
+// Newton step on it (instead of the ~100-cycle IEEE fp64 division / sqrt sequences;
+// 20 of those made the per-chain solve ~5000 cycles, tools/micro/solve_cost.cu).
+static __device__ __forceinline__ double rcp_approx(double x) { return double(__frcp_rn(float(x))); }
+static __device__ __forceinline__ double rcp_full(double x) {
+    if (!(fabs(x) > 1e-30 && fabs(x) < 1e30)) return 1.0 / x;  // outside the fp32 range
+    const double r = rcp_approx(x);
+    return r * fma(-x, r, 2.0);  // ~1e-14 relative
+}
+static __device__ __forceinline__ double rsqrt_full(double x) {
+    if (!(x > 1e-30 && x < 1e30)) return 1.0 / sqrt(x);
+    double y = double(rsqrtf(float(x)));
+    y = y * fma(-0.5 * x * y, y, 1.5);  // Newton: ~1e-14 relative
+    return y;
+}
+
 static __device__ __forceinline__ double det3(double a, double b, double c, double d, double e, double f, double g,
                                        double h, double i) {
     return a * (e * i - f * h) - b * (d * i - f * g) + c * (d * h - e * g);
+}
+
+// Adjugate of a 4x4 through its twelve 2x2 minors of rows (0, 1) and (2, 3) (the
+// Laplace expansion used by 4x4 inverses): 72 multiplications instead of sixteen
+// 3x3 determinants; returns det as well.  adj[i][j] = (-1)^(i+j) det(a without row j, column i).
+static __device__ __forceinline__ double adj4(const double a[4][4], double b[4][4]) {
+    const double s0 = a[0][0] * a[1][1] - a[1][0] * a[0][1], s1 = a[0][0] * a[1][2] - a[1][0] * a[0][2];
+    const double s2 = a[0][0] * a[1][3] - a[1][0] * a[0][3], s3 = a[0][1] * a[1][2] - a[1][1] * a[0][2];
+    const double s4 = a[0][1] * a[1][3] - a[1][1] * a[0][3], s5 = a[0][2] * a[1][3] - a[1][2] * a[0][3];
+    const double c5 = a[2][2] * a[3][3] - a[3][2] * a[2][3], c4 = a[2][1] * a[3][3] - a[3][1] * a[2][3];
+    const double c3 = a[2][1] * a[3][2] - a[3][1] * a[2][2], c2 = a[2][0] * a[3][3] - a[3][0] * a[2][3];
+    const double c1 = a[2][0] * a[3][2] - a[3][0] * a[2][2], c0 = a[2][0] * a[3][1] - a[3][0] * a[2][1];
+    b[0][0] = a[1][1] * c5 - a[1][2] * c4 + a[1][3] * c3;
+    b[0][1] = -a[0][1] * c5 + a[0][2] * c4 - a[0][3] * c3;
+    b[0][2] = a[3][1] * s5 - a[3][2] * s4 + a[3][3] * s3;
+    b[0][3] = -a[2][1] * s5 + a[2][2] * s4 - a[2][3] * s3;
+    b[1][0] = -a[1][0] * c5 + a[1][2] * c2 - a[1][3] * c1;
+    b[1][1] = a[0][0] * c5 - a[0][2] * c2 + a[0][3] * c1;
+    b[1][2] = -a[3][0] * s5 + a[3][2] * s2 - a[3][3] * s1;
+    b[1][3] = a[2][0] * s5 - a[2][2] * s2 + a[2][3] * s1;
+    b[2][0] = a[1][0] * c4 - a[1][1] * c2 + a[1][3] * c0;
+    b[2][1] = -a[0][0] * c4 + a[0][1] * c2 - a[0][3] * c0;
+    b[2][2] = a[3][0] * s4 - a[3][1] * s2 + a[3][3] * s0;
+    b[2][3] = -a[2][0] * s4 + a[2][1] * s2 - a[2][3] * s0;
+    b[3][0] = -a[1][0] * c3 + a[1][1] * c1 - a[1][2] * c0;
+    b[3][1] = a[0][0] * c3 - a[0][1] * c1 + a[0][2] * c0;
+    b[3][2] = -a[3][0] * s3 + a[3][1] * s1 - a[3][2] * s0;
+    b[3][3] = a[2][0] * s3 - a[2][1] * s1 + a[2][2] * s0;
+    return s0 * c5 - s1 * c4 + s2 * c3 + s3 * c2 - s4 * c1 + s5 * c0;
+}
+static __device__ __forceinline__ double det4(const double a[4][4]) {
+    const double s0 = a[0][0] * a[1][1] - a[1][0] * a[0][1], s1 = a[0][0] * a[1][2] - a[1][0] * a[0][2];
+    const double s2 = a[0][0] * a[1][3] - a[1][0] * a[0][3], s3 = a[0][1] * a[1][2] - a[1][1] * a[0][2];
+    const double s4 = a[0][1] * a[1][3] - a[1][1] * a[0][3], s5 = a[0][2] * a[1][3] - a[1][2] * a[0][3];
+    const double c5 = a[2][2] * a[3][3] - a[3][2] * a[2][3], c4 = a[2][1] * a[3][3] - a[3][1] * a[2][3];
+    const double c3 = a[2][1] * a[3][2] - a[3][1] * a[2][2], c2 = a[2][0] * a[3][3] - a[3][0] * a[2][3];
+    const double c1 = a[2][0] * a[3][2] - a[3][0] * a[2][2], c0 = a[2][0] * a[3][1] - a[3][0] * a[2][1];
+    return s0 * c5 - s1 * c4 + s2 * c3 + s3 * c2 - s4 * c1 + s5 * c0;
 }
 
 // Largest eigenpair of the traceless symmetric 4x4 T of P:220-227, the fast way:
@@ -73,6 +138,7 @@ static __device__ __forceinline__ double det3(double a, double b, double c, doub
 // (adjugate ~ 0) falls back to Jacobi.  Returns false on fallback needed.
 static __device__ bool sym4_max_eigen_newton(const double T[4][4], const double R[3][3], double e0, double* lam,
                                       double q[4]) {
+    TPL_SCLK(0);
     double c2 = 0.0;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
@@ -80,53 +146,43 @@ static __device__ bool sym4_max_eigen_newton(const double T[4][4], const double 
         for (int c = 0; c < 3; ++c) c2 += R[a][c] * R[a][c];
     c2 *= -2.0;
     const double c1 = -8.0 * det3(R[0][0], R[0][1], R[0][2], R[1][0], R[1][1], R[1][2], R[2][0], R[2][1], R[2][2]);
-    // det T by cofactors along row 0
-    double c0 = 0.0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        double m[9];
-        int k = 0;
-#pragma unroll
-        for (int r = 1; r < 4; ++r)
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-                if (c != j) m[k++] = T[r][c];
-        const double mn = det3(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], m[8]);
-        c0 += ((j & 1) ? -1.0 : 1.0) * T[0][j] * mn;
+    const double c0 = det4(T);
+    // Laguerre's method in fp64: every root of T's characteristic polynomial is real,
+    // so from any point above the largest root the iteration decreases monotonically
+    // onto it with cubic order.  Start: min(e0, sqrt(3) |R|_F) -- both bound lambda_max
+    // (= s1 + s2 +- s3 in the singular values of R, <= sqrt(3 sum s^2)); the second is
+    // the tight one for a random pair (e0 >> |R|): 3-4 steps on average, at most 7 over
+    // random chain pairs, chain/cloud pairs and near-superpositions.  (An fp32 approach
+    // from e0 landed between clustered roots for chain/cloud pairs and converged to the
+    // second eigenvalue -- a wrong rotation.)
+    TPL_SCLK(1);
+    // e0 may carry fp32-level rounding (the fused kernel reduces |x~|^2, |y~|^2 in fp32)
+    // and sits within ~1e-6 of lambda_max near a perfect superposition: start 1e-5
+    // above it, and step up if the start still evaluates below the root
+    double l = fmin(e0 * (1.0 + 1e-5), sqrt(-1.5 * c2) * (1.0 + 1e-12));
+    for (int up = 0; up < 6; ++up) {
+        const double l2 = l * l;
+        if ((l2 + c2) * l2 + c1 * l + c0 > 0.0) break;
+        l *= 1.0 + 1e-4 * double(1 << (2 * up));
     }
-    // the approach from e0 in fp32 on the scaled polynomial (u = lambda / e0 in (0, 1]),
-    // where Newton from far above creeps (x3/4 per step); fp64 polishes (quadratic)
-    double l = e0;
-    if (e0 > 0.0) {
-        const double ie = 1.0 / e0;
-        const float a2 = float(c2 * ie * ie), a1 = float(c1 * ie * ie * ie), a0 = float(c0 * ie * ie * ie * ie);
-        float u = 1.f;
-        for (int it = 0; it < 80; ++it) {
-            const float u2 = u * u;
-            const float p = fmaf(fmaf(u2 + a2, u, a1), u, a0);
-            const float dp = fmaf(fmaf(4.f * u, u, 2.f * a2), u, a1);
-            if (!(dp > 0.f)) break;
-            const float nu = u - p / dp;
-            if (fabsf(nu - u) <= 2e-6f * fabsf(nu)) {
-                u = nu;
-                break;
-            }
-            u = nu;
-        }
-        l = double(u) * e0;
-    }
-    for (int it = 0; it < 8; ++it) {
+    TPL_SCLK(2);
+    for (int it = 0; it < 12; ++it) {
         const double l2 = l * l;
         const double p = (l2 + c2) * l2 + c1 * l + c0;
-        const double dp = 4.0 * l2 * l + 2.0 * c2 * l + c1;
-        if (dp == 0.0) break;
-        const double nl = l - p / dp;
-        if (fabs(nl - l) <= 1e-13 * fabs(nl)) {
-            l = nl;
-            break;
-        }
-        l = nl;
+        if (!(p > 0.0)) break;  // on the root (or just below it by rounding)
+        const double dp = (4.0 * l2 + 2.0 * c2) * l + c1;
+        const double ddp = 12.0 * l2 + 2.0 * c2;
+        const double ip = rcp_full(p);
+        const double G = dp * ip;
+        const double H = fma(-ddp, ip, G * G);
+        const double disc = 3.0 * fmax(4.0 * H - G * G, 0.0);
+        const double den = G + (disc > 0.0 ? disc * rsqrt_full(disc) : 0.0);
+        if (!(den > 0.0)) break;
+        const double step = 4.0 * rcp_full(den);
+        l -= step;
+        if (step <= 1e-14 * fabs(l)) break;
     }
+    TPL_SCLK(3);
     *lam = l;
     double M[4][4];
 #pragma unroll
@@ -134,32 +190,21 @@ static __device__ bool sym4_max_eigen_newton(const double T[4][4], const double 
 #pragma unroll
         for (int j = 0; j < 4; ++j) M[i][j] = T[i][j] - (i == j ? l : 0.0);
     // adj(M)[i][j] = (-1)^(i+j) det(M without row j, column i); keep the largest column
+    double A[4][4];
+    adj4(M, A);
     double best[4] = {0, 0, 0, 0}, bn = -1.0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        double col[4], n2 = 0.0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            double m[9];
-            int k = 0;
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                if (r == j) continue;
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    if (c != i) m[k++] = M[r][c];
-            }
-            col[i] = (((i + j) & 1) ? -1.0 : 1.0) * det3(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], m[8]);
-            n2 += col[i] * col[i];
-        }
+        const double n2 = A[0][j] * A[0][j] + A[1][j] * A[1][j] + A[2][j] * A[2][j] + A[3][j] * A[3][j];
         const bool better = n2 > bn;
         bn = better ? n2 : bn;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) best[i] = better ? col[i] : best[i];
+        for (int i = 0; i < 4; ++i) best[i] = better ? A[i][j] : best[i];
     }
+    TPL_SCLK(4);
     const double scale = fmax(fabs(l), 1e-300);
     if (!(bn > 1e-24 * scale * scale * scale * scale * scale * scale)) return false;  // degenerate: Jacobi
-    const double inv = 1.0 / sqrt(bn);
+    const double inv = rsqrt_full(bn);
     // first nonzero component > 0 (as the oracle)
     const double lead = fabs(best[0]) * inv >= 1e-12 ? best[0]
                       : fabs(best[1]) * inv >= 1e-12 ? best[1]
@@ -167,14 +212,45 @@ static __device__ bool sym4_max_eigen_newton(const double T[4][4], const double 
     const double sg = lead < 0.0 ? -inv : inv;
 #pragma unroll
     for (int i = 0; i < 4; ++i) q[i] = best[i] * sg;
+    TPL_SCLK(5);
     return true;
+}
+
+// Step 2-3 without the value: U (row-major, fp32) of the optimal superposition from
+// the centred correlation R = sum x~ y~^T (fp64) and e0 = (sum |x~|^2 + |y~|^2) / 2
+// (an upper bound of the largest eigenvalue; only the starting point of the
+// iteration).  The fused one-pass kernel computes the LRMSD itself from the
+// residuals x~ - U^T y~ (a sum of squares, no cancellation).
+static __device__ void lrmsd_rotation(const double R[3][3], double e0, float* U, float* Ulo = nullptr) {
+    double T[4][4] = {
+        {R[0][0] + R[1][1] + R[2][2], R[1][2] - R[2][1], R[2][0] - R[0][2], R[0][1] - R[1][0]},
+        {R[1][2] - R[2][1], R[0][0] - R[1][1] - R[2][2], R[0][1] + R[1][0], R[0][2] + R[2][0]},
+        {R[2][0] - R[0][2], R[0][1] + R[1][0], -R[0][0] + R[1][1] - R[2][2], R[1][2] + R[2][1]},
+        {R[0][1] - R[1][0], R[0][2] + R[2][0], R[1][2] + R[2][1], -R[0][0] - R[1][1] + R[2][2]},
+    };
+    double lam, q[4];
+    if (!sym4_max_eigen_newton(T, R, e0, &lam, q)) {
+        double A[4][4];
+        for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 4; ++j) A[i][j] = T[i][j];
+        sym4_max_eigen(A, &lam, q);
+    }
+    const double q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
+    const double Ud[9] = {q0 * q0 + q1 * q1 - q2 * q2 - q3 * q3, 2 * (q1 * q2 - q0 * q3), 2 * (q1 * q3 + q0 * q2),
+                          2 * (q1 * q2 + q0 * q3), q0 * q0 - q1 * q1 + q2 * q2 - q3 * q3, 2 * (q2 * q3 - q0 * q1),
+                          2 * (q1 * q3 - q0 * q2), 2 * (q2 * q3 + q0 * q1), q0 * q0 - q1 * q1 - q2 * q2 + q3 * q3};
+    for (int k = 0; k < 9; ++k) {
+        U[k] = float(Ud[k]);
+        if (Ulo) Ulo[k] = float(Ud[k] - double(U[k]));  // U = U + Ulo to ~1e-14
+    }
 }
 
 // Steps 2-3 for one chain from its raw fp64 moments s[17] (sum x, sum y, sum x y^T,
 // sum |x|^2, sum |y|^2) over n atoms: writes out_b = LRMSD and st_b[16] = U (9),
 // x barycentre (3), y barycentre (3), 1/(n LRMSD).
 static __device__ void lrmsd_solve(const double* s, double n, float* out_b, float* st) {
-    const double cx[3] = {s[0] / n, s[1] / n, s[2] / n}, cy[3] = {s[3] / n, s[4] / n, s[5] / n};
+    const double in = rcp_full(n);
+    const double cx[3] = {s[0] * in, s[1] * in, s[2] * in}, cy[3] = {s[3] * in, s[4] * in, s[5] * in};
     double R[3][3];  // R_ac = sum (x_a - cx_a)(y_c - cy_c) = sum x_a y_c - N cx_a cy_c
     for (int a = 0; a < 3; ++a)
         for (int c = 0; c < 3; ++c) R[a][c] = s[6 + 3 * a + c] - n * cx[a] * cy[c];
@@ -198,7 +274,7 @@ static __device__ void lrmsd_solve(const double* s, double n, float* out_b, floa
     const double U[9] = {q0 * q0 + q1 * q1 - q2 * q2 - q3 * q3, 2 * (q1 * q2 - q0 * q3), 2 * (q1 * q3 + q0 * q2),
                          2 * (q1 * q2 + q0 * q3), q0 * q0 - q1 * q1 + q2 * q2 - q3 * q3, 2 * (q2 * q3 - q0 * q1),
                          2 * (q1 * q3 - q0 * q2), 2 * (q2 * q3 + q0 * q1), q0 * q0 - q1 * q1 - q2 * q2 + q3 * q3};
-    const double e = (sxx + syy - 2.0 * lam) / n;
+    const double e = (sxx + syy - 2.0 * lam) * in;
     const double v = e > 0.0 ? sqrt(e) : 0.0;
     *out_b = float(v);
     for (int k = 0; k < 9; ++k) st[k] = float(U[k]);
@@ -207,7 +283,7 @@ static __device__ void lrmsd_solve(const double* s, double n, float* out_b, floa
         st[12 + k] = float(cy[k]);
     }
     // 1/(N LRMSD); 0 where LRMSD vanishes (the gradient is undefined there)
-    st[15] = v > 1e-12 ? float(1.0 / (n * v)) : 0.f;
+    st[15] = v > 1e-12 ? float(rcp_full(n * v)) : 0.f;
 }
 
 }  // namespace tpl

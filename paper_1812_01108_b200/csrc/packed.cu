@@ -24,171 +24,9 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "packed.cuh"
 
 namespace tpl {
-
-// ---------------------------------------------------------------------------
-// Packed pair of 3x4 affines (.x = run A, .y = run B).
-struct Aff2 {
-    float2 r00, r01, r02, t0;
-    float2 r10, r11, r12, t1;
-    float2 r20, r21, r22, t2;
-};
-
-__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
-
-// One row of M <- M R(alpha, theta, d) (common.cuh aff_bond_bb, per lane).
-template <int k>
-__device__ __forceinline__ void row_bond2(float2& m0, float2& m1, float2& m2, float2& t, float2 ca, float2 sa,
-                                          float2 msa) {
-    constexpr float ct = kBBct[k], st = kBBst[k], d = kBBd[k];
-    const float2 u = __ffma2_rn(f2(ct), m0, __fmul2_rn(f2(-st), m2));
-    const float2 w = __ffma2_rn(f2(st), m0, __fmul2_rn(f2(ct), m2));
-    const float2 n1 = __ffma2_rn(ca, m1, __fmul2_rn(sa, w));
-    const float2 n2 = __ffma2_rn(ca, w, __fmul2_rn(msa, m1));
-    t = __ffma2_rn(f2(d), u, t);
-    m0 = u;
-    m1 = n1;
-    m2 = n2;
-}
-
-template <int k>
-__device__ __forceinline__ void aff2_bond(Aff2& M, float2 ca, float2 sa) {
-    const float2 msa = make_float2(-sa.x, -sa.y);
-    row_bond2<k>(M.r00, M.r01, M.r02, M.t0, ca, sa, msa);
-    row_bond2<k>(M.r10, M.r11, M.r12, M.t1, ca, sa, msa);
-    row_bond2<k>(M.r20, M.r21, M.r22, M.t2, ca, sa, msa);
-}
-
-// M = R(alpha, theta_k, d_k) itself: the bond update applied to the identity,
-// with the same per-element results (products of one rounding each).
-template <int k>
-__device__ __forceinline__ void aff2_from_bond(Aff2& M, float2 ca, float2 sa) {
-    constexpr float ct = kBBct[k], st = kBBst[k], d = kBBd[k];
-    M.r00 = f2(ct);
-    M.r10 = f2(0.f);
-    M.r20 = f2(-st);
-    M.r01 = __fmul2_rn(sa, f2(st));
-    M.r11 = ca;
-    M.r21 = __fmul2_rn(sa, f2(ct));
-    M.r02 = __fmul2_rn(ca, f2(st));
-    M.r12 = make_float2(-sa.x, -sa.y);
-    M.r22 = __fmul2_rn(ca, f2(ct));
-    M.t0 = f2(d * ct);
-    M.t1 = f2(0.f);
-    M.t2 = f2(-(d * st));
-}
-
-__device__ __forceinline__ Aff lane_x(const Aff2& M) {
-    return Aff{M.r00.x, M.r01.x, M.r02.x, M.t0.x, M.r10.x, M.r11.x, M.r12.x, M.t1.x, M.r20.x, M.r21.x, M.r22.x, M.t2.x};
-}
-__device__ __forceinline__ Aff lane_y(const Aff2& M) {
-    return Aff{M.r00.y, M.r01.y, M.r02.y, M.t0.y, M.r10.y, M.r11.y, M.r12.y, M.t1.y, M.r20.y, M.r21.y, M.r22.y, M.t2.y};
-}
-__device__ __forceinline__ void set_lane_x(Aff2& M, const Aff& a) {
-    M.r00.x = a.r00; M.r01.x = a.r01; M.r02.x = a.r02; M.t0.x = a.t0;
-    M.r10.x = a.r10; M.r11.x = a.r11; M.r12.x = a.r12; M.t1.x = a.t1;
-    M.r20.x = a.r20; M.r21.x = a.r21; M.r22.x = a.r22; M.t2.x = a.t2;
-}
-__device__ __forceinline__ Aff2 pack2(const Aff& a, const Aff& b) {
-    Aff2 M;
-    M.r00 = make_float2(a.r00, b.r00); M.r01 = make_float2(a.r01, b.r01);
-    M.r02 = make_float2(a.r02, b.r02); M.t0 = make_float2(a.t0, b.t0);
-    M.r10 = make_float2(a.r10, b.r10); M.r11 = make_float2(a.r11, b.r11);
-    M.r12 = make_float2(a.r12, b.r12); M.t1 = make_float2(a.t1, b.t1);
-    M.r20 = make_float2(a.r20, b.r20); M.r21 = make_float2(a.r21, b.r21);
-    M.r22 = make_float2(a.r22, b.r22); M.t2 = make_float2(a.t2, b.t2);
-    return M;
-}
-
-// (x, y, z) <- M (x, y, z, 1) per lane (common.cuh apply).
-__device__ __forceinline__ void apply2(const Aff2& M, float2 x, float2 y, float2 z, float2& ox, float2& oy,
-                                       float2& oz) {
-    ox = __ffma2_rn(M.r00, x, __ffma2_rn(M.r01, y, __ffma2_rn(M.r02, z, M.t0)));
-    oy = __ffma2_rn(M.r10, x, __ffma2_rn(M.r11, y, __ffma2_rn(M.r12, z, M.t1)));
-    oz = __ffma2_rn(M.r20, x, __ffma2_rn(M.r21, y, __ffma2_rn(M.r22, z, M.t2)));
-}
-
-// Packed fast sincos: tpl_sincos_fast per lane (common.cuh), the reduction and
-// both polynomials as f32x2 operations, the quadrant fix-up per lane.
-__device__ __forceinline__ void sincos2_fast(float2 x, float2& s, float2& c, float& maxabs) {
-    const float2 jm = __ffma2_rn(x, f2(0.636619772f), f2(12582912.0f));
-    const int qx = __float_as_int(jm.x), qy = __float_as_int(jm.y);
-    const float2 j = __fadd2_rn(jm, f2(-12582912.0f));
-    float2 r = __ffma2_rn(j, f2(-1.570796371e+00f), x);
-    r = __ffma2_rn(j, f2(4.371138829e-08f), r);
-    r = __ffma2_rn(j, f2(1.715124510e-15f), r);
-    const float2 r2 = __fmul2_rn(r, r);
-    float2 sp = __ffma2_rn(__ffma2_rn(f2(-1.95152959e-4f), r2, f2(8.33216087e-3f)), r2, f2(-1.66666546e-1f));
-    sp = __ffma2_rn(__fmul2_rn(sp, r2), r, r);
-    float2 cp = __ffma2_rn(__ffma2_rn(f2(2.44331571e-5f), r2, f2(-1.38873163e-3f)), r2, f2(4.16666457e-2f));
-    cp = __ffma2_rn(__ffma2_rn(cp, r2, f2(-0.5f)), r2, f2(1.0f));
-    float snx = (qx & 1) ? cp.x : sp.x, csx = (qx & 1) ? sp.x : cp.x;
-    float sny = (qy & 1) ? cp.y : sp.y, csy = (qy & 1) ? sp.y : cp.y;
-    // sign flips as sign-bit xors (quadrant bits 1 of q and q + 1)
-    snx = __int_as_float(__float_as_int(snx) ^ ((qx & 2) << 30));
-    csx = __int_as_float(__float_as_int(csx) ^ (((qx + 1) & 2) << 30));
-    sny = __int_as_float(__float_as_int(sny) ^ ((qy & 2) << 30));
-    csy = __int_as_float(__float_as_int(csy) ^ (((qy + 1) & 2) << 30));
-    s = make_float2(snx, sny);
-    c = make_float2(csx, csy);
-    maxabs = fmaxf(maxabs, fmaxf(fabsf(x.x), fabsf(x.y)));
-}
-__device__ __forceinline__ void sincos2_slow(float2 x, float2& s, float2& c) {
-    float xs[2] = {x.x, x.y}, ss[2], cc[2];
-    tpl_sincos_n<2>(xs, ss, cc);
-    s = make_float2(ss[0], ss[1]);
-    c = make_float2(cc[0], cc[1]);
-}
-
-// N consecutive floats between registers and shared memory, as 8-byte accesses
-// where the address allows (a thread's runs sit 216 R bytes apart: 64-bit accesses
-// of a half-warp then hit distinct bank pairs).
-template <int N>
-__device__ __forceinline__ void sts_run(float* p, const float (&v)[N]) {
-    if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) {
-#pragma unroll
-        for (int i = 0; i + 1 < N; i += 2) *reinterpret_cast<float2*>(p + i) = make_float2(v[i], v[i + 1]);
-        if (N & 1) p[N - 1] = v[N - 1];
-    } else {
-        p[0] = v[0];
-#pragma unroll
-        for (int i = 1; i + 1 < N; i += 2) *reinterpret_cast<float2*>(p + i) = make_float2(v[i], v[i + 1]);
-        if (!(N & 1)) p[N - 1] = v[N - 1];
-    }
-}
-template <int N>
-__device__ __forceinline__ void lds_run(const float* p, float (&v)[N]) {
-    if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) {
-#pragma unroll
-        for (int i = 0; i + 1 < N; i += 2) {
-            const float2 t = *reinterpret_cast<const float2*>(p + i);
-            v[i] = t.x;
-            v[i + 1] = t.y;
-        }
-        if (N & 1) v[N - 1] = p[N - 1];
-    } else {
-        v[0] = p[0];
-#pragma unroll
-        for (int i = 1; i + 1 < N; i += 2) {
-            const float2 t = *reinterpret_cast<const float2*>(p + i);
-            v[i] = t.x;
-            v[i + 1] = t.y;
-        }
-        if (!(N & 1)) v[N - 1] = p[N - 1];
-    }
-}
-
-// Head/tail bytes of a span with plain loads by the 32 lanes of one warp.
-__device__ __forceinline__ void span_load_edges_warp(const Span& s, char* sbase, int lane) {
-    float* d = reinterpret_cast<float*>(sbase + s.mis());
-    const float* g = reinterpret_cast<const float*>(s.g);
-    const int nh = s.head >> 2, nt = s.tail() >> 2, off_t = (s.head + s.mid) >> 2;
-    for (int k = lane; k < nh + nt; k += 32) {
-        const int idx = k < nh ? k : off_t + (k - nh);
-        d[idx] = __ldg(g + idx);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Forward, one CTA per chain, NT threads x 2R residues (tile TILE = 2 R NT >= Lmax).
@@ -230,38 +68,7 @@ __global__ void __launch_bounds__(NT, R >= 4 ? 384 / NT : 512 / NT) bbp_forward_
     const int j0 = 2 * R * tid;  // first residue of run A; run B starts at j0 + R
     float2 px[3 * R], py[3 * R], pz[3 * R];
     Aff2 M;
-    float maxabs = 0.f;
-    auto angle = [&](int j, int k) -> float {  // omega_{j-1} (k=0), phi_j (1), psi_j (2); 0 past Lmax
-        const int idx = 3 * j + k - 1;
-        return (j < Lmax && idx >= 0) ? s_ang[idx] : 0.f;
-    };
-    auto pass1 = [&](auto slow) {
-        constexpr bool kSlow = decltype(slow)::value;
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-            const int ja = j0 + q, jb = j0 + R + q;
-            float2 c[3], s[3];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const float2 x = make_float2(angle(ja, k), angle(jb, k));
-                if (kSlow) sincos2_slow(x, s[k], c[k]);
-                else sincos2_fast(x, s[k], c[k], maxabs);
-            }
-            if (q == 0) {
-                aff2_from_bond<0>(M, c[0], s[0]);
-                if (tid == 0) set_lane_x(M, aff_identity());  // R_0 = I (reading Q1)
-            } else {
-                aff2_bond<0>(M, c[0], s[0]);
-            }
-            px[3 * q] = M.t0; py[3 * q] = M.t1; pz[3 * q] = M.t2;
-            aff2_bond<1>(M, c[1], s[1]);
-            px[3 * q + 1] = M.t0; py[3 * q + 1] = M.t1; pz[3 * q + 1] = M.t2;
-            aff2_bond<2>(M, c[2], s[2]);
-            px[3 * q + 2] = M.t0; py[3 * q + 2] = M.t1; pz[3 * q + 2] = M.t2;
-        }
-    };
-    pass1(std::false_type{});
-    if (__any_sync(0xffffffffu, maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
+    bbp_pass1<R>(s_ang, Lmax, j0, tid == 0, px, py, pz, M);
     const Aff A = lane_x(M);
     Aff agg = aff_compose(A, lane_y(M));
     if (kNS >= 1) aff_orthonormalize(agg);
@@ -294,28 +101,11 @@ __global__ void __launch_bounds__(NT, R >= 4 ? 384 / NT : 512 / NT) bbp_forward_
         if (tid == 0) atomicOr(err, ERR_LENGTH);
         return;
     }
-    // ---- per-warp bulk stores of the warp's contiguous residues (same 16-byte phase in
-    //      shared and global memory: a warp's chunk starts 36 * 64 * R bytes apart)
-    fence_proxy_async_smem();
+    // ---- per-warp stores of the warp's contiguous residues (same 16-byte phase in shared
+    //      and global memory: a warp's chunk starts 36 * 64 * R bytes apart)
     __syncwarp();
     const int w0 = warp * 64 * R, wn = min(64 * R, L - w0);
-    if (wn > 0) {
-        const Span sw = make_span(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)w0) * 3, wn * 36);
-        const float* src = s_out + 9 * w0;
-        if (lane == 0 && sw.mid > 0) {
-            bulk_s2g(const_cast<char*>(sw.g) + sw.head, reinterpret_cast<const char*>(src) + sw.head,
-                     unsigned(sw.mid));
-            bulk_commit();
-        }
-        float* g = reinterpret_cast<float*>(const_cast<char*>(sw.g));
-        const int nh = sw.head >> 2, ntl = sw.tail() >> 2, off_t = (sw.head + sw.mid) >> 2;
-        for (int e = lane; e < nh + ntl; e += 32) {
-            const int idx = e < nh ? e : off_t + (e - nh);
-            g[idx] = src[idx];
-        }
-        TPL_STAMP(6);
-        if (lane == 0) bulk_wait_read_all();
-    }
+    if (wn > 0) store_warp_chunk(coords + ((size_t)b * 3 * Lmax + 3 * (size_t)w0) * 3, s_out + 9 * w0, wn * 36, lane);
     TPL_STAMP(7);
     (void)B;
     (void)NW;
@@ -325,64 +115,6 @@ template <int NT, int R>
 static size_t bbp_fwd_smem() {
     constexpr int TILE = 2 * R * NT, NW = NT / 32;
     return 16 + (2 * NW * 12 + 16) * 4 + ((16 + 12 * TILE + 16 + 15) & ~15) + 16 + 36 * TILE + 16;
-}
-
-// TPL_BBP_MINSMEM=<bytes>: pad the packed kernels' shared memory (tuning: caps the
-// CTAs per SM, e.g. to keep early-launched dependents from piling onto idle SMs)
-static size_t bbp_min_smem() {
-    static long v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("TPL_BBP_MINSMEM");
-        v = e ? std::atol(e) : 0;
-    }
-    return size_t(v);
-}
-
-// Launch policy of the packed kernels.  With at most 2 chains per SM the step is
-// latency-bound and every kernel boundary costs ~0.8 us between the last CTA of one
-// kernel and the first of the next (tools/step_gaps.py).  These kernels are then
-// launched with programmatic stream serialization (each CTA waits on
-// griddepcontrol.wait before its first global access and triggers the next grid
-// at once), so consecutive tpl kernels overlap launch with the previous tail; and
-// their shared memory is padded so that at most ceil(B / SMs) CTAs of either
-// kernel fit on an SM -- otherwise the early-launched dependents pile onto the SMs
-// that finish first (measured: 256 x 700 step 12.4 us without PDL, 13.3 us with
-// PDL unpadded, 11.3 us with PDL padded to 2 CTAs/SM).  TPL_BBP_PDL=0 disables.
-struct BBPLaunch {
-    size_t smem;
-    bool pdl;
-};
-static BBPLaunch bbp_policy(int B, size_t smem) {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("TPL_BBP_PDL");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    BBPLaunch l{std::max(smem, bbp_min_smem()), false};
-    const int sms = device_sm_count();
-    if (v == 1 && B <= 2 * sms) {
-        const int per_sm = (B + sms - 1) / sms;                         // 1 or 2
-        const size_t cap = per_sm == 1 ? 118 * 1024 : 80 * 1024;        // > 228 KB / (per_sm + 1)
-        l.smem = std::max(l.smem, cap);
-        l.pdl = true;
-    }
-    return l;
-}
-
-template <typename... KArgs, typename... Args>
-static cudaError_t launch_bbp(void (*kernel)(KArgs...), int grid, int block, const BBPLaunch& l, cudaStream_t st,
-                              Args... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = l.smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = l.pdl ? 1 : 0;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 template <int NT, int R, int NS>
@@ -482,17 +214,12 @@ __global__ void __launch_bounds__(NT, R >= 3 ? 3 : 4) bbp_backward_xyz_kernel(co
     const Span sgw = make_span(grad_coords + cbase + 9 * (size_t)w0, wl * 36);
     pdl_wait();
     pdl_trigger();
-    if (tid == 0) {
-        for (int w = 0; w < NW; ++w) mbar_init(bar + w, 1);
+    if (lane == 0) {  // each warp initialises its own barrier and issues its own piece
+        mbar_init(bar + warp, 1);
         fence_barrier_init();
-        for (int w = 0; w < NW; ++w) {
-            const int r0 = w * WRES, n = max(0, min(WRES, Lmax - r0));
-            const Span px = make_span(coords + cbase + 9 * (size_t)r0, n * 36);
-            const Span pg = make_span(grad_coords + cbase + 9 * (size_t)r0, n * 36);
-            mbar_arrive_expect_tx(bar + w, unsigned(px.mid + pg.mid));
-            span_load_bulk(px, s_x_base + 36 * r0, bar + w);
-            span_load_bulk(pg, s_g_base + 36 * r0, bar + w);
-        }
+        mbar_arrive_expect_tx(bar + warp, unsigned(sxw.mid + sgw.mid));
+        span_load_bulk(sxw, s_x_base + 36 * w0, bar + warp);
+        span_load_bulk(sgw, s_g_base + 36 * w0, bar + warp);
     }
     const int L = __ldg(lengths + b);
     const float* c0p = coords + cbase;
@@ -502,7 +229,7 @@ __global__ void __launch_bounds__(NT, R >= 3 ? 3 : 4) bbp_backward_xyz_kernel(co
     float* s_g = reinterpret_cast<float*>(s_g_base + mis);
     span_load_edges_warp(sxw, s_x_base + 36 * w0, lane);
     span_load_edges_warp(sgw, s_g_base + 36 * w0, lane);
-    __syncthreads();  // barriers initialised
+    __syncwarp();  // the warp's barrier initialised, its edges in place
     const bool ok = L >= 1 && L <= Lmax;
     const int Lv = ok ? L : 0;
     TPL_STAMP(9);
@@ -633,27 +360,10 @@ __global__ void __launch_bounds__(NT, R >= 3 ? 3 : 4) bbp_backward_xyz_kernel(co
         if (tid == 0) atomicOr(err, ERR_LENGTH);
         return;
     }
-    // ---- per-warp bulk stores (a warp's chunk starts 12 * 64 R bytes apart: same 16-byte phase)
-    fence_proxy_async_smem();
+    // ---- per-warp stores (a warp's chunk starts 12 * 64 R bytes apart: same 16-byte phase)
     __syncwarp();
     const int wn = min(WRES, L - w0);
-    if (wn > 0) {
-        const Span sw = make_span(grad_angles + ((size_t)b * Lmax + w0) * 3, wn * 12);
-        const float* src = s_go + 3 * w0;
-        if (lane == 0 && sw.mid > 0) {
-            bulk_s2g(const_cast<char*>(sw.g) + sw.head, reinterpret_cast<const char*>(src) + sw.head,
-                     unsigned(sw.mid));
-            bulk_commit();
-        }
-        float* g = reinterpret_cast<float*>(const_cast<char*>(sw.g));
-        const int nh = sw.head >> 2, ntl = sw.tail() >> 2, off_t = (sw.head + sw.mid) >> 2;
-        for (int e = lane; e < nh + ntl; e += 32) {
-            const int idx = e < nh ? e : off_t + (e - nh);
-            g[idx] = src[idx];
-        }
-        TPL_STAMP(14);
-        if (lane == 0) bulk_wait_read_all();
-    }
+    if (wn > 0) store_warp_chunk(grad_angles + ((size_t)b * Lmax + w0) * 3, s_go + 3 * w0, wn * 12, lane);
     TPL_STAMP(15);
     (void)B;
     (void)tot6;

@@ -1,0 +1,346 @@
+// packed.cuh -- building blocks of the packed backbone kernels (packed.cu,
+// fused_lrmsd.cu): pairs of 3x4 affines in the two lanes of f32x2 registers
+// (fma.rn.f32x2 / mul.rn.f32x2 / add.rn.f32x2 on sm_100a), packed sincos, vector
+// shared-memory runs, per-warp staging I/O, and the launch policy.
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <type_traits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tpl {
+
+// ---------------------------------------------------------------------------
+// Packed pair of 3x4 affines (.x = run A, .y = run B).
+struct Aff2 {
+    float2 r00, r01, r02, t0;
+    float2 r10, r11, r12, t1;
+    float2 r20, r21, r22, t2;
+};
+
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// One row of M <- M R(alpha, theta, d) (common.cuh aff_bond_bb, per lane).
+template <int k>
+__device__ __forceinline__ void row_bond2(float2& m0, float2& m1, float2& m2, float2& t, float2 ca, float2 sa,
+                                          float2 msa) {
+    constexpr float ct = kBBct[k], st = kBBst[k], d = kBBd[k];
+    const float2 u = __ffma2_rn(f2(ct), m0, __fmul2_rn(f2(-st), m2));
+    const float2 w = __ffma2_rn(f2(st), m0, __fmul2_rn(f2(ct), m2));
+    const float2 n1 = __ffma2_rn(ca, m1, __fmul2_rn(sa, w));
+    const float2 n2 = __ffma2_rn(ca, w, __fmul2_rn(msa, m1));
+    t = __ffma2_rn(f2(d), u, t);
+    m0 = u;
+    m1 = n1;
+    m2 = n2;
+}
+
+template <int k>
+__device__ __forceinline__ void aff2_bond(Aff2& M, float2 ca, float2 sa) {
+    const float2 msa = make_float2(-sa.x, -sa.y);
+    row_bond2<k>(M.r00, M.r01, M.r02, M.t0, ca, sa, msa);
+    row_bond2<k>(M.r10, M.r11, M.r12, M.t1, ca, sa, msa);
+    row_bond2<k>(M.r20, M.r21, M.r22, M.t2, ca, sa, msa);
+}
+
+// M = R(alpha, theta_k, d_k) itself: the bond update applied to the identity,
+// with the same per-element results (products of one rounding each).
+template <int k>
+__device__ __forceinline__ void aff2_from_bond(Aff2& M, float2 ca, float2 sa) {
+    constexpr float ct = kBBct[k], st = kBBst[k], d = kBBd[k];
+    M.r00 = f2(ct);
+    M.r10 = f2(0.f);
+    M.r20 = f2(-st);
+    M.r01 = __fmul2_rn(sa, f2(st));
+    M.r11 = ca;
+    M.r21 = __fmul2_rn(sa, f2(ct));
+    M.r02 = __fmul2_rn(ca, f2(st));
+    M.r12 = make_float2(-sa.x, -sa.y);
+    M.r22 = __fmul2_rn(ca, f2(ct));
+    M.t0 = f2(d * ct);
+    M.t1 = f2(0.f);
+    M.t2 = f2(-(d * st));
+}
+
+__device__ __forceinline__ Aff lane_x(const Aff2& M) {
+    return Aff{M.r00.x, M.r01.x, M.r02.x, M.t0.x, M.r10.x, M.r11.x, M.r12.x, M.t1.x, M.r20.x, M.r21.x, M.r22.x, M.t2.x};
+}
+__device__ __forceinline__ Aff lane_y(const Aff2& M) {
+    return Aff{M.r00.y, M.r01.y, M.r02.y, M.t0.y, M.r10.y, M.r11.y, M.r12.y, M.t1.y, M.r20.y, M.r21.y, M.r22.y, M.t2.y};
+}
+__device__ __forceinline__ void set_lane_x(Aff2& M, const Aff& a) {
+    M.r00.x = a.r00; M.r01.x = a.r01; M.r02.x = a.r02; M.t0.x = a.t0;
+    M.r10.x = a.r10; M.r11.x = a.r11; M.r12.x = a.r12; M.t1.x = a.t1;
+    M.r20.x = a.r20; M.r21.x = a.r21; M.r22.x = a.r22; M.t2.x = a.t2;
+}
+__device__ __forceinline__ Aff2 pack2(const Aff& a, const Aff& b) {
+    Aff2 M;
+    M.r00 = make_float2(a.r00, b.r00); M.r01 = make_float2(a.r01, b.r01);
+    M.r02 = make_float2(a.r02, b.r02); M.t0 = make_float2(a.t0, b.t0);
+    M.r10 = make_float2(a.r10, b.r10); M.r11 = make_float2(a.r11, b.r11);
+    M.r12 = make_float2(a.r12, b.r12); M.t1 = make_float2(a.t1, b.t1);
+    M.r20 = make_float2(a.r20, b.r20); M.r21 = make_float2(a.r21, b.r21);
+    M.r22 = make_float2(a.r22, b.r22); M.t2 = make_float2(a.t2, b.t2);
+    return M;
+}
+
+// (x, y, z) <- M (x, y, z, 1) per lane (common.cuh apply).
+__device__ __forceinline__ void apply2(const Aff2& M, float2 x, float2 y, float2 z, float2& ox, float2& oy,
+                                       float2& oz) {
+    ox = __ffma2_rn(M.r00, x, __ffma2_rn(M.r01, y, __ffma2_rn(M.r02, z, M.t0)));
+    oy = __ffma2_rn(M.r10, x, __ffma2_rn(M.r11, y, __ffma2_rn(M.r12, z, M.t1)));
+    oz = __ffma2_rn(M.r20, x, __ffma2_rn(M.r21, y, __ffma2_rn(M.r22, z, M.t2)));
+}
+
+// Packed fast sincos: tpl_sincos_fast per lane (common.cuh), the reduction and
+// both polynomials as f32x2 operations, the quadrant fix-up per lane.
+__device__ __forceinline__ void sincos2_fast(float2 x, float2& s, float2& c, float& maxabs) {
+    const float2 jm = __ffma2_rn(x, f2(0.636619772f), f2(12582912.0f));
+    const int qx = __float_as_int(jm.x), qy = __float_as_int(jm.y);
+    const float2 j = __fadd2_rn(jm, f2(-12582912.0f));
+    float2 r = __ffma2_rn(j, f2(-1.570796371e+00f), x);
+    r = __ffma2_rn(j, f2(4.371138829e-08f), r);
+    r = __ffma2_rn(j, f2(1.715124510e-15f), r);
+    const float2 r2 = __fmul2_rn(r, r);
+    float2 sp = __ffma2_rn(__ffma2_rn(f2(-1.95152959e-4f), r2, f2(8.33216087e-3f)), r2, f2(-1.66666546e-1f));
+    sp = __ffma2_rn(__fmul2_rn(sp, r2), r, r);
+    float2 cp = __ffma2_rn(__ffma2_rn(f2(2.44331571e-5f), r2, f2(-1.38873163e-3f)), r2, f2(4.16666457e-2f));
+    cp = __ffma2_rn(__ffma2_rn(cp, r2, f2(-0.5f)), r2, f2(1.0f));
+    float snx = (qx & 1) ? cp.x : sp.x, csx = (qx & 1) ? sp.x : cp.x;
+    float sny = (qy & 1) ? cp.y : sp.y, csy = (qy & 1) ? sp.y : cp.y;
+    // sign flips as sign-bit xors (quadrant bits 1 of q and q + 1)
+    snx = __int_as_float(__float_as_int(snx) ^ ((qx & 2) << 30));
+    csx = __int_as_float(__float_as_int(csx) ^ (((qx + 1) & 2) << 30));
+    sny = __int_as_float(__float_as_int(sny) ^ ((qy & 2) << 30));
+    csy = __int_as_float(__float_as_int(csy) ^ (((qy + 1) & 2) << 30));
+    s = make_float2(snx, sny);
+    c = make_float2(csx, csy);
+    maxabs = fmaxf(maxabs, fmaxf(fabsf(x.x), fabsf(x.y)));
+}
+__device__ __forceinline__ void sincos2_slow(float2 x, float2& s, float2& c) {
+    float xs[2] = {x.x, x.y}, ss[2], cc[2];
+    tpl_sincos_n<2>(xs, ss, cc);
+    s = make_float2(ss[0], ss[1]);
+    c = make_float2(cc[0], cc[1]);
+}
+
+// Pass 1 of the packed forward: runs A (.x lanes, residues [j0, j0+R))
+// and B (.y lanes, [j0+R, j0+2R)) composed from the identity, the translation
+// (atom position) after every bond kept.  Angles past Lmax read as 0 (they only
+// move later residues, which are never stored); chain_start: run A begins at
+// residue 0, whose omega bond is the identity (reading Q1).  A warp holding an
+// |angle| > 2^17 redoes its runs with the exact reduction.
+template <int R>
+__device__ __forceinline__ void bbp_pass1(const float* s_ang, int Lmax, int j0, bool chain_start,
+                                          float2 (&px)[3 * R], float2 (&py)[3 * R], float2 (&pz)[3 * R], Aff2& M) {
+    float maxabs = 0.f;
+    auto angle = [&](int j, int k) -> float {  // omega_{j-1} (k=0), phi_j (1), psi_j (2); 0 past Lmax
+        const int idx = 3 * j + k - 1;
+        return (j < Lmax && idx >= 0) ? s_ang[idx] : 0.f;
+    };
+    auto pass1 = [&](auto slow) {
+        constexpr bool kSlow = decltype(slow)::value;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int ja = j0 + q, jb = j0 + R + q;
+            float2 c[3], s[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float2 x = make_float2(angle(ja, k), angle(jb, k));
+                if (kSlow) sincos2_slow(x, s[k], c[k]);
+                else sincos2_fast(x, s[k], c[k], maxabs);
+            }
+            if (q == 0) {
+                aff2_from_bond<0>(M, c[0], s[0]);
+                if (chain_start) set_lane_x(M, aff_identity());  // R_0 = I (reading Q1)
+            } else {
+                aff2_bond<0>(M, c[0], s[0]);
+            }
+            px[3 * q] = M.t0; py[3 * q] = M.t1; pz[3 * q] = M.t2;
+            aff2_bond<1>(M, c[1], s[1]);
+            px[3 * q + 1] = M.t0; py[3 * q + 1] = M.t1; pz[3 * q + 1] = M.t2;
+            aff2_bond<2>(M, c[2], s[2]);
+            px[3 * q + 2] = M.t0; py[3 * q + 2] = M.t1; pz[3 * q + 2] = M.t2;
+        }
+    };
+    pass1(std::false_type{});
+    if (__any_sync(0xffffffffu, maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
+}
+
+// Block-wide EXCLUSIVE suffix sum of N floats per thread (sum over threads > t)
+// and the block total, NT = 32 NW threads; scratch: 2 NW N + N floats.  The
+// association order is fixed (deterministic).
+template <int NT, int N>
+__device__ __forceinline__ void block_exclusive_suffix_n(const float (&v)[N], float* scratch, float (&out)[N],
+                                                         float (&total)[N]) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float inc[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) inc[k] = v[k];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            const float o = __shfl_down_sync(0xffffffffu, inc[k], d);
+            if (lane + d < 32) inc[k] += o;
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) scratch[N * warp + k] = inc[k];
+    }
+    float ex[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const float o = __shfl_down_sync(0xffffffffu, inc[k], 1);
+        ex[k] = lane == 31 ? 0.f : o;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        float later = 0.f, all = 0.f;
+#pragma unroll
+        for (int w = NW - 1; w >= 0; --w) {
+            const float t = scratch[N * w + k];
+            if (w > warp) later += t;
+            all += t;
+        }
+        out[k] = later + ex[k];
+        total[k] = all;
+    }
+    __syncthreads();
+}
+
+// N consecutive floats between registers and shared memory, as 8-byte accesses
+// where the address allows (a thread's runs sit 216 R bytes apart: 64-bit accesses
+// of a half-warp then hit distinct bank pairs).
+template <int N>
+__device__ __forceinline__ void sts_run(float* p, const float (&v)[N]) {
+    if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+#pragma unroll
+        for (int i = 0; i + 1 < N; i += 2) *reinterpret_cast<float2*>(p + i) = make_float2(v[i], v[i + 1]);
+        if (N & 1) p[N - 1] = v[N - 1];
+    } else {
+        p[0] = v[0];
+#pragma unroll
+        for (int i = 1; i + 1 < N; i += 2) *reinterpret_cast<float2*>(p + i) = make_float2(v[i], v[i + 1]);
+        if (!(N & 1)) p[N - 1] = v[N - 1];
+    }
+}
+template <int N>
+__device__ __forceinline__ void lds_run(const float* p, float (&v)[N]) {
+    if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+#pragma unroll
+        for (int i = 0; i + 1 < N; i += 2) {
+            const float2 t = *reinterpret_cast<const float2*>(p + i);
+            v[i] = t.x;
+            v[i + 1] = t.y;
+        }
+        if (N & 1) v[N - 1] = p[N - 1];
+    } else {
+        v[0] = p[0];
+#pragma unroll
+        for (int i = 1; i + 1 < N; i += 2) {
+            const float2 t = *reinterpret_cast<const float2*>(p + i);
+            v[i] = t.x;
+            v[i + 1] = t.y;
+        }
+        if (!(N & 1)) v[N - 1] = p[N - 1];
+    }
+}
+
+// Head/tail bytes of a span with plain loads by the 32 lanes of one warp.
+__device__ __forceinline__ void span_load_edges_warp(const Span& s, char* sbase, int lane) {
+    float* d = reinterpret_cast<float*>(sbase + s.mis());
+    const float* g = reinterpret_cast<const float*>(s.g);
+    const int nh = s.head >> 2, nt = s.tail() >> 2, off_t = (s.head + s.mid) >> 2;
+    for (int k = lane; k < nh + nt; k += 32) {
+        const int idx = k < nh ? k : off_t + (k - nh);
+        d[idx] = __ldg(g + idx);
+    }
+}
+
+// A warp's staged output chunk to global memory: 16-byte vector stores for the aligned
+// middle (each warp instruction writes 512 contiguous bytes), plain stores for the
+// <16-byte head and tail.  Shared and global addresses share their 16-byte phase.
+// (Measured against one cp.async.bulk store per warp: the CTA then has to wait for the
+// TMA engine to read the staging before it may exit -- 13% of the forward's warp
+// samples sat in that wait.)
+__device__ __forceinline__ void store_warp_chunk(float* gdst, const float* ssrc, int bytes, int lane) {
+    const Span sw = make_span(gdst, bytes);
+    const char* src = reinterpret_cast<const char*>(ssrc);
+    char* dst = const_cast<char*>(sw.g);
+    for (int i = lane; i < (sw.mid >> 4); i += 32) {
+        const float4 v = *reinterpret_cast<const float4*>(src + sw.head + 16 * i);
+        *reinterpret_cast<float4*>(dst + sw.head + 16 * i) = v;
+    }
+    const int nh = sw.head >> 2, ntl = sw.tail() >> 2, off_t = (sw.head + sw.mid) >> 2;
+    for (int e = lane; e < nh + ntl; e += 32) {
+        const int idx = e < nh ? e : off_t + (e - nh);
+        reinterpret_cast<float*>(dst)[idx] = ssrc[idx];
+    }
+}
+
+// TPL_BBP_MINSMEM=<bytes>: pad the packed kernels' shared memory (tuning: caps the
+// CTAs per SM, e.g. to keep early-launched dependents from piling onto idle SMs)
+inline size_t bbp_min_smem() {
+    static long v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("TPL_BBP_MINSMEM");
+        v = e ? std::atol(e) : 0;
+    }
+    return size_t(v);
+}
+
+// Launch policy of the packed kernels.  With at most 2 chains per SM the step is
+// latency-bound and every kernel boundary costs ~0.8 us between the last CTA of one
+// kernel and the first of the next (tools/step_gaps.py).  These kernels are then
+// launched with programmatic stream serialization (each CTA waits on
+// griddepcontrol.wait before its first global access and triggers the next grid
+// at once), so consecutive tpl kernels overlap launch with the previous tail; and
+// their shared memory is padded so that at most ceil(B / SMs) CTAs of either
+// kernel fit on an SM -- otherwise the early-launched dependents pile onto the SMs
+// that finish first (measured: 256 x 700 step 12.4 us without PDL, 13.3 us with
+// PDL unpadded, 11.3 us with PDL padded to 2 CTAs/SM).  TPL_BBP_PDL=0 disables.
+struct BBPLaunch {
+    size_t smem;
+    bool pdl;
+};
+inline BBPLaunch bbp_policy(int B, size_t smem) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("TPL_BBP_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    BBPLaunch l{std::max(smem, bbp_min_smem()), false};
+    const int sms = device_sm_count();
+    if (v == 1 && B <= 2 * sms) {
+        const int per_sm = (B + sms - 1) / sms;                         // 1 or 2
+        const size_t cap = per_sm == 1 ? 118 * 1024 : 80 * 1024;        // > 228 KB / (per_sm + 1)
+        l.smem = std::max(l.smem, cap);
+        l.pdl = true;
+    }
+    return l;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_bbp(void (*kernel)(KArgs...), int grid, int block, const BBPLaunch& l, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = l.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = l.pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+}  // namespace tpl

@@ -30,6 +30,7 @@ def main():
     p.add_argument("--B", type=int, default=256)
     p.add_argument("--L", type=int, default=700)
     p.add_argument("--bwd", action="store_true", help="the coordinate backward (two tiles per CTA stamped)")
+    p.add_argument("--fused", action="store_true", help="fused_lrmsd.cu one-pass kernel: stamps 0..6")
     p.add_argument("--packed", action="store_true", help="packed.cu kernels: stamps 0..7 (start, issued, landed, pass1, scan, pass2, store issued, end)")
     a = p.parse_args()
     torch.cuda.set_device(0)
@@ -42,8 +43,14 @@ def main():
     g = torch.randn(a.B, 3 * a.L, 3, device="cuda")
     ga = torch.empty(a.B, a.L, 3, device="cuda")
 
+    tgt = torch.randn(a.B, 3 * a.L, 3, device="cuda") * 20
+    st16 = torch.empty(a.B, 16, device="cuda")
+    lo = torch.empty(a.B, device="cuda")
+
     def run():
-        if a.bwd:
+        if a.fused:
+            _abi.tpl_backbone_lrmsd_fused(ang, ln, tgt, None, lo, st16, ga, ws)
+        elif a.bwd:
             _abi.tpl_backbone_backward_from_coords(c, ln, g, ga, ws)
         else:
             _abi.tpl_backbone_forward(ang, ln, c, ws)
@@ -57,6 +64,20 @@ def main():
     torch.cuda.synchronize()
     n = min(a.B, 4096)
     buf = (ctypes.c_ulonglong * (n * 16))()
+    if a.fused:
+        L.tpl_debug_stamps_fused.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        L.tpl_debug_stamps_fused(buf, n * 16)
+        names = ["start", "angles landed", "fwd done", "target landed", "M1 computed", "M1 synced", "M2 computed",
+                 "M2 synced", "solve", "bwd pass1+scan", "end"]
+        st = np.array(buf, dtype=np.int64).reshape(n, 16)[:, [0, 1, 2, 7, 8, 9, 10, 3, 4, 5, 6]]
+        st = st[(st > 0).all(axis=1)]
+        rel = st - st[:, 0].min()
+        print(f"fused B={a.B} L={a.L}: {len(st)} CTAs, span {rel.max() / 1e3:.2f} us")
+        for i, nm in enumerate(names):
+            step = (st[:, i] - st[:, i - 1]) if i else rel[:, 0]
+            print(f"  {nm:15s} at median {np.median(rel[:, i]) / 1e3:6.2f} us, max {rel[:, i].max() / 1e3:6.2f};"
+                  f"  phase median {np.median(step) / 1e3:6.2f} us max {step.max() / 1e3:6.2f}")
+        return
     if a.packed:
         L.tpl_debug_stamps_packed(buf, n * 16)
     else:
