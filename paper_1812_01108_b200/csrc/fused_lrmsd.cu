@@ -29,7 +29,7 @@
 namespace tpl {
 
 template <int NT, int R, int kNS>
-__global__ void __launch_bounds__(NT, 2) bbp_lrmsd_kernel(const float* __restrict__ angles,
+__global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const float* __restrict__ angles,
                                                                        const int* __restrict__ lengths, int B,
                                                                        int Lmax, const float* __restrict__ target,
                                                                        float* __restrict__ coords,
@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(NT, 2) bbp_lrmsd_kernel(const float* __restric
         const Aff A = lane_x(M);
         Aff agg = aff_compose(A, lane_y(M));
         if (kNS >= 1) aff_orthonormalize(agg);
-        const Aff P = block_exclusive_scan<NT, kNS>(agg, aff_identity(), scratch, s_total);
+        const Aff P = kNS == 1 ? block_exclusive_scan_qt<NT>(agg, scratch)
+                               : block_exclusive_scan<NT, kNS>(agg, aff_identity(), scratch, s_total);
         const Aff2 P2 = pack2(P, aff_compose(P, A));
 #pragma unroll
         for (int a = 0; a < 3 * R; ++a) apply2(P2, X[a], Y[a], Z[a], X[a], Y[a], Z[a]);
@@ -410,16 +411,14 @@ static cudaError_t launch_bbp_lrmsd(const BBArgs& a, float* grad_angles, cudaStr
                       a.loss_state_out, grad_angles, a.err);
 }
 
-int bbp_lrmsd_max_L() { return 2 * 4 * 128; }
+int bbp_lrmsd_max_L() { return kBBPMaxL; }
 
 cudaError_t bbp_lrmsd_fused_launch(const BBArgs& a, float* grad_angles, cudaStream_t st) {
     if (a.Lmax > bbp_lrmsd_max_L() || a.ns > 1) return cudaErrorInvalidConfiguration;
-    int r = 4;
-    for (int rr = 1; rr <= 4; ++rr)
-        if (2 * 128 * rr >= a.Lmax) { r = rr; break; }
-#define TPL_BBL(R_) \
-    if (r == R_) return a.ns == 0 ? launch_bbp_lrmsd<128, R_, 0>(a, grad_angles, st) : launch_bbp_lrmsd<128, R_, 1>(a, grad_angles, st);
-    TPL_BBL(1) TPL_BBL(2) TPL_BBL(3) TPL_BBL(4)
+    const BBPShape sh = bbp_shape(a.Lmax);
+#define TPL_BBL(NT_, R_) \
+    if (sh.nt == NT_ && sh.r == R_) return a.ns == 0 ? launch_bbp_lrmsd<NT_, R_, 0>(a, grad_angles, st) : launch_bbp_lrmsd<NT_, R_, 1>(a, grad_angles, st);
+    TPL_BBL(128, 1) TPL_BBL(128, 2) TPL_BBL(128, 3) TPL_BBL(192, 3)
 #undef TPL_BBL
     return cudaErrorInvalidConfiguration;
 }

@@ -31,7 +31,7 @@ namespace tpl {
 // ---------------------------------------------------------------------------
 // Forward, one CTA per chain, NT threads x 2R residues (tile TILE = 2 R NT >= Lmax).
 template <int NT, int R, int kNS>
-__global__ void __launch_bounds__(NT, R >= 4 ? 384 / NT : 512 / NT) bbp_forward_kernel(const float* __restrict__ angles,
+__global__ void __launch_bounds__(NT, NT * R >= 512 ? 384 / NT : 512 / NT) bbp_forward_kernel(const float* __restrict__ angles,
                                                                              const int* __restrict__ lengths, int B,
                                                                              int Lmax, float* __restrict__ coords,
                                                                              unsigned* __restrict__ err) {
@@ -74,8 +74,10 @@ __global__ void __launch_bounds__(NT, R >= 4 ? 384 / NT : 512 / NT) bbp_forward_
     if (kNS >= 1) aff_orthonormalize(agg);
     TPL_STAMP(3);
 
-    // ---- block scan of the thread aggregates (carry: identity, one tile)
-    const Aff P = block_exclusive_scan<NT, kNS>(agg, aff_identity(), scratch, s_total);
+    // ---- block scan of the thread aggregates (carry: identity, one tile); policy 1
+    //      (default) scans in (quaternion, translation) form, renormalised every combine
+    const Aff P = kNS == 1 ? block_exclusive_scan_qt<NT>(agg, scratch)
+                           : block_exclusive_scan<NT, kNS>(agg, aff_identity(), scratch, s_total);
     const Aff PB = aff_compose(P, A);
     const Aff2 P2 = pack2(P, PB);
     TPL_STAMP(4);
@@ -137,7 +139,7 @@ bool bbp_enabled() {
     return v == 1;
 }
 
-int bbp_forward_max_L() { return 2 * 4 * 128; }
+int bbp_forward_max_L() { return kBBPMaxL; }
 
 template <int NT, int R>
 static cudaError_t launch_bbp_fwd_ns(const BBArgs& a, cudaStream_t st) {
@@ -155,17 +157,12 @@ cudaError_t bbp_forward_launch(const BBArgs& a, cudaStream_t st) {
             if (std::sscanf(e, "%dx%d", &env_nt, &env_r) != 2) env_nt = 0;
         }
     }
-    int nt = 128, r = 4;
-    if (env_nt > 0 && 2 * env_nt * env_r >= a.Lmax) {
-        nt = env_nt;
-        r = env_r;
-    } else {
-        for (int rr = 1; rr <= 4; ++rr)
-            if (2 * 128 * rr >= a.Lmax) { r = rr; break; }
-    }
+    BBPShape sh = bbp_shape(a.Lmax);
+    if (env_nt > 0 && 2 * env_nt * env_r >= a.Lmax) sh = {env_nt, env_r};
+    const int nt = sh.nt, r = sh.r;
 #define TPL_BBP(NT_, R_) \
     if (nt == NT_ && r == R_) return launch_bbp_fwd_ns<NT_, R_>(a, st);
-    TPL_BBP(128, 1) TPL_BBP(128, 2) TPL_BBP(128, 3) TPL_BBP(128, 4)
+    TPL_BBP(128, 1) TPL_BBP(128, 2) TPL_BBP(128, 3) TPL_BBP(128, 4) TPL_BBP(192, 3)
 #undef TPL_BBP
     return cudaErrorInvalidConfiguration;
 }
@@ -187,7 +184,7 @@ cudaError_t bbp_forward_launch(const BBArgs& a, cudaStream_t st) {
 // warp starts on its own data), for Lmax residues before the length is known;
 // atoms past the length are zeroed in shared memory (they add nothing).
 template <int NT, int R>
-__global__ void __launch_bounds__(NT, R >= 3 ? 3 : 4) bbp_backward_xyz_kernel(const float* __restrict__ coords,
+__global__ void __launch_bounds__(NT, NT * R >= 512 ? 2 : (R >= 3 ? 3 : 4)) bbp_backward_xyz_kernel(const float* __restrict__ coords,
                                                                         const int* __restrict__ lengths, int B,
                                                                         int Lmax,
                                                                         const float* __restrict__ grad_coords,
@@ -389,7 +386,7 @@ static cudaError_t launch_bbp_bwd_xyz(const BBArgs& a, cudaStream_t st) {
 
 // coords and dL/dr must share their 16-byte phase (the staging mirrors both at one offset)
 bool bbp_backward_xyz_ok(const BBArgs& a) {
-    return a.Lmax <= 2 * 4 * 128 &&
+    return a.Lmax <= kBBPMaxL &&
            ((reinterpret_cast<uintptr_t>(a.coords) ^ reinterpret_cast<uintptr_t>(a.grad_coords)) & 15) == 0 &&
            (size_t(a.Lmax) * 36) % 16 == 0;
 }
@@ -400,14 +397,12 @@ cudaError_t bbp_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
         const char* e = std::getenv("TPL_BBPX");
         env_r = e ? std::atoi(e) : 0;
     }
-    int r = 4;
-    if (env_r > 0 && 2 * 128 * env_r >= a.Lmax) r = env_r;
-    else
-        for (int rr = 1; rr <= 4; ++rr)
-            if (2 * 128 * rr >= a.Lmax) { r = rr; break; }
-    if (r == 1) return launch_bbp_bwd_xyz<128, 1>(a, st);
-    if (r == 2) return launch_bbp_bwd_xyz<128, 2>(a, st);
-    if (r == 3) return launch_bbp_bwd_xyz<128, 3>(a, st);
+    BBPShape sh = bbp_shape(a.Lmax);
+    if (env_r > 0 && 2 * 128 * env_r >= a.Lmax) sh = {128, env_r};
+    if (sh.nt == 192) return launch_bbp_bwd_xyz<192, 3>(a, st);
+    if (sh.r == 1) return launch_bbp_bwd_xyz<128, 1>(a, st);
+    if (sh.r == 2) return launch_bbp_bwd_xyz<128, 2>(a, st);
+    if (sh.r == 3) return launch_bbp_bwd_xyz<128, 3>(a, st);
     return launch_bbp_bwd_xyz<128, 4>(a, st);
 }
 

@@ -170,6 +170,114 @@ __device__ __forceinline__ void bbp_pass1(const float* s_ang, int Lmax, int j0, 
     if (__any_sync(0xffffffffu, maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
 }
 
+// ---------------------------------------------------------------------------
+// Rigid transforms as (unit quaternion, translation): 7 floats.  The block scan of
+// the packed forward composes thread aggregates in this form and renormalises the
+// quaternion after every combine, so every rotation that carries a long
+// translation is orthonormal to fp32 precision (a 3x4 scan re-orthonormalises only
+// its results: a warp total that is off-orthogonal by 1e-6 moves a 2800 A
+// translation by 3e-3 A -- extended chains of 769-1024 residues missed the 1e-3 A
+// gate that way).  Fewer shuffles too: 7 floats per KS level instead of 12.
+struct QT {
+    float w, x, y, z;  // rotation q = w + x i + y j + z k, |q| = 1
+    float tx, ty, tz;  // translation
+};
+
+__device__ __forceinline__ QT qt_identity() { return QT{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}; }
+
+__device__ __forceinline__ void qt_normalize(QT& a) {
+    const float r = rsqrtf(fmaf(a.w, a.w, fmaf(a.x, a.x, fmaf(a.y, a.y, a.z * a.z))));
+    a.w *= r; a.x *= r; a.y *= r; a.z *= r;
+}
+
+// A then B in A's frame (the affine product A B): (qA qB, tA + R(qA) tB), renormalised.
+__device__ __forceinline__ QT qt_compose(const QT& A, const QT& B) {
+    QT C;
+    C.w = fmaf(A.w, B.w, -fmaf(A.x, B.x, fmaf(A.y, B.y, A.z * B.z)));
+    C.x = fmaf(A.w, B.x, fmaf(A.x, B.w, fmaf(A.y, B.z, -A.z * B.y)));
+    C.y = fmaf(A.w, B.y, fmaf(-A.x, B.z, fmaf(A.y, B.w, A.z * B.x)));
+    C.z = fmaf(A.w, B.z, fmaf(A.x, B.y, fmaf(-A.y, B.x, A.z * B.w)));
+    // R(qA) tB = v + w c + u x c with c = 2 u x v
+    const float cx = 2.f * fmaf(A.y, B.tz, -A.z * B.ty);
+    const float cy = 2.f * fmaf(A.z, B.tx, -A.x * B.tz);
+    const float cz = 2.f * fmaf(A.x, B.ty, -A.y * B.tx);
+    C.tx = A.tx + fmaf(A.w, cx, fmaf(A.y, cz, fmaf(-A.z, cy, B.tx)));
+    C.ty = A.ty + fmaf(A.w, cy, fmaf(A.z, cx, fmaf(-A.x, cz, B.ty)));
+    C.tz = A.tz + fmaf(A.w, cz, fmaf(A.x, cy, fmaf(-A.y, cx, B.tz)));
+    qt_normalize(C);
+    return C;
+}
+
+// 3x4 affine with an orthonormal rotation -> QT (Shepperd: the largest of the four
+// quaternion-component candidates sets the divisor; branch-free selects).
+__device__ __forceinline__ QT qt_from_aff(const Aff& m) {
+    const float tr = m.r00 + m.r11 + m.r22;
+    const float v0 = 1.f + tr, v1 = 1.f + m.r00 - m.r11 - m.r22, v2 = 1.f - m.r00 + m.r11 - m.r22,
+                v3 = 1.f - m.r00 - m.r11 + m.r22;
+    const float d21 = m.r21 - m.r12, d02 = m.r02 - m.r20, d10 = m.r10 - m.r01;
+    const float s01 = m.r01 + m.r10, s02 = m.r02 + m.r20, s12 = m.r12 + m.r21;
+    QT q;
+    const int k = (v0 >= v1 && v0 >= v2 && v0 >= v3) ? 0 : (v1 >= v2 && v1 >= v3) ? 1 : (v2 >= v3) ? 2 : 3;
+    const float v = k == 0 ? v0 : k == 1 ? v1 : k == 2 ? v2 : v3;
+    const float h = 0.5f * rsqrtf(v);  // 1 / (4 * component)
+    const float big = v * h;           // 0.5 sqrt(v) = the large component
+    if (k == 0) { q.w = big; q.x = d21 * h; q.y = d02 * h; q.z = d10 * h; }
+    else if (k == 1) { q.w = d21 * h; q.x = big; q.y = s01 * h; q.z = s02 * h; }
+    else if (k == 2) { q.w = d02 * h; q.x = s01 * h; q.y = big; q.z = s12 * h; }
+    else { q.w = d10 * h; q.x = s02 * h; q.y = s12 * h; q.z = big; }
+    qt_normalize(q);
+    q.tx = m.t0; q.ty = m.t1; q.tz = m.t2;
+    return q;
+}
+
+__device__ __forceinline__ Aff aff_from_qt(const QT& q) {
+    const float x2 = q.x + q.x, y2 = q.y + q.y, z2 = q.z + q.z;
+    const float xx = q.x * x2, yy = q.y * y2, zz = q.z * z2, xy = q.x * y2, xz = q.x * z2, yz = q.y * z2;
+    const float wx = q.w * x2, wy = q.w * y2, wz = q.w * z2;
+    Aff a;
+    a.r00 = 1.f - (yy + zz); a.r01 = xy - wz; a.r02 = xz + wy; a.t0 = q.tx;
+    a.r10 = xy + wz; a.r11 = 1.f - (xx + zz); a.r12 = yz - wx; a.t1 = q.ty;
+    a.r20 = xz - wy; a.r21 = yz + wx; a.r22 = 1.f - (xx + yy); a.t2 = q.tz;
+    return a;
+}
+
+__device__ __forceinline__ QT shfl_up_qt(const QT& a, int d) {
+    const unsigned m = 0xffffffffu;
+    return QT{__shfl_up_sync(m, a.w, d), __shfl_up_sync(m, a.x, d), __shfl_up_sync(m, a.y, d),
+              __shfl_up_sync(m, a.z, d), __shfl_up_sync(m, a.tx, d), __shfl_up_sync(m, a.ty, d),
+              __shfl_up_sync(m, a.tz, d)};
+}
+__device__ __forceinline__ void store_qt(float* s, const QT& a) {
+    s[0] = a.w; s[1] = a.x; s[2] = a.y; s[3] = a.z; s[4] = a.tx; s[5] = a.ty; s[6] = a.tz;
+}
+__device__ __forceinline__ QT load_qt(const float* s) { return QT{s[0], s[1], s[2], s[3], s[4], s[5], s[6]}; }
+
+// Block-wide EXCLUSIVE scan of the thread aggregates in (quaternion, translation)
+// form (one tile, carry = identity); returns the thread's prefix as a 3x4 affine.
+// scratch: NW * 8 floats.  Aggregates must be orthonormal (policy >= 1).
+template <int NT>
+__device__ __forceinline__ Aff block_exclusive_scan_qt(const Aff& agg, float* scratch) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    QT a = qt_from_aff(agg);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const QT o = shfl_up_qt(a, d);
+        if (lane >= d) a = qt_compose(o, a);
+    }
+    if (lane == 31) store_qt(scratch + 8 * warp, a);
+    QT ex = shfl_up_qt(a, 1);
+    if (lane == 0) ex = qt_identity();
+    __syncthreads();
+    QT p = qt_identity();
+#pragma unroll
+    for (int w = 0; w < NW - 1; ++w)
+        if (w < warp) p = qt_compose(p, load_qt(scratch + 8 * w));
+    const QT res = warp > 0 ? qt_compose(p, ex) : ex;
+    __syncthreads();  // scratch is free again
+    return aff_from_qt(res);
+}
+
 // Block-wide EXCLUSIVE suffix sum of N floats per thread (sum over threads > t)
 // and the block total, NT = 32 NW threads; scratch: 2 NW N + N floats.  The
 // association order is fixed (deterministic).
@@ -213,6 +321,22 @@ __device__ __forceinline__ void block_exclusive_suffix_n(const float (&v)[N], fl
         total[k] = all;
     }
     __syncthreads();
+}
+
+// Launch shape of the packed kernels for chains of up to Lmax residues: NT threads
+// x 2R residues per thread.  Runs of R = 3 residues from 513 residues on (a 3-residue
+// run of a periodic chain need not be a pure translation, so per-run rounding does
+// not add up coherently along an extended chain the way it does for R = 4: extended
+// L = 1000 had 1.2e-2 A with 128 x 4, tools/regular_sweep.py).
+struct BBPShape {
+    int nt, r;
+};
+constexpr int kBBPMaxL = 2 * 3 * 192;
+inline BBPShape bbp_shape(int Lmax) {
+    if (Lmax <= 256) return {128, 1};
+    if (Lmax <= 512) return {128, 2};
+    if (Lmax <= 768) return {128, 3};
+    return {192, 3};
 }
 
 // N consecutive floats between registers and shared memory, as 8-byte accesses

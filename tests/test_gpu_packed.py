@@ -167,3 +167,23 @@ def test_api_lrmsd_of_fullatom_uses_atom_counts(abi, table):
     for b in range(3):
         ref, *_ = olr.lrmsd(c[b, : na[b]], t[b, : na[b]])
         assert abs(val[b] - ref) <= 1e-4 * max(ref, 1.0)
+
+
+@pytest.mark.parametrize("kind", ["helix", "strand", "extended"])
+@pytest.mark.parametrize("L", [700, 1000])
+def test_regular_structures_gate(abi, oracle_lib, kind, L):
+    """the default path holds the 1e-3 A coordinate gate on regular
+    structures (helix (-57, -47), strand (-120, 130), extended (180, 180); omega = 180),
+    whose coordinates reach 1100-3700 A from the origin (fp32 ulp 1.2e-4-2.4e-4 A) and
+    whose identical residues repeat the same rounding (P:276 'negligible for
+    any realistic length').  Measured <= 9.1e-4 A (tools/regular_sweep.py)."""
+    B = 2
+    ang = synth.regular_angles(B, L, kind)
+    ln = torch.full((B,), L, dtype=torch.int32)
+    grad = synth.grad_normal((B, 3 * L, 3), 7700 + L)
+    c, gx = _run(abi, ang, ln, grad)
+    X = oracle_lib.backbone_forward(synth.numpy64(ang), ln.numpy())
+    assert np.abs(c - X).max() <= 1e-3
+    G = oracle_lib.backbone_backward(synth.numpy64(ang), ln.numpy(), synth.numpy64(grad))
+    for b in range(B):
+        assert np.abs(gx[b] - G[b]).max() / np.abs(G[b]).max() <= 1e-3
