@@ -90,3 +90,55 @@ def test_segment_bounds():
         assert max(sizes) - min(sizes) <= 1
     with pytest.raises(ValueError):
         tdist.segment_bounds(3, 4)
+
+
+def _bench_worker(rank, world, port, q):
+    """bench.py's own rank helpers under a gloo group: the strong-scaling shard of
+    the metric config (256 x 700) and of config 4 (ragged), and the max / sum
+    reductions the timed region and the residue count go through."""
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    import synth
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = {}
+    for c in ("metric", 4):
+        if c == 4:
+            lengths = synth.lengths_uniform(4096, 50, 2000, 3000 + 4)
+        else:
+            lengths = torch.full((256,), 700, dtype=torch.int32)
+        idx = bench.shard_for_rank(lengths, world, rank)
+        ids = [None] * world
+        dist.all_gather_object(ids, idx.tolist())
+        res = bench.sum_over_ranks(float(lengths[idx].sum()), dist)
+        out[str(c)] = (sorted(i for s in ids for i in s), res, float(lengths.sum()),
+                       [int(lengths[torch.tensor(s)].sum()) for s in ids])
+    t = bench.max_over_ranks(1.0 + rank, dist)
+    q.put((rank, out, t))
+    dist.destroy_process_group()
+
+
+def test_bench_rank_helpers_gloo_world2():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, out, t in res:
+        assert t == 2.0  # max over ranks of (1 + rank)
+        ids, tot, ref, loads = out["metric"]
+        assert ids == list(range(256)) and tot == ref and loads == [128 * 700, 128 * 700]
+        ids, tot, ref, loads = out["4"]
+        assert ids == list(range(4096)) and tot == ref
+        assert max(loads) / (sum(loads) / world) < 1.01  # LPT balance of the ragged config
