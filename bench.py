@@ -64,6 +64,8 @@ def parse():
 
 
 def cfg_key(c):
+    if isinstance(c, str) and ":" in c:
+        return synth.register_custom(c)
     return c if c in synth.CONFIGS else int(c)
 
 

@@ -1825,6 +1825,13 @@ static BBClShape bbxc_shape(int B, int Lmax) {
 
 cudaError_t bb_backward_xyz_launch(const BBArgs& a, cudaStream_t st) {
     if (!a.loss_state && !a.seg_totals && bbp_enabled() && bbp_backward_xyz_ok(a)) return bbp_backward_xyz_launch(a, st);
+    // longer chains, more of them than the decoupled / cluster regimes: tiles walked per CTA,
+    // opt-in (TPL_BBPXT=NTxRxNB): measured 89.7-91.0 us for config 4 against 86.1 us for the
+    // chain-serial 128 x 3 kernel below (tools/gpu.sh ab), so the default stays there
+    static const bool tiles_bwd = std::getenv("TPL_BBPXT") != nullptr;
+    if (tiles_bwd && !a.loss_state && !a.seg_totals && bbp_enabled() && !dl_enabled(a.B, a.Lmax) &&
+        a.B > sm_count())
+        return bbp_backward_xyz_tiles_launch(a, st);
     if (a.loss_state) {  // f1 fused LRMSD: chain-serial shapes
         const BBShape l = bbx_shape(a.B, a.Lmax);
 #define TPL_BBXL(NT_, R_) \
@@ -2014,6 +2021,9 @@ static cudaError_t dispatch_fwd_cl(const BBArgs& a, BBClShape s, cudaStream_t st
 cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st) {
     if (!a.loss_out && !a.seg_agg_out && !a.seg_omega_prev && bbp_enabled() && a.Lmax <= bbp_forward_max_L())
         return bbp_forward_launch(a, st);
+    // longer chains, more of them than the decoupled kernels' regime: tiles walked per CTA
+    if (!a.loss_out && !a.seg_agg_out && !a.seg_omega_prev && bbp_enabled() && a.ns == 1 && !dl_enabled(a.B, a.Lmax))
+        return bbp_forward_tiles_launch(a, st);
     if (a.loss_out) return a.ns == 0 ? dispatch_fwd_loss<0>(a, st) : dispatch_fwd_loss<1>(a, st);
     if (a.ns == 2) return dispatch<true, 2>(a, st);  // TPL_ORTHO=2/3: chain-per-CTA shapes only
     if (a.ns == 3) return dispatch<true, 3>(a, st);

@@ -63,8 +63,10 @@ cudaError_t bb_forward_launch(const BBArgs& a, cudaStream_t st);
 bool bbp_enabled();
 int bbp_forward_max_L();
 cudaError_t bbp_forward_launch(const BBArgs& a, cudaStream_t st);
+cudaError_t bbp_forward_tiles_launch(const BBArgs& a, cudaStream_t st);  // multi-tile chains, policy 1
 bool bbp_backward_xyz_ok(const BBArgs& a);
 cudaError_t bbp_backward_xyz_launch(const BBArgs& a, cudaStream_t st);
+cudaError_t bbp_backward_xyz_tiles_launch(const BBArgs& a, cudaStream_t st);  // multi-tile chains
 // fused_lrmsd.cu: angles -> coords -> LRMSD -> dLRMSD/dangles in one kernel
 int bbp_lrmsd_max_L();
 cudaError_t bbp_lrmsd_fused_launch(const BBArgs& a, float* grad_angles, cudaStream_t st);

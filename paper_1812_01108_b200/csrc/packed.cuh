@@ -135,11 +135,13 @@ __device__ __forceinline__ void sincos2_slow(float2 x, float2& s, float2& c) {
 // |angle| > 2^17 redoes its runs with the exact reduction.
 template <int R>
 __device__ __forceinline__ void bbp_pass1(const float* s_ang, int Lmax, int j0, bool chain_start,
-                                          float2 (&px)[3 * R], float2 (&py)[3 * R], float2 (&pz)[3 * R], Aff2& M) {
+                                          float2 (&px)[3 * R], float2 (&py)[3 * R], float2 (&pz)[3 * R], Aff2& M,
+                                          bool has_pre = false) {
+    // has_pre: s_ang[-1] holds omega of the residue before (a later tile of a chain)
     float maxabs = 0.f;
     auto angle = [&](int j, int k) -> float {  // omega_{j-1} (k=0), phi_j (1), psi_j (2); 0 past Lmax
         const int idx = 3 * j + k - 1;
-        return (j < Lmax && idx >= 0) ? s_ang[idx] : 0.f;
+        return (j < Lmax && (idx >= 0 || has_pre)) ? s_ang[idx] : 0.f;
     };
     auto pass1 = [&](auto slow) {
         constexpr bool kSlow = decltype(slow)::value;
@@ -166,6 +168,12 @@ __device__ __forceinline__ void bbp_pass1(const float* s_ang, int Lmax, int j0, 
             px[3 * q + 2] = M.t0; py[3 * q + 2] = M.t1; pz[3 * q + 2] = M.t2;
         }
     };
+    if (__all_sync(0xffffffffu, j0 >= Lmax)) {  // the warp's residues are all past the chain (ragged batches)
+        M.r00 = M.r11 = M.r22 = f2(1.f);
+        M.r01 = M.r02 = M.r10 = M.r12 = M.r20 = M.r21 = f2(0.f);
+        M.t0 = M.t1 = M.t2 = f2(0.f);
+        return;
+    }
     pass1(std::false_type{});
     if (__any_sync(0xffffffffu, maxabs > kSinCosFastMax)) pass1(std::true_type{});  // rare: huge angles
 }
@@ -274,6 +282,35 @@ __device__ __forceinline__ Aff block_exclusive_scan_qt(const Aff& agg, float* sc
     for (int w = 0; w < NW - 1; ++w)
         if (w < warp) p = qt_compose(p, load_qt(scratch + 8 * w));
     const QT res = warp > 0 ? qt_compose(p, ex) : ex;
+    __syncthreads();  // scratch is free again
+    return aff_from_qt(res);
+}
+
+// As block_exclusive_scan_qt with a carry: returns carry (x) the thread's exclusive
+// prefix and replaces carry by carry (x) the block's total (the next tile's carry).
+// scratch: NW * 8 + 8 floats.
+template <int NT>
+__device__ __forceinline__ Aff block_exclusive_scan_qt_carry(const Aff& agg, float* scratch, QT& carry) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    QT a = qt_from_aff(agg);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const QT o = shfl_up_qt(a, d);
+        if (lane >= d) a = qt_compose(o, a);
+    }
+    if (lane == 31) store_qt(scratch + 8 * warp, a);
+    QT ex = shfl_up_qt(a, 1);
+    if (lane == 0) ex = qt_identity();
+    __syncthreads();
+    QT p = carry;
+#pragma unroll
+    for (int w = 0; w < NW - 1; ++w)
+        if (w < warp) p = qt_compose(p, load_qt(scratch + 8 * w));
+    const QT res = qt_compose(p, ex);
+    if (threadIdx.x == NT - 1) store_qt(scratch + 8 * NW, qt_compose(p, a));
+    __syncthreads();
+    carry = load_qt(scratch + 8 * NW);
     __syncthreads();  // scratch is free again
     return aff_from_qt(res);
 }

@@ -44,7 +44,27 @@ _IDS = {"metric": 0, "lrmsd": 6, "long": 7}
 
 
 def config_id(c):
-    return _IDS[c] if c in _IDS else int(c)
+    if c in _IDS:
+        return _IDS[c]
+    if isinstance(c, str) and ":" in c:
+        return 90  # ad-hoc measurement shapes (register_custom)
+    return int(c)
+
+
+def register_custom(name):
+    """Ad-hoc measurement shape "bb:B:L", "bb:B:lo-hi" (ragged) or "fa:B:L" (not a
+    BASELINE config: kernel studies beside the configs)."""
+    if name in CONFIGS:
+        return name
+    kind, B, L = name.split(":")
+    cfg = dict(model="backbone" if kind == "bb" else "fullatom", B=int(B), desc=f"ad-hoc {name}")
+    if "-" in L:
+        lo, hi = (int(x) for x in L.split("-"))
+        cfg.update(L=hi, ragged=(lo, hi))
+    else:
+        cfg["L"] = int(L)
+    CONFIGS[name] = cfg
+    return name
 
 
 def _gen(seed):

@@ -5,6 +5,10 @@ policy switch (B <= 2 x SMs: programmatic dependent launch + padded shared
 memory), chain bases that are not 16-byte aligned (odd Lmax), ragged and
 degenerate lengths, and a bitwise comparison of the packed coordinate backward's
 padding behaviour.  Gates: north_star (1e-3 A, 1e-3 per-chain norm-wise)."""
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 import torch
@@ -52,7 +56,8 @@ def _check(oracle_lib, ang, ln, grad, c, gx, chains):
 
 
 @pytest.mark.parametrize("B,Lmax", [(1, 1), (2, 2), (5, 255), (7, 256), (9, 257), (33, 511), (17, 512), (40, 700),
-                                    (3, 701), (12, 767), (6, 768), (4, 1023), (11, 1024), (400, 300), (300, 769)])
+                                    (3, 701), (12, 767), (6, 768), (4, 1023), (11, 1024), (400, 300), (300, 769),
+                                    (7, 1152), (300, 1153), (400, 2000), (320, 3500)])
 def test_packed_shapes_ragged(abi, oracle_lib, B, Lmax):
     seed = 7100 + B * 7 + Lmax
     ang = synth.angles_uniform(B, Lmax, 3, seed)
@@ -187,3 +192,14 @@ def test_regular_structures_gate(abi, oracle_lib, kind, L):
     G = oracle_lib.backbone_backward(synth.numpy64(ang), ln.numpy(), synth.numpy64(grad))
     for b in range(B):
         assert np.abs(gx[b] - G[b]).max() / np.abs(G[b]).max() <= 1e-3
+
+
+def test_packed_tiles_backward_opt_in():
+    """The multi-tile packed coordinate backward (opt-in, TPL_BBPXT; env read once per
+    process): the ragged/long shapes of test_packed_shapes_ragged in a subprocess."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TPL_BBPXT="128x3x1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_packed.py"), "-k", "400-2000 or 320-3500 or 300-1153"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
