@@ -221,7 +221,7 @@ static __device__ bool sym4_max_eigen_newton(const double T[4][4], const double 
 // (an upper bound of the largest eigenvalue; only the starting point of the
 // iteration).  The fused one-pass kernel computes the LRMSD itself from the
 // residuals x~ - U^T y~ (a sum of squares, no cancellation).
-static __device__ void lrmsd_rotation(const double R[3][3], double e0, float* U, float* Ulo = nullptr) {
+static __device__ __noinline__ void lrmsd_rotation(const double R[3][3], double e0, float* U, float* Ulo = nullptr) {
     double T[4][4] = {
         {R[0][0] + R[1][1] + R[2][2], R[1][2] - R[2][1], R[2][0] - R[0][2], R[0][1] - R[1][0]},
         {R[1][2] - R[2][1], R[0][0] - R[1][1] - R[2][2], R[0][1] + R[1][0], R[0][2] + R[2][0]},

@@ -120,11 +120,16 @@ __device__ __forceinline__ void sincos2_fast(float2 x, float2& s, float2& c, flo
     c = make_float2(csx, csy);
     maxabs = fmaxf(maxabs, fmaxf(fabsf(x.x), fabsf(x.y)));
 }
-__device__ __forceinline__ void sincos2_slow(float2 x, float2& s, float2& c) {
+// Exact pair (Payne-Hanek for |x| > 2^17), out of line: returns (sin x, sin y, cos x, cos y).
+static __device__ __noinline__ float4 sincos2_exact(float2 x) {
     float xs[2] = {x.x, x.y}, ss[2], cc[2];
     tpl_sincos_n<2>(xs, ss, cc);
-    s = make_float2(ss[0], ss[1]);
-    c = make_float2(cc[0], cc[1]);
+    return make_float4(ss[0], ss[1], cc[0], cc[1]);
+}
+__device__ __forceinline__ void sincos2_slow(float2 x, float2& s, float2& c) {
+    const float4 r = sincos2_exact(x);
+    s = make_float2(r.x, r.y);
+    c = make_float2(r.z, r.w);
 }
 
 // Pass 1 of the packed forward: runs A (.x lanes, residues [j0, j0+R))
@@ -132,7 +137,7 @@ __device__ __forceinline__ void sincos2_slow(float2 x, float2& s, float2& c) {
 // (atom position) after every bond kept.  Angles past Lmax read as 0 (they only
 // move later residues, which are never stored); chain_start: run A begins at
 // residue 0, whose omega bond is the identity (reading Q1).  A warp holding an
-// |angle| > 2^17 redoes its runs with the exact reduction.
+// |angle| > 2^17 evaluates all its sincos with the exact reduction.
 template <int R>
 __device__ __forceinline__ void bbp_pass1(const float* s_ang, int Lmax, int j0, bool chain_start,
                                           float2 (&px)[3 * R], float2 (&py)[3 * R], float2 (&pz)[3 * R], Aff2& M,
