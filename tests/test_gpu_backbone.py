@@ -66,7 +66,7 @@ def _check(oracle_lib, ang, lengths, grad, coords, gang, chains=None, coord_tol=
         ref = G[n, :L]
         dg = np.abs(gang[b, :L] - ref).max() / max(np.abs(ref).max(), 1e-30)
         worst_c, worst_g = max(worst_c, dc), max(worst_g, dg)
-        tol = coord_tol if L <= 1000 else 5 * coord_tol  # reading Q21: L > 1000 is a target, not a gate
+        tol = coord_tol if L <= 1000 else 5e-3  # reading Q21: L > 1000 is a target (1e-3), gated at 5e-3
         assert dc <= tol, f"chain {b} L={L}: coord err {dc:.3e}"
         assert dg <= GRAD_TOL, f"chain {b} L={L}: grad rel err {dg:.3e}"
         # structural zeros
@@ -196,7 +196,7 @@ def test_long_single_chain_across_ctas(tpl, oracle_lib):
         X = oracle_lib.backbone_forward(synth.numpy64(ang), ln.numpy())
         err = np.abs(coords - X).max()
         print(f"L={L} single chain: max coord err {err:.3e} A")
-        assert err < 1e-2  # Q21: beyond L = 1000 the 1e-3 A gate is a target
+        assert err < 5e-3  # Q21: beyond L = 1000 the 1e-3 A gate is a target, gated at 5e-3
         G = oracle_lib.backbone_backward(synth.numpy64(ang), ln.numpy(), synth.numpy64(grad))
         rel = np.abs(gang - G).max() / np.abs(G).max()
         print(f"L={L} single chain ({'coords' if xyz else 'angles'} backward): grad rel err {rel:.3e}")
@@ -323,7 +323,7 @@ def test_segments_across_ranks_match_oracle(tpl, oracle_lib, n_seg):
     coords = torch.cat([p["c"] for p in parts], 1).cpu().numpy()
     gang = torch.cat([p["ga"] for p in parts], 1).cpu().numpy()
     lengths = torch.full((B,), L, dtype=torch.int32)
-    c, g = _check(oracle_lib, ang, lengths, grad, coords, gang, coord_tol=2e-3)
+    c, g = _check(oracle_lib, ang, lengths, grad, coords, gang)
     print(f"{n_seg} segments, L={L}: max coord err {c:.3e} A, grad rel err {g:.3e}")
 
 
@@ -363,7 +363,7 @@ def test_decoupled_more_items_than_resident_ctas(tpl, oracle_lib):
     coords, gang = _run(tpl, ang, ln, grad, xyz=True)
     lnn = ln.numpy()
     sample = sorted({int(np.argmax(lnn)), int(np.argmin(lnn)), 7, 150})
-    _check(oracle_lib, ang, ln, grad, coords, gang, chains=sample, coord_tol=2e-3)
+    _check(oracle_lib, ang, ln, grad, coords, gang, chains=sample)
 
 
 def test_coordinate_gate_L1000_many_chains(tpl, oracle_lib):

@@ -80,7 +80,7 @@ def test_pipeline_angles_to_lrmsd_gradient(tpl, oracle_lib):
     G = oracle_lib.backbone_backward(a64, ln.numpy(), gx)
     g = a.grad.cpu().numpy()
     for b in range(B):
-        assert np.abs(g[b] - G[b]).max() / np.abs(G[b]).max() <= 2e-3
+        assert np.abs(g[b] - G[b]).max() / np.abs(G[b]).max() <= 1e-3
     assert abs(float(loss.detach()) - vals.sum()) <= 1e-3 * vals.sum()
 
 
@@ -109,8 +109,8 @@ def test_fused_backbone_lrmsd(tpl, oracle_lib, B, L, lengths):
         assert abs(v[b] - vals[b]) <= 1e-3 * max(vals[b], 1e-3), (b, v[b], vals[b])
         if Lb > 1:
             rel = np.abs(g[b, :Lb] - G[b, :Lb]).max() / np.abs(G[b, :Lb]).max()
-            assert rel <= 2e-3, (b, rel)
-        assert np.abs(coords[b, :3 * Lb].cpu().numpy() - X[b, :3 * Lb]).max() <= 5e-3
+            assert rel <= 1e-3, (b, rel)
+        assert np.abs(coords[b, :3 * Lb].cpu().numpy() - X[b, :3 * Lb]).max() <= (1e-3 if Lb <= 1000 else 5e-3)
 
 
 @pytest.mark.parametrize("B,L,lengths,noise", [(3, 700, None, 0.0), (6, 1000, [1000, 1, 2, 3, 517, 999], 0.0),
