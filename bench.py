@@ -590,7 +590,9 @@ def run_ours(args):
         cfgd = work.config()
         gb = work.cfg["B"] if args.scaling == "strong" else work.B * world
         cfgd.update({"global_batch": gb, "parallelism": f"dp{world} (chains sharded, no collective)",
-                     "l2_flush": f"rotating {n_sets} buffer sets ({n_sets * work.footprint() / 2**20:.0f} MiB > 4x L2)",
+                     "l2_flush": f"rotating buffer sets: a timed region of K={K} steps touches {min(K, n_sets)} of "
+                                 f"{n_sets} sets ({min(K, n_sets) * work.footprint() / 2**20:.0f} MiB; L2 "
+                                 f"{l2 / 2**20:.0f} MiB), each set reused only after {min(K, n_sets) - 1} others",
                      "timing": f"CUDA graphs of K steps, median of {len(t_step)} timed regions"})
         out = {"metric": f"residues/sec fwd+bwd ({work.model}, L={work.Lmax}, batch {gb})",
                "value": value, "unit": "residues/s", "n_gpus": world, "steps": K, "warmup": W,

@@ -267,21 +267,38 @@ typedef struct tpl_residue_desc {
 
 typedef struct tpl_tables tpl_tables; /* opaque, immutable after create */
 
-/* Validate and upload `n_types` (1..TPL_MAX_TYPES) residue types; uses the
- * current CUDA device.  *out is NULL on failure. */
+/* The residue-type table of the full-atom model: per type the rigid groups
+ * ("the rigid groups of atoms ... connected by the dihedral angles",
+ * R' of P:48) and their atoms' positions in the group frame (r°);
+ * the paper gives only threonine's topology, so the values are data
+ * (reading Q8).  Validate and upload `n_types` (1..TPL_MAX_TYPES) types;
+ * uses the current CUDA device.  Errors: TPL_ERR_NULL, TPL_ERR_TABLE (a
+ * count out of range, a parent that is neither -1 nor g-1, a slot outside
+ * 3..7, atoms not owner-sorted), TPL_ERR_CUDA.  *out is NULL on failure;
+ * the caller owns the table and frees it with tpl_tables_destroy. */
 TPL_API tpl_status tpl_tables_create(const tpl_residue_desc* types, int32_t n_types, tpl_tables** out);
 TPL_API void tpl_tables_destroy(tpl_tables* tables);
 TPL_API int32_t tpl_tables_n_types(const tpl_tables* tables);
 
-/* Host-side bookkeeping: atoms_per_chain[b] (may be NULL) and the padded
- * *atom_stride = max_b atoms (rounded up to a multiple of 4) for HOST
- * restype [B][Lmax] and lengths [B]. */
+/* Host-side bookkeeping of the packed output layout (each residue
+ * contributes its type's heavy atoms, hydrogens omitted -- reading Q14):
+ * atoms_per_chain[b] (may be NULL) = sum of the chain's per-type atom counts,
+ * and the padded *atom_stride = max_b atoms (rounded up to a multiple of 4)
+ * for HOST restype [B][Lmax] and lengths [B].  Errors: TPL_ERR_NULL,
+ * TPL_ERR_SHAPE (B or Lmax < 1, a length outside [1, Lmax], a restype >= the
+ * table's type count, a stride that overflows int32). */
 TPL_API tpl_status tpl_fullatom_atoms(const tpl_tables* tables, const uint8_t* restype_host, const int32_t* lengths_host,
                               int32_t B, int32_t Lmax, int32_t* atoms_per_chain, int32_t* atom_stride);
 
-/* Forward.  angles [B][Lmax][8] fp32, restype [B][Lmax] uint8 (device),
- * coords [B][atom_stride][3] fp32 output: each chain's atoms packed from
- * index 0, residue by residue, in the table's atom order. */
+/* Forward (P:41-59 on the backbone chain of P:143-175): the backbone frames
+ * N_j, CA_j, C_j by the same transform product as the backbone model, then per
+ * residue the side-chain groups M_g = M_parent R_x(pre) R(chi or fixed, theta,
+ * d) and every atom r = M_owner r°.  angles [B][Lmax][8] fp32 (phi, psi, omega,
+ * chi1..chi5), restype [B][Lmax] uint8 (device), coords [B][atom_stride][3]
+ * fp32 output: each chain's atoms packed from index 0, residue by residue, in
+ * the table's atom order; entries past a chain's atoms are not written.  A
+ * length outside [1, Lmax], a restype >= n_types or a chain that overflows
+ * atom_stride is skipped and flagged in the workspace error word. */
 TPL_API tpl_status tpl_fullatom_forward(const tpl_tables* tables, const float* angles, const uint8_t* restype,
                                 const int32_t* lengths, int32_t B, int32_t Lmax, int32_t atom_stride,
                                 float* coords, void* workspace, size_t ws_bytes, void* stream);
