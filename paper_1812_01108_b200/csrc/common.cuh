@@ -692,6 +692,15 @@ inline cudaError_t launch_cluster(void (*kernel)(KArgs...), int grid, int cl, in
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// L2 prefetch of a global range (bulk, no completion tracking).  Safe before
+// griddepcontrol.wait even for data the preceding kernel writes: L2 is the point of
+// coherence, a prefetched line the producer rewrites later just holds the new bytes;
+// nothing is consumed before the wait.  It only moves a cold input's DRAM latency
+// under the previous kernel's tail.
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Split of a byte range into (head | 16-aligned middle | tail).
 struct Span {
     const char* g;  // global start
