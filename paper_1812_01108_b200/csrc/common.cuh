@@ -369,7 +369,8 @@ __device__ __forceinline__ Aff block_exclusive_scan(Aff a, const Aff& carry, flo
 
 // Block-wide EXCLUSIVE suffix sum of a 6-vector (sum over threads > t) plus a
 // carry (sum over later tiles).  scratch: (2 * NT/32 * 6 + 8) floats.
-template <int NT>
+// kReuse = false: the caller never touches the scratch again (no trailing barrier).
+template <int NT, bool kReuse = true>
 __device__ __forceinline__ void block_exclusive_suffix6(float v[6], const float carry[6], float* scratch,
                                                         float out[6], float total[6]) {
     constexpr int NW = NT / 32;
@@ -444,7 +445,7 @@ __device__ __forceinline__ void block_exclusive_suffix6(float v[6], const float 
         for (int w = NW - 1; w >= 0; --w) s += scratch[6 * w + k];
         total[k] = s;
     }
-    __syncthreads();
+    if (kReuse) __syncthreads();
 }
 
 // Block-wide exclusive prefix sum of an int (plus carry); *total = carry + sum.

@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(NT, NT * R >= 512 ? 2 : (R >= 3 ? 3 : 4)) bbp_
     float v6[6] = {S0.x + S0.y, S1.x + S1.y, S2.x + S2.y, T0.x + T0.y, T1.x + T1.y, T2.x + T2.y};
     const float zero6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float ext[6], tot6[6];
-    block_exclusive_suffix6<NT>(v6, zero6, s_suf, ext, tot6);
+    block_exclusive_suffix6<NT, false>(v6, zero6, s_suf, ext, tot6);
     // running suffix state: lane y = after run B (= ext), lane x = after run A (= ext + run B)
     S0 = make_float2(ext[0] + S0.y, ext[0]); S1 = make_float2(ext[1] + S1.y, ext[1]);
     S2 = make_float2(ext[2] + S2.y, ext[2]); T0 = make_float2(ext[3] + T0.y, ext[3]);

@@ -198,8 +198,12 @@ struct QT {
 
 __device__ __forceinline__ QT qt_identity() { return QT{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}; }
 
+// |q| is within ~1e-6 of 1 here (products of unit quaternions, or Shepperd's
+// conversion): one Newton step q (3 - |q|^2) / 2 renormalises to O(eps^2) without
+// a MUFU rsqrt in the scan's dependency chain.
 __device__ __forceinline__ void qt_normalize(QT& a) {
-    const float r = rsqrtf(fmaf(a.w, a.w, fmaf(a.x, a.x, fmaf(a.y, a.y, a.z * a.z))));
+    const float n2 = fmaf(a.w, a.w, fmaf(a.x, a.x, fmaf(a.y, a.y, a.z * a.z)));
+    const float r = fmaf(-0.5f, n2, 1.5f);
     a.w *= r; a.x *= r; a.y *= r; a.z *= r;
 }
 
@@ -287,7 +291,7 @@ __device__ __forceinline__ Aff block_exclusive_scan_qt(const Aff& agg, float* sc
     for (int w = 0; w < NW - 1; ++w)
         if (w < warp) p = qt_compose(p, load_qt(scratch + 8 * w));
     const QT res = warp > 0 ? qt_compose(p, ex) : ex;
-    __syncthreads();  // scratch is free again
+    // no trailing barrier: the single-tile callers never reuse the scratch
     return aff_from_qt(res);
 }
 
