@@ -701,6 +701,14 @@ inline cudaError_t launch_cluster(void (*kernel)(KArgs...), int grid, int cl, in
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+// Only where the launch is latency-bound (at most two chains per SM, the PDL regime):
+// in the throughput regime the load follows the prefetch at once and the prefetch is a
+// second request for the same lines (config 5 backward +1.4%).
+__device__ __forceinline__ bool prefetch_regime(int B) {
+    unsigned nsm;
+    asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+    return B <= 2 * int(nsm);
+}
 
 // Split of a byte range into (head | 16-aligned middle | tail).
 struct Span {

@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "packed.cuh"
 
 namespace tpl {
 // added to a thread's atom count when its residue type is out of range: far above any
@@ -143,7 +144,12 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
             bulk_g2s(smem + S::kTable, a.types, tb, bar);
         }
     }
-    pdl_wait();  // the dependent launches when this grid exits (early triggers cost SM slots)
+    if (tid == 0 && prefetch_regime(a.B)) {  // cold inputs into L2 under the previous kernel's tail (safe before the wait)
+        const Span pa = make_span(a.angles + (size_t)b * a.Lmax * kFASlots, a.Lmax * 32);
+        if (pa.mid > 0) prefetch_l2(pa.g + pa.head, unsigned(pa.mid));
+    }
+    pdl_wait();
+    pdl_trigger();  // launched with PDL only for <= 2 chains per SM, where every CTA is resident
     const int L = a.lengths[b];
     __syncthreads();
     if (kTS) {
@@ -684,7 +690,12 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
             bulk_g2s(smem + S::kTable, a.types, tb, bar + 2);
         }
     }
+    if (tid == 0 && prefetch_regime(a.B)) {  // dL/dr is cold: into L2 under the previous kernel's tail
+        const Span pg = make_span(a.grad_coords + (size_t)b * a.atom_stride * 3, a.atom_stride * 12);
+        if (pg.mid > 0) prefetch_l2(pg.g + pg.head, unsigned(pg.mid));
+    }
     pdl_wait();
+    pdl_trigger();
     const int L = a.lengths[b];
     __syncthreads();
     if (kTabSmem) mbar_wait(bar + 2, 0);
@@ -970,7 +981,7 @@ static cudaError_t fa_fwd_v(const FAArgs& a, cudaStream_t st) {
     static LaunchCfg cfg;  // one grid CTA per chain: only the shared-memory opt-in is used
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
-    return launch_pdl(k, a.B, NT, sm, st, a, a.max_atoms);
+    return launch_bbp(k, a.B, NT, BBPLaunch{sm, a.B <= 2 * device_sm_count()}, st, a, a.max_atoms);
 }
 // TPL_FAF=NTxTSxMINB (tuning) or the default.
 struct FAFShape {
@@ -1043,7 +1054,7 @@ static cudaError_t fa_bwd_xyz(const FAArgs& a, cudaStream_t st) {
     static LaunchCfg cfg;  // one grid CTA per chain: only the shared-memory opt-in is used
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
-    return launch_pdl(k, a.B, NT, sm, st, a, max_tiles);
+    return launch_bbp(k, a.B, NT, BBPLaunch{sm, a.B <= 2 * device_sm_count()}, st, a, max_tiles);
 }
 
 cudaError_t fa_backward_xyz_launch(const FAArgs& a, cudaStream_t st) {

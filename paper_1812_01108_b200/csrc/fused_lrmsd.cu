@@ -60,8 +60,10 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const f
     const Span sa = make_span(angles + (size_t)b * Lmax * 3, Lmax * 12);
     const int w0 = warp * WRES;
     const Span syw = make_span(target + cbase + 9 * (size_t)w0, max(0, min(WRES, Lmax - w0)) * 36);
-    if (tid == 0 && sa.mid > 0) prefetch_l2(sa.g + sa.head, unsigned(sa.mid));
-    if (lane == 0 && syw.mid > 0) prefetch_l2(syw.g + syw.head, unsigned(syw.mid));
+    if (prefetch_regime(B)) {
+        if (tid == 0 && sa.mid > 0) prefetch_l2(sa.g + sa.head, unsigned(sa.mid));
+        if (lane == 0 && syw.mid > 0) prefetch_l2(syw.g + syw.head, unsigned(syw.mid));
+    }
     pdl_wait();
     pdl_trigger();
     if (tid == 0) {

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(NT, NT * R >= 512 ? 384 / NT : 512 / NT) bbp_f
     const int b = blockIdx.x;
     TPL_STAMP(0);
     const Span sa = make_span(angles + (size_t)b * Lmax * 3, Lmax * 12);
-    if (tid == 0 && sa.mid > 0) prefetch_l2(sa.g + sa.head, unsigned(sa.mid));  // under the previous kernel's tail
+    if (tid == 0 && sa.mid > 0 && prefetch_regime(B)) prefetch_l2(sa.g + sa.head, unsigned(sa.mid));  // under the previous kernel's tail
     pdl_wait();     // programmatic dependent launch: nothing global is read before this
     pdl_trigger();  // every CTA is resident: the next kernel may start launching
     if (tid == 0) {
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(NT, NT * R >= 512 ? 2 : (R >= 3 ? 3 : 4)) bbp_
     const int wl = max(0, min(WRES, Lmax - w0));      // residues of the warp's piece (speculative: Lmax)
     const Span sxw = make_span(coords + cbase + 9 * (size_t)w0, wl * 36);
     const Span sgw = make_span(grad_coords + cbase + 9 * (size_t)w0, wl * 36);
-    if (lane == 0 && sgw.mid > 0) prefetch_l2(sgw.g + sgw.head, unsigned(sgw.mid));  // dL/dr is cold
+    if (lane == 0 && sgw.mid > 0 && prefetch_regime(B)) prefetch_l2(sgw.g + sgw.head, unsigned(sgw.mid));  // dL/dr is cold
     pdl_wait();
     pdl_trigger();
     if (lane == 0) {  // each warp initialises its own barrier and issues its own piece
