@@ -47,12 +47,12 @@ PY
     launches)
       c=${args[0]}
       python bench.py --config $c $SMALL_ARGS --no-parity > /dev/null 2>&1 && \
-      ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 \
+      ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --kernel-name-base demangled -c 400 \
           --csv --log-file gpurun_out/launches_$c.csv python bench.py --config $c $SMALL_ARGS --no-parity > gpurun_out/ncu_launch.log 2>&1
       echo "launches $c exit $?" ;;
     full)
       c=${args[0]}; k=${args[1]}
-      ncu --set full --clock-control none --import-source on -k regex:$k -s 4 -c 1 \
+      ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:$k -s 4 -c 1 \
           -o gpurun_out/full_${c}_$k -f python bench.py --config $c $SMALL_ARGS --no-parity > gpurun_out/ncu_full_$c.log 2>&1
       echo "full $c $k exit $?" ;;
     sanitize)
