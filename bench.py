@@ -35,6 +35,8 @@ import torch  # noqa: E402
 
 import synth  # noqa: E402
 
+BWD_FROM = "coords"  # --bwd-from
+
 BYTES_PER_RES = {  # algorithmic bytes
     # bwd: the operation's own bytes (angles + dL/dr in, dL/dangles out).  The kernel
     # reads the forward's coordinates instead of the angles (36 B, not 12): moved
@@ -57,6 +59,9 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds of the cpu_baseline sample")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-parity", action="store_true", help="skip the oracle parity leg (A/B timing runs only)")
+    p.add_argument("--bwd-from", default="coords", choices=["coords", "angles"],
+                   help="backward entry point: from the forward's coordinates (the autograd layers' path, "
+                        "default) or from the angles (stateless; reads 12 / 33 B/res of angles instead)")
     p.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                    help="strong (default, the metric's definition: the config's batch sharded over the "
                         "ranks, contiguous or LPT); weak: every rank runs the whole batch")
@@ -223,6 +228,9 @@ class BackboneWork:
     def bwd(self, s, stream=None):
         from paper_1812_01108_b200 import _abi
 
+        if BWD_FROM == "angles":  # stateless: recompute the forward from the angles
+            _abi.tpl_backbone_backward(s["angles"], s["lengths"], s["grad"], s["gang"], s["ws"], stream)
+            return
         # the autograd layer's backward: from the forward's coordinates
         _abi.tpl_backbone_backward_from_coords(s["coords"], s["lengths"], s["grad"], s["gang"], s["ws"], stream)
 
@@ -363,6 +371,10 @@ class FullAtomWork:
     def bwd(self, s, stream=None):
         from paper_1812_01108_b200 import _abi
 
+        if BWD_FROM == "angles":  # stateless: recompute the forward from the angles
+            _abi.tpl_fullatom_backward(self.tables.handle, s["angles"], s["restype"], s["lengths"], s["grad"],
+                                       s["gang"], s["ws"], stream)
+            return
         # the autograd layer's backward: from the forward's coordinates
         _abi.tpl_fullatom_backward_from_coords(self.tables.handle, s["coords"], s["restype"], s["lengths"],
                                                s["grad"], s["gang"], s["ws"], stream)
@@ -829,7 +841,9 @@ def run_reference(args):
 
 
 def main():
+    global BWD_FROM
     args = parse()
+    BWD_FROM = args.bwd_from
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -85,6 +85,8 @@ def main():
     if a.packed:
         names = ["start", "issued", "landed", "pass1", "scan", "pass2", "store issued", "end"]
         st = np.array(buf, dtype=np.int64).reshape(n, 16)[:, 8:16] if a.bwd else np.array(buf, dtype=np.int64).reshape(n, 16)[:, :8]
+        for c in range(1, st.shape[1]):  # a phase without a stamp (e.g. no separate store issue) takes the one before
+            st[:, c] = np.where(st[:, c] > 0, st[:, c], st[:, c - 1])
         st = st[(st > 0).all(axis=1)]
         rel = st - st[:, 0].min()
         print(f"{'bwd' if a.bwd else 'fwd'} B={a.B} L={a.L}: {len(st)} CTAs, span {rel.max() / 1e3:.2f} us")
