@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
     }
 
     Aff carry = aff_identity();
+    QT carryq = qt_identity();  // policies 1 and 3: the chain prefix in (quaternion, translation) form
     int carry_atoms = 0;
     const int rl0 = tid * RPT;
     float* coords = a.coords + (size_t)b * a.atom_stride * 3;
@@ -224,8 +225,15 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
         Aff FN[RPT], FCA[RPT], FC[RPT];
         fa_chunk<RPT>(s_ang, rl0, r0, n, M, FN, FCA, FC);
         if (kNS >= 1) aff_orthonormalize(M);
-        const Aff P = block_exclusive_scan<NT, kNS>(M, carry, s_scan, s_total);
-        carry = load_aff(s_total);
+        // policies 1 / 3: the (quaternion, translation) scan of packed.cuh (renormalised every
+        // combine, 7 floats per shuffle level; reading Q25); 0 / 2: the 3x4 affine scan
+        Aff P;
+        if (kNS == 1 || kNS == 3) {
+            P = block_exclusive_scan_qt_carry<NT>(M, s_scan, carryq);
+        } else {
+            P = block_exclusive_scan<NT, kNS>(M, carry, s_scan, s_total);
+            carry = load_aff(s_total);
+        }
 
         const int n_tile_atoms = tile_end_atoms - carry_atoms;
         const Span so = make_span(coords + (size_t)carry_atoms * 3, n_tile_atoms * 12);

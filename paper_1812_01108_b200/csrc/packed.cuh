@@ -297,7 +297,7 @@ __device__ __forceinline__ Aff block_exclusive_scan_qt(const Aff& agg, float* sc
 
 // As block_exclusive_scan_qt with a carry: returns carry (x) the thread's exclusive
 // prefix and replaces carry by carry (x) the block's total (the next tile's carry).
-// scratch: NW * 8 + 8 floats.
+// scratch: NW * 8 + 8 floats ((2 NW + 1) * 8 for NW > 4).
 template <int NT>
 __device__ __forceinline__ Aff block_exclusive_scan_qt_carry(const Aff& agg, float* scratch, QT& carry) {
     constexpr int NW = NT / 32;
@@ -313,9 +313,28 @@ __device__ __forceinline__ Aff block_exclusive_scan_qt_carry(const Aff& agg, flo
     if (lane == 0) ex = qt_identity();
     __syncthreads();
     QT p = carry;
+    if (NW > 4) {
+        // wide blocks: warp 0 scans the NW warp totals in log2(NW) steps (a serial chain of
+        // NW - 1 combines cost the 512-thread full-atom forward 9%) and parks each warp's
+        // prefix, carry included, at scratch[8 (NW + 1 + w)]; scratch: (2 NW + 1) 8 floats
+        if (warp == 0) {
+            QT t = lane < NW ? load_qt(scratch + 8 * lane) : qt_identity();
 #pragma unroll
-    for (int w = 0; w < NW - 1; ++w)
-        if (w < warp) p = qt_compose(p, load_qt(scratch + 8 * w));
+            for (int d = 1; d < NW; d <<= 1) {
+                const QT o = shfl_up_qt(t, d);
+                if (lane >= d) t = qt_compose(o, t);
+            }
+            QT e = shfl_up_qt(t, 1);
+            if (lane == 0) e = qt_identity();
+            if (lane < NW) store_qt(scratch + 8 * (NW + 1 + lane), qt_compose(carry, e));
+        }
+        __syncthreads();
+        p = load_qt(scratch + 8 * (NW + 1 + warp));
+    } else {
+#pragma unroll
+        for (int w = 0; w < NW - 1; ++w)
+            if (w < warp) p = qt_compose(p, load_qt(scratch + 8 * w));
+    }
     const QT res = qt_compose(p, ex);
     if (threadIdx.x == NT - 1) store_qt(scratch + 8 * NW, qt_compose(p, a));
     __syncthreads();
