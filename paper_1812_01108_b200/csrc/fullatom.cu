@@ -76,6 +76,16 @@ __device__ __forceinline__ float axis_moment(float ex, float ey, float ez, float
     return fmaf(ex, c0, fmaf(ey, c1, ez * c2));
 }
 
+// a side-chain group's constants as four independent 16-byte loads (the fields' latency
+// chain -- parent, slot, angle, bond constants, atom range -- is one round trip)
+__device__ __forceinline__ FAGroup load_group(const FAGroup& g) {
+    FAGroup r;
+    const int4* s = reinterpret_cast<const int4*>(&g);
+    int4* d = reinterpret_cast<int4*>(&r);
+    d[0] = s[0]; d[1] = s[1]; d[2] = s[2]; d[3] = s[3];
+    return r;
+}
+
 // r° of atom k as one 16-byte load (the table row is float[4], 16-byte aligned)
 __device__ __forceinline__ float4 r0_of(const FAType& T, int k) { return *reinterpret_cast<const float4*>(T.r[k]); }
 __device__ __forceinline__ void apply4(const Aff& M, float4 r, float& ox, float& oy, float& oz) {
@@ -255,7 +265,7 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
                     apply4(gCA, r0_of(T, k), o[3 * k], o[3 * k + 1], o[3 * k + 2]);
                 Aff G = gCA;
                 for (int g = 0; g < T.n_groups; ++g) {
-                    const FAGroup& gr = T.g[g];
+                    const FAGroup gr = load_group(T.g[g]);
                     if (gr.parent < 0) {
                         G = gCA;
                         if (gr.has_pre) aff_rot_x(G, gr.cb, gr.sb);

@@ -85,7 +85,7 @@ cudaError_t paper_bb_backward_launch(const BBArgs& a, const float* Msave, cudaSt
 // ---- full atom -------------------------------------------------------------
 // Device residue-type table (fp32, uploaded once by tpl_tables_create).
 // One record per type, 16-byte aligned, copied whole into shared memory.
-struct FAGroup {
+struct alignas(16) FAGroup {  // 64 bytes: loaded whole with four 16-byte loads
     float ca, sa;      // cos/sin of the fixed alpha (slot < 0)
     float ct, st, d;   // bond constants
     float cb, sb;      // R' = R_x(pre_rx); (1, 0) when absent
@@ -96,7 +96,9 @@ struct FAGroup {
     int end_atom;      // one past the group's last atom
     int origin;        // atom at the group frame's origin (owned by g, r° = 0), -1 if none
     int porigin;       // atom at the parent frame's origin (CA for parent -1), -1 if none
+    int pad_[2];
 };
+static_assert(sizeof(FAGroup) == 64, "FAGroup is loaded as four 16-byte vectors");
 struct alignas(16) FAType {
     int n_groups, n_atoms;
     int n_N, n_CA;            // atoms owned by the N / CA frames (first n_N, then n_CA)
