@@ -335,7 +335,7 @@ __device__ __forceinline__ void fa_residue_backward(const FAType& T, const float
         Aff G = gCA;
         if (T.g[g0].has_pre) aff_rot_x(G, T.g[g0].cb, T.g[g0].sb);
         for (int g = g0; g <= g1; ++g) {
-            const FAGroup& gr = T.g[g];
+            const FAGroup gr = load_group(T.g[g]);
             float s, c;
             if (gr.slot >= 0) tpl_sincos(ang[gr.slot], &s, &c);
             else { s = gr.sa; c = gr.ca; }
@@ -343,7 +343,7 @@ __device__ __forceinline__ void fa_residue_backward(const FAType& T, const float
         }
         float br[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         for (int g = g1; g >= g0; --g) {
-            const FAGroup& gr = T.g[g];
+            const FAGroup gr = load_group(T.g[g]);
             for (k = gr.first_atom; k < gr.end_atom; ++k) {
                 float x, y, z;
                 apply4(G, r0_of(T, k), x, y, z);
@@ -868,7 +868,7 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
                 for (int i = T.first_C; i < T.n_atoms; ++i) acc(RC[q], i);
                 float br[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 for (int gi = T.n_groups - 1; gi >= 0; --gi) {
-                    const FAGroup& gr = T.g[gi];
+                    const FAGroup gr = load_group(T.g[gi]);
                     for (int i = gr.first_atom; i < gr.end_atom; ++i) acc(br, i);
                     if (gr.slot >= 0) {
                         const int o = gr.origin, p = gr.porigin;
