@@ -76,6 +76,19 @@ __device__ __forceinline__ float axis_moment(float ex, float ey, float ez, float
     return fmaf(ex, c0, fmaf(ey, c1, ez * c2));
 }
 
+// a residue type's header (counts and origin atoms) as two 16-byte loads
+struct FAHead {
+    int n_groups, n_atoms, n_N, n_CA, first_C, iN, iCA, iC;
+};
+__device__ __forceinline__ FAHead load_head(const FAType& T) {
+    FAHead h;
+    const int4* s = reinterpret_cast<const int4*>(&T);
+    int4* d = reinterpret_cast<int4*>(&h);
+    d[0] = s[0];
+    d[1] = s[1];
+    return h;
+}
+
 // a side-chain group's constants as four independent 16-byte loads (the fields' latency
 // chain -- parent, slot, angle, bond constants, atom range -- is one round trip)
 __device__ __forceinline__ FAGroup load_group(const FAGroup& g) {
@@ -254,17 +267,18 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
             const int rl = rl0 + q;
             if (rl < n) {
                 const FAType& T = s_types[typ[q]];
+                const FAHead h = load_head(T);
                 const Aff gN = aff_compose(P, FN[q]);
                 const Aff gCA = aff_compose(P, FCA[q]);
                 const Aff gC = aff_compose(P, FC[q]);
                 const float* ang = s_ang + 8 * rl;
                 float* o = s_out + 3 * off;
                 int k = 0;
-                for (; k < T.n_N; ++k) apply4(gN, r0_of(T, k), o[3 * k], o[3 * k + 1], o[3 * k + 2]);
-                for (; k < T.n_N + T.n_CA; ++k)
+                for (; k < h.n_N; ++k) apply4(gN, r0_of(T, k), o[3 * k], o[3 * k + 1], o[3 * k + 2]);
+                for (; k < h.n_N + h.n_CA; ++k)
                     apply4(gCA, r0_of(T, k), o[3 * k], o[3 * k + 1], o[3 * k + 2]);
                 Aff G = gCA;
-                for (int g = 0; g < T.n_groups; ++g) {
+                for (int g = 0; g < h.n_groups; ++g) {
                     const FAGroup gr = load_group(T.g[g]);
                     if (gr.parent < 0) {
                         G = gCA;
@@ -278,9 +292,9 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
                     for (k = gr.first_atom; k < gr.end_atom; ++k)
                         apply4(G, r0_of(T, k), o[3 * k], o[3 * k + 1], o[3 * k + 2]);
                 }
-                for (k = T.first_C; k < T.n_atoms; ++k)
+                for (k = h.first_C; k < h.n_atoms; ++k)
                     apply4(gC, r0_of(T, k), o[3 * k], o[3 * k + 1], o[3 * k + 2]);
-                off += T.n_atoms;
+                off += h.n_atoms;
             }
         }
         fence_proxy_async_smem();
@@ -311,27 +325,28 @@ __device__ __forceinline__ void fa_residue_backward(const FAType& T, const float
 #pragma unroll
     for (int k = 0; k < 6; ++k) R.all[k] = R.nN[k] = R.cC[k] = 0.f;
     const float cx = gCA.t0, cy = gCA.t1, cz = gCA.t2;
+    const FAHead h = load_head(T);
     int k = 0;
-    for (; k < T.n_N; ++k) {
+    for (; k < h.n_N; ++k) {
         float x, y, z;
         apply4(gN, r0_of(T, k), x, y, z);
         cross_acc(R.nN, x - cx, y - cy, z - cz, gk[3 * k], gk[3 * k + 1], gk[3 * k + 2]);
     }
-    for (; k < T.n_N + T.n_CA; ++k) {
+    for (; k < h.n_N + h.n_CA; ++k) {
         float x, y, z;
         apply4(gCA, r0_of(T, k), x, y, z);
         cross_acc(R.all, x - cx, y - cy, z - cz, gk[3 * k], gk[3 * k + 1], gk[3 * k + 2]);
     }
-    for (k = T.first_C; k < T.n_atoms; ++k) {
+    for (k = h.first_C; k < h.n_atoms; ++k) {
         float x, y, z;
         apply4(gC, r0_of(T, k), x, y, z);
         cross_acc(R.cC, x - cx, y - cy, z - cz, gk[3 * k], gk[3 * k + 1], gk[3 * k + 2]);
     }
     // side-chain branches: forward to the branch tip, then walk back
     int g0 = 0;
-    while (g0 < T.n_groups) {
+    while (g0 < h.n_groups) {
         int g1 = g0;
-        while (g1 + 1 < T.n_groups && T.g[g1 + 1].parent == g1) ++g1;
+        while (g1 + 1 < h.n_groups && T.g[g1 + 1].parent == g1) ++g1;
         Aff G = gCA;
         if (T.g[g0].has_pre) aff_rot_x(G, T.g[g0].cb, T.g[g0].sb);
         for (int g = g0; g <= g1; ++g) {
@@ -549,6 +564,7 @@ __global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_
             const int rl = rl0 + q;
             if (rl < n) {
                 const FAType& T = s_types[typ[q]];
+                const FAHead h = load_head(T);
                 const Aff gN = aff_compose(P, FN[q]);
                 const Aff gCA = aff_compose(P, FCA[q]);
                 const Aff gC = aff_compose(P, FC[q]);
@@ -570,7 +586,7 @@ __global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_
                 thr[3] += s6[3] + fmaf(gCA.t1, s6[2], -gCA.t2 * s6[1]);
                 thr[4] += s6[4] + fmaf(gCA.t2, s6[0], -gCA.t0 * s6[2]);
                 thr[5] += s6[5] + fmaf(gCA.t0, s6[1], -gCA.t1 * s6[0]);
-                off += T.n_atoms;
+                off += h.n_atoms;
             }
         }
         float suf[6], tot6[6];
@@ -840,22 +856,23 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
             const int rl = rl0 + q;
             if (rl < n) {
                 const FAType& T = s_types[typ[q]];
+                const FAHead h = load_head(T);
                 const float* x = X + 3 * off;
                 const float* g = G + 3 * off;
                 float* go = s_go + 8 * rl;
 #pragma unroll
                 for (int c = 3; c < 8; ++c) go[c] = 0.f;
-                const float cx = x[3 * T.iCA], cy = x[3 * T.iCA + 1], cz = x[3 * T.iCA + 2];
+                const float cx = x[3 * h.iCA], cy = x[3 * h.iCA + 1], cz = x[3 * h.iCA + 2];
                 PCA[q][0] = cx; PCA[q][1] = cy; PCA[q][2] = cz;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    PN[q][c] = x[3 * T.iN + c];
-                    PC[q][c] = x[3 * T.iC + c];
+                    PN[q][c] = x[3 * h.iN + c];
+                    PC[q][c] = x[3 * h.iC + c];
                 }
                 const int j = r0 + rl;
                 if (j + 1 < L) {  // N of the next residue: in this tile, or the first of the later tile
                     const int iN = s_types[s_rtc[j + 1]].iN;
-                    const float* xn = rl + 1 < n ? x + 3 * T.n_atoms : xb + (size_t)s_off[t + 1] * 3;
+                    const float* xn = rl + 1 < n ? x + 3 * h.n_atoms : xb + (size_t)s_off[t + 1] * 3;
 #pragma unroll
                     for (int c = 0; c < 3; ++c) PNX[q][c] = xn[3 * iN + c];
                 }
@@ -863,11 +880,11 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
                     cross_acc(s6, x[3 * i] - cx, x[3 * i + 1] - cy, x[3 * i + 2] - cz, g[3 * i], g[3 * i + 1],
                               g[3 * i + 2]);
                 };
-                for (int i = 0; i < T.n_N; ++i) acc(RN[q], i);
-                for (int i = T.n_N; i < T.n_N + T.n_CA; ++i) acc(RA[q], i);
-                for (int i = T.first_C; i < T.n_atoms; ++i) acc(RC[q], i);
+                for (int i = 0; i < h.n_N; ++i) acc(RN[q], i);
+                for (int i = h.n_N; i < h.n_N + h.n_CA; ++i) acc(RA[q], i);
+                for (int i = h.first_C; i < h.n_atoms; ++i) acc(RC[q], i);
                 float br[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                for (int gi = T.n_groups - 1; gi >= 0; --gi) {
+                for (int gi = h.n_groups - 1; gi >= 0; --gi) {
                     const FAGroup gr = load_group(T.g[gi]);
                     for (int i = gr.first_atom; i < gr.end_atom; ++i) acc(br, i);
                     if (gr.slot >= 0) {
@@ -892,7 +909,7 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
                 thr[3] += s6[3] + fmaf(dy, s6[2], -dz * s6[1]);
                 thr[4] += s6[4] + fmaf(dz, s6[0], -dx * s6[2]);
                 thr[5] += s6[5] + fmaf(dx, s6[1], -dy * s6[0]);
-                off += T.n_atoms;
+                off += h.n_atoms;
             }
         }
         float suf[6], tot6[6];
