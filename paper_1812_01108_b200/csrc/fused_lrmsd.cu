@@ -428,19 +428,55 @@ cudaError_t bbp_lrmsd_fused_launch(const BBArgs& a, float* grad_angles, cudaStre
 }
 
 // dL/dalpha = dL/dLRMSD[b] * dLRMSD/dalpha (the autograd backward of the fused pass).
+// y[b][i] = s[b] x[b][i]: blockIdx.y = chain (no index division), 16-byte vectors
+// when the row and the pointers allow it.
+template <bool kVec>
 __global__ void chain_scale_kernel(const float* __restrict__ x, const float* __restrict__ s, int per_chain,
-                                   long n, float* __restrict__ y) {
+                                   float* __restrict__ y) {
     pdl_wait();
     pdl_trigger();
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
-        y[i] = x[i] * __ldg(s + i / per_chain);
+    const int b = blockIdx.y;
+    const float f = __ldg(s + b);
+    const size_t base = (size_t)b * per_chain;
+    if (kVec) {
+        const float4* x4 = reinterpret_cast<const float4*>(x + base);
+        float4* y4 = reinterpret_cast<float4*>(y + base);
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < per_chain / 4; i += gridDim.x * blockDim.x) {
+            float4 v = __ldg(x4 + i);
+            v.x *= f; v.y *= f; v.z *= f; v.w *= f;
+            y4[i] = v;
+        }
+    } else {
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < per_chain; i += gridDim.x * blockDim.x)
+            y[base + i] = __ldg(x + base + i) * f;
+    }
 }
 cudaError_t chain_scale_launch(const float* x, const float* s, int B, int per_chain, float* y, cudaStream_t st) {
-    const long n = long(B) * per_chain;
-    if (n == 0) return cudaSuccess;
-    const int grid = int(std::min<long>((n + 255) / 256, 8L * device_sm_count()));
+    if (B == 0 || per_chain == 0) return cudaSuccess;
+    const bool vec = per_chain % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+    const int items = vec ? per_chain / 4 : per_chain;
+    const int nt = 128;
+    // enough CTAs per chain to cover ~8 waves of the SMs, at most one item per thread
+    const int per = std::max(1, std::min((items + nt - 1) / nt, (8 * device_sm_count() + B - 1) / B));
     // programmatic dependent launch: it usually follows the fused pass directly
-    return launch_bbp(chain_scale_kernel, grid, 256, BBPLaunch{0, true}, st, x, s, per_chain, n, y);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    for (int b0 = 0; b0 < B; b0 += 65535) {  // gridDim.y <= 65535 chains per launch
+        const int nb = std::min(B - b0, 65535);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(per, nb);
+        cfg.blockDim = dim3(nt);
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const size_t o = (size_t)b0 * per_chain;
+        const cudaError_t e = vec ? cudaLaunchKernelEx(&cfg, chain_scale_kernel<true>, x + o, s + b0, per_chain, y + o)
+                                  : cudaLaunchKernelEx(&cfg, chain_scale_kernel<false>, x + o, s + b0, per_chain, y + o);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 #ifdef TPL_PROFILE_PHASES

@@ -193,3 +193,21 @@ def test_one_pass_api_backward_scales(tpl, oracle_lib):
     g = a.grad.cpu().numpy()
     for b in range(B):
         assert np.abs(g[b] - G[b]).max() / np.abs(G[b]).max() <= 1e-3
+
+
+@pytest.mark.parametrize("B,per,shift", [(3, 7, 0), (5, 2100, 0), (4, 2100, 1), (1, 4, 0), (300, 36, 0)])
+def test_chain_scale_values(tpl, B, per, shift):
+    """tpl_chain_scale (the autograd backward of the one-pass LRMSD): y[b] = s[b] x[b]
+    exactly, on the 16-byte vector path (per % 4 == 0, aligned) and the scalar one
+    (odd rows, or views shifted off 16-byte alignment)."""
+    from paper_1812_01108_b200 import _abi
+
+    g = torch.Generator().manual_seed(B * 1000 + per + shift)
+    xb = torch.randn(B * per + shift, generator=g).cuda()
+    x = xb[shift:].view(B, per)
+    s = torch.randn(B, generator=g).cuda()
+    yb = torch.full((B * per + shift,), float("nan"), device="cuda")
+    y = yb[shift:].view(B, per)
+    _abi.tpl_chain_scale(x, s, y)
+    torch.cuda.synchronize()
+    assert torch.equal(y.cpu(), x.cpu() * s.cpu()[:, None])
