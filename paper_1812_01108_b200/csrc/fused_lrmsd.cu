@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const f
     constexpr int XB = (16 + 36 * TILE + 16 + 15) & ~15;
     extern __shared__ __align__(16) char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);                  // [0] angles, [1 + w] target pieces
-    double* s_red = reinterpret_cast<double*>(smem + 8 * (NW + 1) + 8);  // NW x 17 moments (+ pad)
+    double* s_red = reinterpret_cast<double*>(smem + 8 * (NW + 1) + 8);  // 6 NW barycentre + 9 NW R sums (+ pad)
     float* s_sol = reinterpret_cast<float*>(s_red + NW * 17 + 1);       // 16 state + value
     float* scratch = s_sol + 32;                                         // 2 NW 12 + 12 (affine scan)
     float* s_total = scratch + 2 * NW * 12;
@@ -214,11 +214,11 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const f
         by = __fmul2_rn(__fadd2_rn(__fadd2_rn(w, f2(-dcy)), f2(-kyy)), v);
         bz = __fmul2_rn(__fadd2_rn(__fadd2_rn(t, f2(-dcz)), f2(-kz)), v);
     };
-    // ---- 2b. centred second moments: R = sum x~ y~^T, sum |x~|^2, sum |y~|^2 (step 1 of §4)
+    // ---- 2b. centred correlation R = sum x~ y~^T (step 1 of §4)
     {
-        float2 m[11];
+        float2 m[9];
 #pragma unroll
-        for (int k = 0; k < 11; ++k) m[k] = f2(0.f);
+        for (int k = 0; k < 9; ++k) m[k] = f2(0.f);
 #pragma unroll
         for (int i = 0; i < 3 * R; ++i) {
             float2 ax, ay, az, bx, by, bz;
@@ -226,8 +226,6 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const f
             m[0] = __ffma2_rn(ax, bx, m[0]); m[1] = __ffma2_rn(ax, by, m[1]); m[2] = __ffma2_rn(ax, bz, m[2]);
             m[3] = __ffma2_rn(ay, bx, m[3]); m[4] = __ffma2_rn(ay, by, m[4]); m[5] = __ffma2_rn(ay, bz, m[5]);
             m[6] = __ffma2_rn(az, bx, m[6]); m[7] = __ffma2_rn(az, by, m[7]); m[8] = __ffma2_rn(az, bz, m[8]);
-            m[9] = __ffma2_rn(ax, ax, __ffma2_rn(ay, ay, __ffma2_rn(az, az, m[9])));
-            m[10] = __ffma2_rn(bx, bx, __ffma2_rn(by, by, __ffma2_rn(bz, bz, m[10])));
         }
         // fp64 from the thread partials on: R's rounding sets U's, and near a perfect
         // superposition the gradient's residuals x~ - U^T y~ are tiny (fp32 warp sums
@@ -239,37 +237,25 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const f
 #pragma unroll
             for (int d = 16; d > 0; d >>= 1) c[k] += __shfl_down_sync(0xffffffffu, c[k], d);
         }
-        float e[2] = {m[9].x + m[9].y, m[10].x + m[10].y};  // e0 only starts the iteration: fp32
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) e[k] += __shfl_down_sync(0xffffffffu, e[k], d);
-        }
         TPL_STAMP(10);
-        __syncthreads();  // every thread has read the barycentre sums
-        if (lane == 0) {
+        if (lane == 0) {  // after the barycentre sums (s_red[0, 6 NW)): no barrier between
 #pragma unroll
-            for (int k = 0; k < 9; ++k) s_red[11 * warp + k] = c[k];
-            s_red[11 * warp + 9] = double(e[0]);
-            s_red[11 * warp + 10] = double(e[1]);
+            for (int k = 0; k < 9; ++k) s_red[6 * NW + 9 * warp + k] = c[k];
         }
     }
     __syncthreads();
     TPL_STAMP(3);
-    // ---- 3. steps 2-3 of §4 on one thread (fp64): T, its largest eigenpair, U.  The
-    //      moments are centred, so the barycentres handed to the solver are 0.
-    if (tid == 0) {
-        double Rm[3][3], sxx = 0.0, syy = 0.0;
+    // ---- 3. steps 2-3 of §4 on warp 0 (fp64): T, its largest eigenpair (the root
+    //      bracketed across the lanes), U.  The moments are centred, so the barycentres
+    //      handed to the solver are 0.
+    if (warp == 0) {
+        double Rm[3][3];
         for (int k = 0; k < 9; ++k) {
             double v = 0.0;
-            for (int w = 0; w < NW; ++w) v += s_red[11 * w + k];
+            for (int w = 0; w < NW; ++w) v += s_red[6 * NW + 9 * w + k];
             Rm[k / 3][k % 3] = v;
         }
-        for (int w = 0; w < NW; ++w) {
-            sxx += s_red[11 * w + 9];
-            syy += s_red[11 * w + 10];
-        }
-        lrmsd_rotation(Rm, 0.5 * (sxx + syy), s_sol);  // U in s_sol[0..8]
+        lrmsd_rotation_warp(Rm, s_sol);  // U in s_sol[0..8]
     }
     __syncthreads();
     TPL_STAMP(4);

@@ -130,6 +130,41 @@ static __device__ __forceinline__ double det4(const double a[4][4]) {
     return s0 * c5 - s1 * c4 + s2 * c3 + s3 * c2 - s4 * c1 + s5 * c0;
 }
 
+// Unit eigenvector of the symmetric 4x4 T for its (simple) eigenvalue l: the largest
+// column of adj(T - l I), first nonzero component > 0 (as the oracle).  False when the
+// adjugate vanishes (a degenerate pair: the caller falls back to Jacobi).
+static __device__ __forceinline__ bool sym4_vector_at(const double T[4][4], double l, double q[4]) {
+    double M[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) M[i][j] = T[i][j] - (i == j ? l : 0.0);
+    // adj(M)[i][j] = (-1)^(i+j) det(M without row j, column i); keep the largest column
+    double A[4][4];
+    adj4(M, A);
+    double best[4] = {0, 0, 0, 0}, bn = -1.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const double n2 = A[0][j] * A[0][j] + A[1][j] * A[1][j] + A[2][j] * A[2][j] + A[3][j] * A[3][j];
+        const bool better = n2 > bn;
+        bn = better ? n2 : bn;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) best[i] = better ? A[i][j] : best[i];
+    }
+    TPL_SCLK(4);
+    const double scale = fmax(fabs(l), 1e-300);
+    if (!(bn > 1e-24 * scale * scale * scale * scale * scale * scale)) return false;  // degenerate: Jacobi
+    const double inv = rsqrt_full(bn);
+    // first nonzero component > 0 (as the oracle)
+    const double lead = fabs(best[0]) * inv >= 1e-12 ? best[0]
+                      : fabs(best[1]) * inv >= 1e-12 ? best[1]
+                      : fabs(best[2]) * inv >= 1e-12 ? best[2] : best[3];
+    const double sg = lead < 0.0 ? -inv : inv;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[i] = best[i] * sg;
+    return true;
+}
+
 // Largest eigenpair of the traceless symmetric 4x4 T of P:220-227, the fast way:
 // Newton on its characteristic polynomial lambda^4 + c2 lambda^2 + c1 lambda + c0
 // (c2 = -2 |R|_F^2, c1 = -8 det R, c0 = det T) from the upper bound e0 =
@@ -184,36 +219,102 @@ static __device__ bool sym4_max_eigen_newton(const double T[4][4], const double 
     }
     TPL_SCLK(3);
     *lam = l;
-    double M[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) M[i][j] = T[i][j] - (i == j ? l : 0.0);
-    // adj(M)[i][j] = (-1)^(i+j) det(M without row j, column i); keep the largest column
-    double A[4][4];
-    adj4(M, A);
-    double best[4] = {0, 0, 0, 0}, bn = -1.0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const double n2 = A[0][j] * A[0][j] + A[1][j] * A[1][j] + A[2][j] * A[2][j] + A[3][j] * A[3][j];
-        const bool better = n2 > bn;
-        bn = better ? n2 : bn;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) best[i] = better ? A[i][j] : best[i];
-    }
-    TPL_SCLK(4);
-    const double scale = fmax(fabs(l), 1e-300);
-    if (!(bn > 1e-24 * scale * scale * scale * scale * scale * scale)) return false;  // degenerate: Jacobi
-    const double inv = rsqrt_full(bn);
-    // first nonzero component > 0 (as the oracle)
-    const double lead = fabs(best[0]) * inv >= 1e-12 ? best[0]
-                      : fabs(best[1]) * inv >= 1e-12 ? best[1]
-                      : fabs(best[2]) * inv >= 1e-12 ? best[2] : best[3];
-    const double sg = lead < 0.0 ? -inv : inv;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) q[i] = best[i] * sg;
+    const bool ok = sym4_vector_at(T, l, q);
     TPL_SCLK(5);
-    return true;
+    return ok;
+}
+
+// Largest root of lambda^4 + c2 lambda^2 + c1 lambda + c0 (T's characteristic
+// polynomial, c2 = -2 |R|_F^2 < 0), cooperatively on the 32 lanes of one warp (same
+// coefficients in every lane; every lane returns the root).  In mu = lambda / |R|_F
+// every root lies in [-sqrt 3, sqrt 3] and lambda_max >= 0 (T is traceless):
+//  1. three rounds of 32-section of [0, sqrt 3] in fp64, one sample per lane.  A
+//     sample lies above every root iff p, p', p'' > 0 there (the third derivative
+//     24 mu > 0 and the fourth 24 > 0: Budan-Fourier, no sign change = no root above;
+//     above the largest root every derivative is positive, since their roots interlace
+//     below it), so the lowest such sample brackets lambda_max to 1/32 per round.
+//  2. Laguerre from the bracket's top (within 5e-5 relative): p in fp64, the step as
+//     an fp32 correction -- 1-2 steps (every root is real, so the iteration decreases
+//     monotonically onto the largest one).
+// tools/micro/polish.cu: <= ~1100 cycles against 1100-4400 for fp64 Laguerre from the
+// bound; lambda within ~1e-10 relative of the fp64 iteration's.
+static __device__ __forceinline__ double quartic_max_root_warp(double c2, double c1, double c0) {
+    const double s2 = -0.5 * c2;
+    if (!(s2 > 1e-200)) return 0.0;  // R = 0: T = 0
+    const double is = rsqrt_full(s2), sc = s2 * is;
+    const double b1 = c1 * is * is * is, b0 = c0 * (is * is) * (is * is);
+    const int lane = threadIdx.x & 31;
+    double lo = 0.0, hi = 1.7320508075688772 * (1.0 + 1e-9);
+#pragma unroll
+    for (int round = 0; round < 3; ++round) {
+        const double w = (hi - lo) * (1.0 / 32.0);
+        const double mu = fma(w, double(lane + 1), lo);  // lane 31: hi
+        const double m2 = mu * mu;
+        const double p = fma(m2 - 2.0, m2, fma(b1, mu, b0));
+        const double dp = fma(fma(4.0, m2, -4.0), mu, b1);
+        const double ddp = fma(12.0, m2, -4.0);
+        const unsigned above = __ballot_sync(0xffffffffu, p > 0.0 && dp > 0.0 && ddp > 0.0);
+        const int first = above ? __ffs(above) - 1 : 31;  // the samples above every root: an upper set
+        hi = fma(w, double(first + 1), lo);
+        lo = hi - w;
+    }
+    double mu = hi;
+    const float b1f = float(b1);
+    for (int it = 0; it < 12; ++it) {
+        const double m2 = mu * mu;
+        const double p = fma(m2 - 2.0, m2, fma(b1, mu, b0));
+        if (!(p > 0.0)) break;  // on the root (or just below it by rounding)
+        const float mf = float(mu), pf = float(p), m2f = mf * mf;
+        const float dp = fmaf(fmaf(4.f, m2f, -4.f), mf, b1f);
+        const float ddp = fmaf(12.f, m2f, -4.f);
+        // Laguerre (degree 4): step = 4 p / (p' + sqrt(3 (3 p'^2 - 4 p p'')))
+        const float disc = fmaxf(fmaf(9.f * dp, dp, -12.f * pf * ddp), 0.f);
+        const float den = dp + disc * rsqrtf(fmaxf(disc, 1e-37f));
+        if (!(den > 0.f)) break;
+        const float step = 4.f * pf * __frcp_rn(den);
+        mu -= double(step);
+        if (double(step) <= 1e-9 * fabs(mu)) break;  // the next step would be below ~1e-16
+    }
+    return mu * sc;
+}
+
+// U (row-major fp32) from the unit quaternion q (the eigenvector of P:220-227)
+static __device__ __forceinline__ void rotation_from_q(const double q[4], float* U, float* Ulo) {
+    const double q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
+    const double Ud[9] = {q0 * q0 + q1 * q1 - q2 * q2 - q3 * q3, 2 * (q1 * q2 - q0 * q3), 2 * (q1 * q3 + q0 * q2),
+                          2 * (q1 * q2 + q0 * q3), q0 * q0 - q1 * q1 + q2 * q2 - q3 * q3, 2 * (q2 * q3 - q0 * q1),
+                          2 * (q1 * q3 - q0 * q2), 2 * (q2 * q3 + q0 * q1), q0 * q0 - q1 * q1 - q2 * q2 + q3 * q3};
+    for (int k = 0; k < 9; ++k) {
+        U[k] = float(Ud[k]);
+        if (Ulo) Ulo[k] = float(Ud[k] - double(U[k]));  // U = U + Ulo to ~1e-14
+    }
+}
+
+// lrmsd_rotation on one whole warp (every lane passes the same R; lane 0 writes U):
+// the largest root by quartic_max_root_warp, then the adjugate eigenvector.
+static __device__ __noinline__ void lrmsd_rotation_warp(const double R[3][3], float* U) {
+    double T[4][4] = {
+        {R[0][0] + R[1][1] + R[2][2], R[1][2] - R[2][1], R[2][0] - R[0][2], R[0][1] - R[1][0]},
+        {R[1][2] - R[2][1], R[0][0] - R[1][1] - R[2][2], R[0][1] + R[1][0], R[0][2] + R[2][0]},
+        {R[2][0] - R[0][2], R[0][1] + R[1][0], -R[0][0] + R[1][1] - R[2][2], R[1][2] + R[2][1]},
+        {R[0][1] - R[1][0], R[0][2] + R[2][0], R[1][2] + R[2][1], -R[0][0] - R[1][1] + R[2][2]},
+    };
+    double c2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) c2 += R[a][c] * R[a][c];
+    c2 *= -2.0;
+    const double c1 = -8.0 * det3(R[0][0], R[0][1], R[0][2], R[1][0], R[1][1], R[1][2], R[2][0], R[2][1], R[2][2]);
+    const double c0 = det4(T);
+    double lam = quartic_max_root_warp(c2, c1, c0), q[4];
+    if (!sym4_vector_at(T, lam, q)) {
+        double A[4][4];
+        for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 4; ++j) A[i][j] = T[i][j];
+        sym4_max_eigen(A, &lam, q);
+    }
+    if ((threadIdx.x & 31) == 0) rotation_from_q(q, U, nullptr);
 }
 
 // Step 2-3 without the value: U (row-major, fp32) of the optimal superposition from
