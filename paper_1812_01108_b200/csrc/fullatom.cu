@@ -105,12 +105,13 @@ __device__ __forceinline__ void apply4(const Aff& M, float4 r, float& ox, float&
     apply(M, r.x, r.y, r.z, ox, oy, oz);
 }
 
-// Backbone chunk of one thread: residues [rl0, rl0+RPT) of the tile.
-// Saves the local N, CA and C frames of every residue and returns the
-// chunk aggregate (product of all its transforms) in M.
+// Backbone chunk of one thread: residues [rl0, rl0+RPT) of the tile.  Returns the
+// chunk aggregate (product of all its transforms) in M and keeps the bonds' (sin,
+// cos); after the scan the thread walks its residues again from its prefix, so the
+// per-residue N, CA and C frames are never held across the scan.
 template <int RPT>
-__device__ __forceinline__ void fa_chunk(const float* s_ang, int rl0, int r0, int n, Aff& M,
-                                         Aff (&FN)[RPT], Aff (&FCA)[RPT], Aff (&FC)[RPT]) {
+__device__ __forceinline__ void fa_chunk(const float* s_ang, int rl0, int r0, int n, Aff& M, float (&bs)[RPT][3],
+                                         float (&bc)[RPT][3]) {
     M = aff_identity();
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
@@ -119,18 +120,10 @@ __device__ __forceinline__ void fa_chunk(const float* s_ang, int rl0, int r0, in
         if (rl < n) {
             // omega_{j-1} (C_{j-1} -> N_j; R_0 = I for j = 0), phi_j (-> CA_j), psi_j (-> C_j)
             const float x[3] = {j > 0 ? s_ang[8 * rl - 6] : 0.f, s_ang[8 * rl + 0], s_ang[8 * rl + 1]};
-            float s[3], c[3];
-            tpl_sincos_n<3>(x, s, c);
-            if (j > 0) aff_bond_bb<0>(M, c[0], s[0]);
-            FN[q] = M;
-            aff_bond_bb<1>(M, c[1], s[1]);
-            FCA[q] = M;
-            aff_bond_bb<2>(M, c[2], s[2]);
-            FC[q] = M;
-        } else {
-            FN[q] = M;
-            FCA[q] = M;
-            FC[q] = M;
+            tpl_sincos_n<3>(x, bs[q], bc[q]);
+            if (j > 0) aff_bond_bb<0>(M, bc[q][0], bs[q][0]);
+            aff_bond_bb<1>(M, bc[q][1], bs[q][1]);
+            aff_bond_bb<2>(M, bc[q][2], bs[q][2]);
         }
     }
 }
@@ -245,8 +238,8 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
         }
 
         Aff M;
-        Aff FN[RPT], FCA[RPT], FC[RPT];
-        fa_chunk<RPT>(s_ang, rl0, r0, n, M, FN, FCA, FC);
+        float bs[RPT][3], bc[RPT][3];
+        fa_chunk<RPT>(s_ang, rl0, r0, n, M, bs, bc);
         if (kNS >= 1) aff_orthonormalize(M);
         // policies 1 / 3: the (quaternion, translation) scan of packed.cuh (renormalised every
         // combine, 7 floats per shuffle level; reading Q25); 0 / 2: the 3x4 affine scan
@@ -262,15 +255,19 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
         const Span so = make_span(coords + (size_t)carry_atoms * 3, n_tile_atoms * 12);
         float* s_out = reinterpret_cast<float*>(s_out_base + so.mis());
         int off = off0 - carry_atoms;  // tile-local atom index of the thread's first atom
+        Aff Gb = P;                     // the chain walked again from the thread's prefix
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
             const int rl = rl0 + q;
             if (rl < n) {
                 const FAType& T = s_types[typ[q]];
                 const FAHead h = load_head(T);
-                const Aff gN = aff_compose(P, FN[q]);
-                const Aff gCA = aff_compose(P, FCA[q]);
-                const Aff gC = aff_compose(P, FC[q]);
+                if (r0 + rl > 0) aff_bond_bb<0>(Gb, bc[q][0], bs[q][0]);
+                const Aff gN = Gb;
+                aff_bond_bb<1>(Gb, bc[q][1], bs[q][1]);
+                const Aff gCA = Gb;
+                aff_bond_bb<2>(Gb, bc[q][2], bs[q][2]);
+                const Aff gC = Gb;
                 const float* ang = s_ang + 8 * rl;
                 float* o = s_out + 3 * off;
                 int k = 0;
@@ -464,8 +461,8 @@ __global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_
                 return;
             }
             Aff M;
-            Aff FN[RPT], FCA[RPT], FC[RPT];
-            fa_chunk<RPT>(s_ang, rl0, r0, TILE, M, FN, FCA, FC);
+            float bs[RPT][3], bc[RPT][3];
+            fa_chunk<RPT>(s_ang, rl0, r0, TILE, M, bs, bc);
             if (kNS >= 1) aff_orthonormalize(M);
             block_exclusive_scan<NT, kNS>(M, carry, s_scan, s_total);
             carry = load_aff(s_total);
@@ -543,8 +540,8 @@ __global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_
         span_load_edges_f32(sg, s_g_base);
 
         Aff M;
-        Aff FN[RPT], FCA[RPT], FC[RPT];
-        fa_chunk<RPT>(s_ang, rl0, r0, n, M, FN, FCA, FC);
+        float bs[RPT][3], bc[RPT][3];
+        fa_chunk<RPT>(s_ang, rl0, r0, n, M, bs, bc);
         if (kNS >= 1) aff_orthonormalize(M);
         const Aff P = block_exclusive_scan<NT, kNS>(M, carry, s_scan, s_total);  // contains __syncthreads
         mbar_wait(bar, phase);
@@ -559,15 +556,19 @@ __global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_
         ResSums RS[RPT];
         float thr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         int off = off0 - carry_atoms;
+        Aff Gb = P;  // the chain walked again from the thread's prefix
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
             const int rl = rl0 + q;
             if (rl < n) {
                 const FAType& T = s_types[typ[q]];
                 const FAHead h = load_head(T);
-                const Aff gN = aff_compose(P, FN[q]);
-                const Aff gCA = aff_compose(P, FCA[q]);
-                const Aff gC = aff_compose(P, FC[q]);
+                if (r0 + rl > 0) aff_bond_bb<0>(Gb, bc[q][0], bs[q][0]);
+                const Aff gN = Gb;
+                aff_bond_bb<1>(Gb, bc[q][1], bs[q][1]);
+                const Aff gCA = Gb;
+                aff_bond_bb<2>(Gb, bc[q][2], bs[q][2]);
+                const Aff gC = Gb;
                 float* go = s_go + 8 * rl;
                 go[0] = go[1] = 0.f;
 #pragma unroll
@@ -1009,10 +1010,10 @@ static size_t fa_bwd_smem(int n_types, int max_atoms) {
     return fa_fwd_smem<NT, RPT>(n_types, max_atoms) + Lay::go_bytes;
 }
 
-template <int NT, int NS, bool TS, int MINB>
+template <int NT, int NS, bool TS, int MINB, int RPT = 1>
 static cudaError_t fa_fwd_v(const FAArgs& a, cudaStream_t st) {
-    auto k = fa_forward_kernel<NT, 1, NS, TS, MINB>;
-    const size_t sm = fa_fwd_smem<NT, 1>(a.n_types, a.max_atoms, TS);
+    auto k = fa_forward_kernel<NT, RPT, NS, TS, MINB>;
+    const size_t sm = fa_fwd_smem<NT, RPT>(a.n_types, a.max_atoms, TS);
     static LaunchCfg cfg;  // one grid CTA per chain: only the shared-memory opt-in is used
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
@@ -1020,33 +1021,48 @@ static cudaError_t fa_fwd_v(const FAArgs& a, cudaStream_t st) {
 }
 // TPL_FAF=NTxTSxMINB (tuning) or the default.
 struct FAFShape {
-    int nt, ts, minb;
+    int nt, ts, minb, rpt;
 };
 static FAFShape faf_shape(int B, int Lmax) {
-    static FAFShape env{-1, 0, 0};
+    static FAFShape env{-1, 0, 0, 1};
     if (env.nt < 0) {
-        env = {0, 0, 0};
+        env = {0, 0, 0, 1};
         if (const char* e = std::getenv("TPL_FAF")) {
-            FAFShape s{0, 1, 2};
-            if (std::sscanf(e, "%dx%dx%d", &s.nt, &s.ts, &s.minb) == 3) env = s;
+            FAFShape s{0, 1, 2, 1};
+            if (std::sscanf(e, "%dx%dx%dx%d", &s.nt, &s.ts, &s.minb, &s.rpt) >= 3) env = s;
         }
     }
     if (env.nt) return env;
-    // measured (tools/gpu_faf.sh): few chains -> 256 threads, table in shared
-    // memory; many chains -> 128 threads, table through L1, 6 CTAs/SM
-    // at most one chain per SM and chains longer than 256 residues: one 512-thread
-    // tile per chain instead of two serial 256-residue tiles (config 3: 13.7 -> 10.6 us)
-    if (B <= 148 && Lmax > 256) return FAFShape{512, 1, 1};
-    return B <= 2 * 148 ? FAFShape{256, 1, 2} : FAFShape{128, 0, 6};
+    // measured (TPL_FAF sweeps, same box): few chains -> 256 threads, table in shared
+    // memory; at most one chain per SM and chains longer than 256 residues: one
+    // 512-thread tile per chain instead of two serial 256-residue tiles (config 3:
+    // 13.7 -> 10.6 us); many chains -> table through L1 and either 128 threads x 1
+    // residue at 6 CTAs/SM or 64 threads x 2 residues at 8 CTAs/SM (the block scan,
+    // a third of the kernel's instructions at one residue per thread, amortised over
+    // two).  64 x 2 wins for long chains in large batches (x 500: 1024 chains 66.0 ->
+    // 52.6 us, 2048 104.9 -> 100.8, 8192 360.5 -> 331.7) and loses for shorter ones
+    // (x 300: 512 chains 25.9 -> 30.2 us, 4096 134.4 -> 138.8).
+    if (B <= 148 && Lmax > 256) return FAFShape{512, 1, 1, 1};
+    if (B <= 2 * 148) return FAFShape{256, 1, 2, 1};
+    return B >= 1024 && Lmax > 384 ? FAFShape{64, 0, 8, 2} : FAFShape{128, 0, 6, 1};
 }
 template <int NS>
 static cudaError_t fa_fwd(const FAArgs& a, cudaStream_t st) {
     const FAFShape s = faf_shape(a.B, a.Lmax);
 #define TPL_FAF(NT_, TS_, MB_) \
-    if (s.nt == NT_ && s.ts == TS_ && s.minb == MB_) return fa_fwd_v<NT_, NS, TS_, MB_>(a, st);
+    if (s.nt == NT_ && s.ts == TS_ && s.minb == MB_ && s.rpt == 1) return fa_fwd_v<NT_, NS, TS_, MB_>(a, st);
     TPL_FAF(256, 1, 2) TPL_FAF(256, 0, 2) TPL_FAF(256, 0, 3) TPL_FAF(256, 1, 3) TPL_FAF(512, 1, 1)
     TPL_FAF(128, 1, 4) TPL_FAF(128, 0, 4) TPL_FAF(128, 0, 6) TPL_FAF(128, 1, 6)
 #undef TPL_FAF
+#define TPL_FAF2(NT_, TS_, MB_) \
+    if (s.nt == NT_ && s.ts == TS_ && s.minb == MB_ && s.rpt == 2) return fa_fwd_v<NT_, NS, TS_, MB_, 2>(a, st);
+    TPL_FAF2(64, 0, 8) TPL_FAF2(64, 0, 6) TPL_FAF2(128, 0, 4) TPL_FAF2(128, 0, 3) TPL_FAF2(64, 1, 5)
+    TPL_FAF2(64, 0, 7) TPL_FAF2(256, 1, 1) TPL_FAF2(256, 1, 2) TPL_FAF2(128, 1, 2) TPL_FAF2(128, 1, 4)
+#undef TPL_FAF2
+#define TPL_FAF3(NT_, TS_, MB_) \
+    if (s.nt == NT_ && s.ts == TS_ && s.minb == MB_ && s.rpt == 3) return fa_fwd_v<NT_, NS, TS_, MB_, 3>(a, st);
+    TPL_FAF3(64, 0, 5) TPL_FAF3(64, 0, 4) TPL_FAF3(32, 0, 8)
+#undef TPL_FAF3
     return cudaErrorInvalidConfiguration;
 }
 template <int NS>

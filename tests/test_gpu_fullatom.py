@@ -127,6 +127,24 @@ def test_config5_shape_sampled(tpl, oracle_lib, table, xyz):
     _check(oracle_lib, table, ang, rt, lengths, grad, coords, gang, apc, chains=sample)
 
 
+def test_large_batch_ragged_two_residues_per_thread(tpl, oracle_lib, table):
+    """The large-batch forward shape (64 threads x 2 residues per thread, chosen for >= 1024
+    chains longer than 384 residues): ragged lengths so that runs end mid-pair, tiles end
+    mid-run and single-residue chains occur; parity on the edge chains and a sample."""
+    tables = tpl.Tables(table)
+    B, L = 1024, 520
+    ang, rt, _ = synth.fullatom_inputs(5, B=B, L=L)
+    lengths = synth.lengths_uniform(B, 1, L, 7301)
+    edge = {0: L, 1: 1, 2: 2, 3: 127, 4: 128, 5: 129, 6: 255, 7: 257, 8: 385}
+    for b, n in edge.items():
+        lengths[b] = n
+    coords, gang, grad, apc = _run(tpl, tables, ang, rt, lengths, lambda B, S: synth.fullatom_grad(B, S, 5))
+    sample = sorted(set(edge) | set(np.random.default_rng(5).choice(B, 8, replace=False).tolist()))
+    _check(oracle_lib, table, ang, rt, lengths, grad, coords, gang, apc, chains=sample)
+    for b in sample:  # atoms past each chain's count are never written
+        assert np.isnan(coords[b, apc[b]:]).all()
+
+
 def test_backbone_atoms_match_backbone_kernel(tpl, table):
     """Fig:ErrorEstimate methodology between the two GPU models."""
     tables = tpl.Tables(table)
