@@ -698,6 +698,7 @@ __host__ __device__ constexpr int fax_table_bytes(bool tab_smem, int n_types) {
 template <int NT, int RPT, bool kDB, bool kTabSmem>
 __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_tiles) {
     constexpr int TILE = NT * RPT;
+    static_assert(TILE * kMaxAtomsPerRes < 65536, "tile-relative atom offsets are 16-bit");
     using S = FAXSmem<NT>;
     extern __shared__ __align__(16) char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
@@ -706,7 +707,9 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
     const FAType* __restrict__ s_types =
         kTabSmem ? reinterpret_cast<const FAType*>(smem + S::kTable) : a.types;
     int* s_off = reinterpret_cast<int*>(smem + S::kTable + fax_table_bytes(kTabSmem, a.n_types));
-    char* s_rt_base = reinterpret_cast<char*>(s_off) + r16(4 * (max_tiles + 1));  // the chain's restype
+    // tile-relative atom offsets fit 16 bits (< TILE * kMaxAtomsPerRes <= 8192)
+    unsigned short* s_roff = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(s_off) + r16(4 * (max_tiles + 1)));
+    char* s_rt_base = reinterpret_cast<char*>(s_roff) + r16(2 * max_tiles * NT);  // the chain's restype
     char* s_buf = s_rt_base + r16(16 + a.Lmax);
     const FAXTile lay = fax_tile_layout(TILE, a.max_atoms);
     char* s_go_base = s_buf + (kDB ? 2 : 1) * lay.total;
@@ -755,7 +758,8 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
         s_rtc = reinterpret_cast<const unsigned char*>(s_rt_base + sr.mis());
     }
 
-    // pre-pass: atom offset of every tile start (and validity of the types)
+    // pre-pass: atom offset of every tile start and of every thread's first atom within
+    // its tile (s_roff: the tile loop needs no scan of its own), validity of the types
     {
         int carry = 0;
         bool bad = false;
@@ -771,7 +775,7 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
                 }
             }
             int end;
-            block_exclusive_sum_int<NT>(cnt, carry, s_int, &end);
+            s_roff[t * NT + tid] = (unsigned short)(block_exclusive_sum_int<NT>(cnt, carry, s_int, &end) - carry);
             if (tid == 0) s_off[t] = carry;
             carry = end;
         }
@@ -824,14 +828,9 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
 
         if (tid == 0) bulk_wait_read_all();  // grad staging free (read by the previous store)
         int typ[RPT];
-        int cnt = 0;
 #pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-            typ[q] = rl0 + q < n ? s_rt[rl0 + q] : 0;
-            cnt += rl0 + q < n ? s_types[typ[q]].n_atoms : 0;
-        }
-        int tile_atoms;
-        const int off0 = block_exclusive_sum_int<NT>(cnt, 0, s_int, &tile_atoms);
+        for (int q = 0; q < RPT; ++q) typ[q] = rl0 + q < n ? s_rt[rl0 + q] : 0;
+        const int off0 = s_roff[t * NT + tid];
         const float rx = X[0], ry = X[1], rz = X[2];  // tile reference point
         if (k > 0) {  // later tiles' moment about this tile's reference
             const float dx = cpx - rx, dy = cpy - ry, dz = cpz - rz;
@@ -1101,7 +1100,7 @@ static cudaError_t fa_bwd_xyz(const FAArgs& a, cudaStream_t st) {
     constexpr int TILE = NT * RPT;
     const int max_tiles = (a.Lmax + TILE - 1) / TILE;
     const size_t sm = FAXSmem<NT>::kTable + fax_table_bytes(TS, a.n_types) + r16(4 * (max_tiles + 1)) +
-                      r16(16 + a.Lmax) + (DB ? 2 : 1) * fax_tile_layout(TILE, a.max_atoms).total + r16(32 * TILE);
+                      r16(2 * max_tiles * NT) + r16(16 + a.Lmax) + (DB ? 2 : 1) * fax_tile_layout(TILE, a.max_atoms).total + r16(32 * TILE);
     static LaunchCfg cfg;  // one grid CTA per chain: only the shared-memory opt-in is used
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
