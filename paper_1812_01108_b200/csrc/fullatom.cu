@@ -130,7 +130,7 @@ __device__ __forceinline__ void fa_chunk(const float* s_ang, int rl0, int r0, in
 
 // kTS: residue table staged in shared memory (else read through L1);
 // kMinB: __launch_bounds__ min blocks (register budget).  TPL_FAF tunes them.
-template <int NT, int RPT, int kNS, bool kTS = true, int kMinB = 2>
+template <int NT, int RPT, int kNS, bool kTS = true, int kMinB = 2, bool kDBI = true>
 __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int stage_atoms_per_res) {
     constexpr int TILE = NT * RPT;
     using S = FASmem<NT>;
@@ -142,15 +142,17 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
     float* s_total = reinterpret_cast<float*>(smem + S::kTotal);
     int* s_misc = reinterpret_cast<int*>(smem + S::kMisc);
     const FAType* __restrict__ s_types = kTS ? reinterpret_cast<const FAType*>(smem + S::kTable) : a.types;
-    char* s_ang_base = smem + S::kTable + (kTS ? r16(a.n_types * int(sizeof(FAType))) : 0);
-    char* s_rt_base = s_ang_base + Lay::ang_bytes;
-    char* s_out_base = s_rt_base + Lay::rt_bytes;
+    // kDBI: tile inputs double-buffered (angles + residue types; bar[0] / bar[1]): tile
+    // t + 1's loads fly while tile t computes
+    char* s_in_base = smem + S::kTable + (kTS ? r16(a.n_types * int(sizeof(FAType))) : 0);
+    char* s_out_base = s_in_base + 2 * (Lay::ang_bytes + Lay::rt_bytes);
 
     const int b = blockIdx.x;
     const int tid = threadIdx.x;
-    unsigned phase = 0;
+    unsigned phase = 0;  // bit i: the parity bar[i] waits for next
     if (tid == 0) {
         mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
         fence_barrier_init();
         // the residue table is immutable after tpl_tables_create: it may be
         // fetched before pdl_wait, overlapping the previous kernel's tail
@@ -182,21 +184,42 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
     int carry_atoms = 0;
     const int rl0 = tid * RPT;
     float* coords = a.coords + (size_t)b * a.atom_stride * 3;
-    for (int r0 = 0; r0 < L; r0 += TILE) {
+    auto in_spans = [&](int r0, Span& sa, Span& sr) {
+        const int n = min(TILE, L - r0), pre = r0 > 0 ? 1 : 0;
+        sa = make_span(a.angles + ((size_t)b * a.Lmax + r0 - pre) * kFASlots, (n + pre) * 32);
+        sr = make_span(a.restype + (size_t)b * a.Lmax + r0, n);
+    };
+    auto issue_in = [&](int r0, int buf) {  // thread 0
+        Span sa, sr;
+        in_spans(r0, sa, sr);
+        char* base = s_in_base + buf * (Lay::ang_bytes + Lay::rt_bytes);
+        mbar_arrive_expect_tx(bar + buf, unsigned(sa.mid + sr.mid));
+        span_load_bulk(sa, base, bar + buf);
+        span_load_bulk(sr, base + Lay::ang_bytes, bar + buf);
+    };
+    // before an early return: the prefetch in flight must land first (no bulk copy may
+    // outlive the CTA), and the stores drain
+    auto drain = [&](int r0, int buf) {
+        if (kDBI && r0 + TILE < L) mbar_wait(bar + (buf ^ 1), (phase >> (buf ^ 1)) & 1u);
+        bulk_wait_all();
+    };
+    if (tid == 0) issue_in(0, 0);
+    for (int r0 = 0, buf = 0; r0 < L; r0 += TILE, buf ^= kDBI ? 1 : 0) {
         const int n = min(TILE, L - r0);
         const int pre = r0 > 0 ? 1 : 0;
-        const Span sa = make_span(a.angles + ((size_t)b * a.Lmax + r0 - pre) * kFASlots, (n + pre) * 32);
-        const Span sr = make_span(a.restype + (size_t)b * a.Lmax + r0, n);
-        if (tid == 0) {
-            bulk_wait_read_all();
-            mbar_arrive_expect_tx(bar, unsigned(sa.mid + sr.mid));
-            span_load_bulk(sa, s_ang_base, bar);
-            span_load_bulk(sr, s_rt_base, bar);
-        }
+        Span sa, sr;
+        in_spans(r0, sa, sr);
+        char* s_ang_base = s_in_base + buf * (Lay::ang_bytes + Lay::rt_bytes);
+        char* s_rt_base = s_ang_base + Lay::ang_bytes;
+        // the other buffer (single-buffered: this one) was last read by tile t - 1,
+        // before its closing barrier
+        if (kDBI && tid == 0 && r0 + TILE < L) issue_in(r0 + TILE, buf ^ 1);
+        if (!kDBI && tid == 0 && r0 > 0) issue_in(r0, 0);
+        if (tid == 0) bulk_wait_read_all();  // the output staging is free again
         span_load_edges_f32(sa, s_ang_base);
         span_load_edges_u8(sr, s_rt_base);
-        mbar_wait(bar, phase);
-        phase ^= 1u;
+        mbar_wait(bar + buf, (phase >> buf) & 1u);
+        phase ^= 1u << buf;
         __syncthreads();
         const float* s_ang = reinterpret_cast<const float*>(s_ang_base + sa.mis()) + 8 * pre;
         const unsigned char* s_rt = reinterpret_cast<const unsigned char*>(s_rt_base + sr.mis());
@@ -225,14 +248,14 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
         if (tile_end_atoms - carry_atoms >= kBadRestype) {
             if (tid == 0) {
                 atomicOr(a.err, ERR_RESTYPE);
-                bulk_wait_all();
+                drain(r0, buf);
             }
             return;
         }
         if (tile_end_atoms > a.atom_stride) {  // the chain's atoms do not fit its row: flag, skip
             if (tid == 0) {
                 atomicOr(a.err, ERR_STRIDE);
-                bulk_wait_all();
+                drain(r0, buf);
             }
             return;
         }
@@ -397,9 +420,10 @@ __global__ void __launch_bounds__(NT, 3) fa_backward_kernel(FAArgs a, int stage_
 
     const int b = blockIdx.x;
     const int tid = threadIdx.x;
-    unsigned phase = 0;
+    unsigned phase = 0;  // bit i: the parity bar[i] waits for next
     if (tid == 0) {
         mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
         fence_barrier_init();
         // the residue table is immutable after tpl_tables_create: it may be
         // fetched before pdl_wait, overlapping the previous kernel's tail
@@ -997,10 +1021,10 @@ int fa_rpt_for(int) { return kFABwdRPT; }
 int fa_tile_for(int) { return kFABwdThreads * kFABwdRPT; }  // backward tile: sizes the workspace prefixes
 
 template <int NT, int RPT>
-static size_t fa_fwd_smem(int n_types, int max_atoms, bool ts = true) {
+static size_t fa_fwd_smem(int n_types, int max_atoms, bool ts = true, int in_bufs = 1) {
     using S = FASmem<NT>;
     using Lay = FALayout<NT, RPT>;
-    return S::kTable + (ts ? r16(n_types * int(sizeof(FAType))) : 0) + Lay::ang_bytes + Lay::rt_bytes +
+    return S::kTable + (ts ? r16(n_types * int(sizeof(FAType))) : 0) + in_bufs * (Lay::ang_bytes + Lay::rt_bytes) +
            r16(16 + 12 * max_atoms * Lay::TILE);
 }
 template <int NT, int RPT>
@@ -1009,10 +1033,10 @@ static size_t fa_bwd_smem(int n_types, int max_atoms) {
     return fa_fwd_smem<NT, RPT>(n_types, max_atoms) + Lay::go_bytes;
 }
 
-template <int NT, int NS, bool TS, int MINB, int RPT = 1>
+template <int NT, int NS, bool TS, int MINB, int RPT = 1, bool DBI = true>
 static cudaError_t fa_fwd_v(const FAArgs& a, cudaStream_t st) {
-    auto k = fa_forward_kernel<NT, RPT, NS, TS, MINB>;
-    const size_t sm = fa_fwd_smem<NT, RPT>(a.n_types, a.max_atoms, TS);
+    auto k = fa_forward_kernel<NT, RPT, NS, TS, MINB, DBI>;
+    const size_t sm = fa_fwd_smem<NT, RPT>(a.n_types, a.max_atoms, TS, DBI ? 2 : 1);
     static LaunchCfg cfg;  // one grid CTA per chain: only the shared-memory opt-in is used
     cudaError_t e = ensure_launch_cfg(cfg, k, NT, sm);
     if (e != cudaSuccess) return e;
@@ -1054,14 +1078,9 @@ static cudaError_t fa_fwd(const FAArgs& a, cudaStream_t st) {
     TPL_FAF(128, 1, 4) TPL_FAF(128, 0, 4) TPL_FAF(128, 0, 6) TPL_FAF(128, 1, 6)
 #undef TPL_FAF
 #define TPL_FAF2(NT_, TS_, MB_) \
-    if (s.nt == NT_ && s.ts == TS_ && s.minb == MB_ && s.rpt == 2) return fa_fwd_v<NT_, NS, TS_, MB_, 2>(a, st);
-    TPL_FAF2(64, 0, 8) TPL_FAF2(64, 0, 6) TPL_FAF2(128, 0, 4) TPL_FAF2(128, 0, 3) TPL_FAF2(64, 1, 5)
-    TPL_FAF2(64, 0, 7) TPL_FAF2(256, 1, 1) TPL_FAF2(256, 1, 2) TPL_FAF2(128, 1, 2) TPL_FAF2(128, 1, 4)
+    if (s.nt == NT_ && s.ts == TS_ && s.minb == MB_ && s.rpt == 2) return fa_fwd_v<NT_, NS, TS_, MB_, 2, false>(a, st);
+    TPL_FAF2(64, 0, 8) TPL_FAF2(64, 0, 6) TPL_FAF2(128, 0, 4) TPL_FAF2(256, 1, 2)
 #undef TPL_FAF2
-#define TPL_FAF3(NT_, TS_, MB_) \
-    if (s.nt == NT_ && s.ts == TS_ && s.minb == MB_ && s.rpt == 3) return fa_fwd_v<NT_, NS, TS_, MB_, 3>(a, st);
-    TPL_FAF3(64, 0, 5) TPL_FAF3(64, 0, 4) TPL_FAF3(32, 0, 8)
-#undef TPL_FAF3
     return cudaErrorInvalidConfiguration;
 }
 template <int NS>
