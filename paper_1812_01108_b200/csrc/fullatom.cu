@@ -910,6 +910,7 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
                 float br[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 for (int gi = h.n_groups - 1; gi >= 0; --gi) {
                     const FAGroup gr = load_group(T.g[gi]);
+#pragma unroll 2
                     for (int i = gr.first_atom; i < gr.end_atom; ++i) acc(br, i);
                     if (gr.slot >= 0) {
                         const int o = gr.origin, p = gr.porigin;
