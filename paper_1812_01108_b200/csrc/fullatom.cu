@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
                     else { s = gr.sa; c = gr.ca; }
                     const BondC bc{gr.ct, gr.st, gr.d};
                     aff_bond(G, c, s, bc);
+#pragma unroll 2
                     for (k = gr.first_atom; k < gr.end_atom; ++k)
                         apply4(G, r0_of(T, k), o[3 * k], o[3 * k + 1], o[3 * k + 2]);
                 }
