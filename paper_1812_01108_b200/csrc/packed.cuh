@@ -286,9 +286,9 @@ __device__ __forceinline__ Aff block_exclusive_scan_qt(const Aff& agg, float* sc
     QT ex = shfl_up_qt(a, 1);
     if (lane == 0) ex = qt_identity();
     __syncthreads();
-    QT p = qt_identity();
+    QT p = load_qt(scratch);  // the warp totals before this warp (warp 0 uses none)
 #pragma unroll
-    for (int w = 0; w < NW - 1; ++w)
+    for (int w = 1; w < NW - 1; ++w)
         if (w < warp) p = qt_compose(p, load_qt(scratch + 8 * w));
     const QT res = warp > 0 ? qt_compose(p, ex) : ex;
     // no trailing barrier: the single-tile callers never reuse the scratch
