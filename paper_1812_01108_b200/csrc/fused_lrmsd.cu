@@ -332,10 +332,11 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const f
             const float2 c0 = __fadd2_rn(T0, __ffma2_rn(make_float2(-py.x, -py.y), S2, __fmul2_rn(pz, S1)));
             const float2 c1 = __fadd2_rn(T1, __ffma2_rn(make_float2(-pz.x, -pz.y), S0, __fmul2_rn(px, S2)));
             const float2 c2 = __fadd2_rn(T2, __ffma2_rn(make_float2(-px.x, -px.y), S1, __fmul2_rn(py, S0)));
-            const float2 uu = __ffma2_rn(ux, ux, __ffma2_rn(uy, uy, __fmul2_rn(uz, uz)));
             const float2 uc = __ffma2_rn(ux, c0, __ffma2_rn(uy, c1, __fmul2_rn(uz, c2)));
-            const float2 gv = __fmul2_rn(uc, make_float2(rsqrtf(uu.x), rsqrtf(uu.y)));
             const int q = i / 3, k = i - 3 * q;
+            // the bond ending at atom i has the model's length kBBd[k] (the forward built it so):
+            // its unit axis is u / d, no rsqrt
+            const float2 gv = __fmul2_rn(uc, f2(bb_invd(k)));
             if (k == 1) { oa[3 * q] = gv.x; ob[3 * q] = gv.y; }
             else if (k == 2) { oa[3 * q + 1] = gv.x; ob[3 * q + 1] = gv.y; }
             else {
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const f
             const float c0 = ext[3] - fmaf(ny, ext[2], -nz * ext[1]);
             const float c1 = ext[4] - fmaf(nz, ext[0], -nx * ext[2]);
             const float c2 = ext[5] - fmaf(nx, ext[1], -ny * ext[0]);
-            wl_ = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * fmaf(ux, c0, fmaf(uy, c1, uz * c2));
+            wl_ = bb_invd(0) * fmaf(ux, c0, fmaf(uy, c1, uz * c2));  // C -> N bond: length kBBd[0]
         }
         ob[3 * (R - 1) + 2] = wl_;
 #pragma unroll

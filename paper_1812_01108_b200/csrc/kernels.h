@@ -25,6 +25,9 @@ constexpr int kFASlots = 8;
 constexpr float kBBct[3] = {5.208135247e-01f, 3.600333929e-01f, 4.708055854e-01f};
 constexpr float kBBst[3] = {8.536704779e-01f, 9.329394102e-01f, 8.822369576e-01f};
 constexpr float kBBd[3] = {1.330000043e+00f, 1.460000038e+00f, 1.524999976e+00f};
+// 1 / kBBd[k]: the backward's unit bond axes from coordinates (the selects fold in unrolled code)
+constexpr float kBBinvd0 = 1.f / kBBd[0], kBBinvd1 = 1.f / kBBd[1], kBBinvd2 = 1.f / kBBd[2];
+__host__ __device__ constexpr float bb_invd(int k) { return k == 0 ? kBBinvd0 : k == 1 ? kBBinvd1 : kBBinvd2; }
 struct BBConst {
     BondC b[3];
 };
