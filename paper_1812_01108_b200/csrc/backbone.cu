@@ -1124,7 +1124,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
                 grad_of(x, g, Gx[a], Gy[a], Gz[a]);
                 if (r0 + rl0 + a / 3 > 0 || a % 3 > 0) {  // atom 0 of the chain carries no angle
                     const float ux = x0 - x[-3], uy = x1 - x[-2], uz = x2 - x[-1];
-                    const float inv = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
+                    const float inv = bb_invd(a % 3);  // the model bond length ending at atom a
                     Ex[a] = ux * inv; Ey[a] = uy * inv; Ez[a] = uz * inv;
                 }
                 sum6[0] += Gx[a]; sum6[1] += Gy[a]; sum6[2] += Gz[a];
@@ -1172,7 +1172,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
                 const float c0 = su[3] - fmaf(py, su[2], -pz * su[1]);
                 const float c1 = su[4] - fmaf(pz, su[0], -px * su[2]);
                 const float c2 = su[5] - fmaf(px, su[1], -py * su[0]);
-                w_last = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * fmaf(ux, c0, fmaf(uy, c1, uz * c2));
+                w_last = bb_invd(0) * fmaf(ux, c0, fmaf(uy, c1, uz * c2));
             }
         }
 #pragma unroll
@@ -1239,7 +1239,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_ker
             if (last_tile && has_ext) {  // omega_{L-1} = e . T_n (the later segments about their N)
                 const float* xc = s_x + 3 * (3 * n - 1);
                 const float ux = cnx - xc[0], uy = cny - xc[1], uz = cnz - xc[2];
-                w = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * fmaf(ux, ext[3], fmaf(uy, ext[4], uz * ext[5]));
+                w = bb_invd(0) * fmaf(ux, ext[3], fmaf(uy, ext[4], uz * ext[5]));
             }
             s_go[3 * (n - 1) + 2] = w;
         }
@@ -1342,7 +1342,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_cl_
             Gx[a] = g[0]; Gy[a] = g[1]; Gz[a] = g[2];
             if (r0 + rl0 + a / 3 > 0 || a % 3 > 0) {  // atom 0 of the chain carries no angle
                 const float ux = x0 - x[-3], uy = x1 - x[-2], uz = x2 - x[-1];
-                const float inv = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
+                const float inv = bb_invd(a % 3);  // the model bond length ending at atom a
                 Ex[a] = ux * inv; Ey[a] = uy * inv; Ez[a] = uz * inv;
             }
             sum6[0] += Gx[a]; sum6[1] += Gy[a]; sum6[2] += Gz[a];
@@ -1417,7 +1417,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_cl_
         if (nlater > 0) {
             const float* xc = s_x + 3 * (3 * n - 1);
             const float ux = cnx - xc[0], uy = cny - xc[1], uz = cnz - xc[2];
-            w = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * fmaf(ux, ext[3], fmaf(uy, ext[4], uz * ext[5]));
+            w = bb_invd(0) * fmaf(ux, ext[3], fmaf(uy, ext[4], uz * ext[5]));
         }
         s_go[3 * (n - 1) + 2] = w;
     }
@@ -1565,7 +1565,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_dl_
                 const float c0 = carry[3] - fmaf(py, carry[2], -pz * carry[1]);
                 const float c1 = carry[4] - fmaf(pz, carry[0], -px * carry[2]);
                 const float c2 = carry[5] - fmaf(px, carry[1], -py * carry[0]);
-                gw = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * fmaf(ux, c0, fmaf(uy, c1, uz * c2));
+                gw = bb_invd(0) * fmaf(ux, c0, fmaf(uy, c1, uz * c2));
             }
             s_go[3 * (n - 1) + 2] = gw;
         }
@@ -1585,7 +1585,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks128Regs(NT)) bb_backward_xyz_dl_
                     const float gx = g[0], gy = g[1], gz = g[2];
                     if (j > 0 || kk > 0) {
                         const float ux = x0 - x[-3], uy = x1 - x[-2], uz = x2 - x[-1];
-                        const float inv = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
+                        const float inv = bb_invd(kk);  // the model bond length ending at this atom
                         const float c0 = su[3] - fmaf(py, su[2], -pz * su[1]);
                         const float c1 = su[4] - fmaf(pz, su[0], -px * su[2]);
                         const float c2 = su[5] - fmaf(px, su[1], -py * su[0]);
