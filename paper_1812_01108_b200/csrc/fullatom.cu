@@ -965,21 +965,21 @@ __global__ void __launch_bounds__(NT) fa_backward_xyz_kernel(FAArgs a, int max_t
                 for (int c = 0; c < 6; ++c) s6[c] = RC[q][c] + aft[c];
                 {
                     const float ux = kx - cx, uy = ky - cy, uz = kz - cz;
-                    go[1] = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * axis_moment(ux, uy, uz, ux, uy, uz, s6);
+                    go[1] = bb_invd(2) * axis_moment(ux, uy, uz, ux, uy, uz, s6);
                 }
                 // phi_j
 #pragma unroll
                 for (int c = 0; c < 6; ++c) s6[c] = RA[q][c] - RN[q][c] + aft[c];
                 {
                     const float ux = cx - nx, uy = cy - ny, uz = cz - nz;
-                    go[0] = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) * axis_moment(ux, uy, uz, 0.f, 0.f, 0.f, s6);
+                    go[0] = bb_invd(1) * axis_moment(ux, uy, uz, 0.f, 0.f, 0.f, s6);
                 }
                 // omega_j: C_j -> N_{j+1}, later residues
                 float gw = 0.f;
                 if (j + 1 < L) {
                     const float px = PNX[q][0], py = PNX[q][1], pz = PNX[q][2];
                     const float ux = px - kx, uy = py - ky, uz = pz - kz;
-                    gw = rsqrtf(fmaf(ux, ux, fmaf(uy, uy, uz * uz))) *
+                    gw = bb_invd(0) *
                          axis_moment(ux, uy, uz, px - cx, py - cy, pz - cz, aft);
                 }
                 go[2] = gw;
