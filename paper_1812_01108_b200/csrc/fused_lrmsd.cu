@@ -28,6 +28,30 @@
 
 namespace tpl {
 
+// Warp sum of S (a power of two, 8 or 16) doubles per lane by recursive halving: at
+// each level a lane sends the half of its slots its partner keeps and adds the half it
+// receives (S - 1 + 1 double shuffles instead of 5 S for a tree per value).  Returns the
+// warp total of slot lane / (32 / S) (every 32 / S consecutive lanes hold the same slot).
+template <int S>
+__device__ __forceinline__ double warp_sum_halving(double (&v)[S]) {
+    static_assert(S == 8 || S == 16, "8 or 16 slots");
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 16, h = S / 2; h >= 1; off >>= 1, h >>= 1) {
+        const bool up = (lane & off) != 0;  // keeps the upper half of its slots
+#pragma unroll
+        for (int k = 0; k < h; ++k) {
+            const double send = up ? v[k] : v[k + h];
+            const double keep = up ? v[k + h] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    // S slots over 32 lanes: the remaining 32 / S lanes per slot still hold partial sums
+#pragma unroll
+    for (int off = 16 / S; off >= 1; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+    return v[0];
+}
+
 template <int NT, int R, int kNS>
 __global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const float* __restrict__ angles,
                                                                        const int* __restrict__ lengths, int B,
@@ -170,17 +194,11 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const f
         // fp64 from the thread partials on: an fp32 warp sum leaves the barycentre ~3e-6 A
         // off, a shift every residual carries coherently into the suffix sums (1e-2 of the
         // gradient near a perfect superposition)
-        double c[6];
+        double c[8];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            c[k] = double(m[k].x) + double(m[k].y);
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) c[k] += __shfl_down_sync(0xffffffffu, c[k], d);
-        }
-        if (lane == 0) {
-#pragma unroll
-            for (int k = 0; k < 6; ++k) s_red[6 * warp + k] = c[k];
-        }
+        for (int k = 0; k < 8; ++k) c[k] = k < 6 ? double(m[k].x) + double(m[k].y) : 0.0;
+        const double tot = warp_sum_halving<8>(c);  // slot lane / 4
+        if ((lane & 3) == 0 && (lane >> 2) < 6) s_red[6 * warp + (lane >> 2)] = tot;
         TPL_STAMP(8);
         __syncthreads();
         TPL_STAMP(9);
@@ -230,18 +248,13 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const f
         // fp64 from the thread partials on: R's rounding sets U's, and near a perfect
         // superposition the gradient's residuals x~ - U^T y~ are tiny (fp32 warp sums
         // cost 4e-3 of gradient accuracy at a 0.05 A jitter)
-        double c[9];
+        double c[16];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) {
-            c[k] = double(m[k].x) + double(m[k].y);
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) c[k] += __shfl_down_sync(0xffffffffu, c[k], d);
-        }
+        for (int k = 0; k < 16; ++k) c[k] = k < 9 ? double(m[k].x) + double(m[k].y) : 0.0;
+        const double tot = warp_sum_halving<16>(c);  // slot lane / 2
         TPL_STAMP(10);
-        if (lane == 0) {  // after the barycentre sums (s_red[0, 6 NW)): no barrier between
-#pragma unroll
-            for (int k = 0; k < 9; ++k) s_red[6 * NW + 9 * warp + k] = c[k];
-        }
+        // after the barycentre sums (s_red[0, 6 NW)): no barrier between
+        if ((lane & 1) == 0 && (lane >> 1) < 9) s_red[6 * NW + 9 * warp + (lane >> 1)] = tot;
     }
     __syncthreads();
     TPL_STAMP(3);
