@@ -142,23 +142,29 @@ static __device__ __forceinline__ bool sym4_vector_at(const double T[4][4], doub
     // adj(M)[i][j] = (-1)^(i+j) det(M without row j, column i); keep the largest column
     double A[4][4];
     adj4(M, A);
-    double best[4] = {0, 0, 0, 0}, bn = -1.0;
+    // the largest column, first of equals, by a two-level tournament (short dependency chain)
+    double n2[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const double n2 = A[0][j] * A[0][j] + A[1][j] * A[1][j] + A[2][j] * A[2][j] + A[3][j] * A[3][j];
-        const bool better = n2 > bn;
-        bn = better ? n2 : bn;
+    for (int j = 0; j < 4; ++j)
+        n2[j] = fma(A[0][j], A[0][j], A[1][j] * A[1][j]) + fma(A[2][j], A[2][j], A[3][j] * A[3][j]);
+    const bool p1 = n2[1] > n2[0], p3 = n2[3] > n2[2];
+    const double na = p1 ? n2[1] : n2[0], nb = p3 ? n2[3] : n2[2];
+    const bool pb = nb > na;
+    const double bn = pb ? nb : na;
+    double best[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) best[i] = better ? A[i][j] : best[i];
+    for (int i = 0; i < 4; ++i) {
+        const double a = p1 ? A[i][1] : A[i][0], b = p3 ? A[i][3] : A[i][2];
+        best[i] = pb ? b : a;
     }
     TPL_SCLK(4);
-    const double scale = fmax(fabs(l), 1e-300);
-    if (!(bn > 1e-24 * scale * scale * scale * scale * scale * scale)) return false;  // degenerate: Jacobi
+    const double scale = fmax(fabs(l), 1e-300), sc2 = scale * scale;
+    if (!(bn > 1e-24 * (sc2 * sc2) * sc2)) return false;  // degenerate: Jacobi
     const double inv = rsqrt_full(bn);
-    // first nonzero component > 0 (as the oracle)
-    const double lead = fabs(best[0]) * inv >= 1e-12 ? best[0]
-                      : fabs(best[1]) * inv >= 1e-12 ? best[1]
-                      : fabs(best[2]) * inv >= 1e-12 ? best[2] : best[3];
+    // first nonzero component > 0 (as the oracle): |best_i| / |best| >= 1e-12, flags beside the rsqrt
+    const bool f0 = best[0] * best[0] >= 1e-24 * bn, f1 = best[1] * best[1] >= 1e-24 * bn,
+               f2 = best[2] * best[2] >= 1e-24 * bn;
+    const double lead = f0 ? best[0] : f1 ? best[1] : f2 ? best[2] : best[3];
     const double sg = lead < 0.0 ? -inv : inv;
 #pragma unroll
     for (int i = 0; i < 4; ++i) q[i] = best[i] * sg;
@@ -299,12 +305,10 @@ static __device__ __noinline__ void lrmsd_rotation_warp(const double R[3][3], fl
         {R[2][0] - R[0][2], R[0][1] + R[1][0], -R[0][0] + R[1][1] - R[2][2], R[1][2] + R[2][1]},
         {R[0][1] - R[1][0], R[0][2] + R[2][0], R[1][2] + R[2][1], -R[0][0] - R[1][1] + R[2][2]},
     };
-    double c2 = 0.0;
+    double rr[3];  // |R|_F^2 as three row sums (a short chain)
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) c2 += R[a][c] * R[a][c];
-    c2 *= -2.0;
+    for (int a = 0; a < 3; ++a) rr[a] = fma(R[a][0], R[a][0], fma(R[a][1], R[a][1], R[a][2] * R[a][2]));
+    const double c2 = -2.0 * ((rr[0] + rr[1]) + rr[2]);
     const double c1 = -8.0 * det3(R[0][0], R[0][1], R[0][2], R[1][0], R[1][1], R[1][2], R[2][0], R[2][1], R[2][2]);
     const double c0 = det4(T);
     double lam = quartic_max_root_warp(c2, c1, c0), q[4];
