@@ -318,7 +318,17 @@ static __device__ __noinline__ void lrmsd_rotation_warp(const double R[3][3], fl
             for (int j = 0; j < 4; ++j) A[i][j] = T[i][j];
         sym4_max_eigen(A, &lam, q);
     }
-    if ((threadIdx.x & 31) == 0) rotation_from_q(q, U, nullptr);
+    // U's nine entries on lanes 0..8, one conversion and one store each (every lane forms all
+    // nine in fp64 -- the same instructions -- and keeps its own)
+    const double q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
+    const double Ud[9] = {q0 * q0 + q1 * q1 - q2 * q2 - q3 * q3, 2 * (q1 * q2 - q0 * q3), 2 * (q1 * q3 + q0 * q2),
+                          2 * (q1 * q2 + q0 * q3), q0 * q0 - q1 * q1 + q2 * q2 - q3 * q3, 2 * (q2 * q3 - q0 * q1),
+                          2 * (q1 * q3 - q0 * q2), 2 * (q2 * q3 + q0 * q1), q0 * q0 - q1 * q1 - q2 * q2 + q3 * q3};
+    const int lane = threadIdx.x & 31;
+    double mine = Ud[0];
+#pragma unroll
+    for (int k = 1; k < 9; ++k) mine = lane == k ? Ud[k] : mine;
+    if (lane < 9) U[lane] = float(mine);
 }
 
 // Step 2-3 without the value: U (row-major, fp32) of the optimal superposition from
