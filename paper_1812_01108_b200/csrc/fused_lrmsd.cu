@@ -7,13 +7,14 @@
 //
 // Per chain (the packed layout of packed.cu: thread t owns residues
 // [2Rt, 2Rt + 2R), run A in the .x lanes, run B in the .y lanes):
-//   1. forward: pass 1, block scan of 3x4 affines, pass 2 -> atom positions x
-//      in registers (and staged in shared memory for the neighbours' axes);
-//   2. step 1 of §4: moments of (x, y - y_0) over the chain's 3L atoms -- fp32
-//      per thread (18 atoms) and per warp, fp64 across warps (shift-invariant
-//      quantities only: y is taken about its first atom, x_0 = 0 by reading Q1);
-//   3. steps 2-3 (lrmsd_math.cuh, one thread): T, its largest eigenpair, U,
-//      the value and the gradient scale 1/(N LRMSD);
+//   1. forward: pass 1, block scan in (quaternion, translation) form, pass 2 ->
+//      atom positions x in registers (and staged in shared memory for the
+//      neighbours' axes);
+//   2. step 1 of §4: barycentres of x and y (x_0 = 0 by reading Q1, y about its
+//      first atom), then the centred correlation R -- fp32 per thread (18 atoms),
+//      fp64 across threads (warp sums by recursive halving, then across warps);
+//   3. steps 2-3 (lrmsd_math.cuh, warp 0): T, its largest eigenpair (the root
+//      bracketed across the lanes), U; the value is the residuals' sum of squares;
 //   4. backward: g_i = (x~_i - U^T y~_i) / (N LRMSD) formed on the fly,
 //      S = sum_{later} g, T = sum_{later} x x g, one block suffix sum, and
 //      dLRMSD/dalpha_a = e_a . (T_a - x_a x S_a) per atom (as packed.cu).
