@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const f
         bbp_pass1<R>(s_ang, Lmax, j0, tid == 0, X, Y, Z, M);
         const Aff A = lane_x(M);
         Aff agg = aff_compose(A, lane_y(M));
-        if (kNS >= 1) aff_orthonormalize(agg);
+        if (kNS >= 2) aff_orthonormalize(agg);  // policy 1: the quaternion extraction renormalises
         const Aff P = kNS == 1 ? block_exclusive_scan_qt<NT>(agg, scratch)
                                : block_exclusive_scan<NT, kNS>(agg, aff_identity(), scratch, s_total);
         const Aff2 P2 = pack2(P, aff_compose(P, A));

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(NT, NT * R >= 512 ? 384 / NT : 512 / NT) bbp_f
     bbp_pass1<R>(s_ang, Lmax, j0, tid == 0, px, py, pz, M);
     const Aff A = lane_x(M);
     Aff agg = aff_compose(A, lane_y(M));
-    if (kNS >= 1) aff_orthonormalize(agg);
+    if (kNS >= 2) aff_orthonormalize(agg);  // policy 1: the quaternion extraction renormalises
     TPL_STAMP(3);
 
     // ---- block scan of the thread aggregates (carry: identity, one tile); policy 1
