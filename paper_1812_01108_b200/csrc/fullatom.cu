@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(NT, kMinB) fa_forward_kernel(FAArgs a, int sta
         Aff M;
         float bs[RPT][3], bc[RPT][3];
         fa_chunk<RPT>(s_ang, rl0, r0, n, M, bs, bc);
-        if (kNS >= 1) aff_orthonormalize(M);
+        if (kNS == 2) aff_orthonormalize(M);  // the quaternion scans (1, 3) renormalise at the extraction
         // policies 1 / 3: the (quaternion, translation) scan of packed.cuh (renormalised every
         // combine, 7 floats per shuffle level; reading Q25); 0 / 2: the 3x4 affine scan
         Aff P;

@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(NT, NT * R >= 512 ? 384 / NT : 512 / NT) bbp_f
         bbp_pass1<R>(s_ang, n, j0, t == 0 && tid == 0, px, py, pz, M, t > 0);
         const Aff A = lane_x(M);
         Aff agg = aff_compose(A, lane_y(M));
-        aff_orthonormalize(agg);
+        // no Newton-Schulz step: the quaternion extraction renormalises (reading Q25)
         const Aff P = block_exclusive_scan_qt_carry<NT>(agg, scratch, carry);
         const Aff2 P2 = pack2(P, aff_compose(P, A));
         float* gout = coords + ((size_t)b * 3 * Lmax + 3 * (size_t)r0) * 3;
