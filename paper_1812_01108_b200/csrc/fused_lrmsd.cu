@@ -305,10 +305,12 @@ __global__ void __launch_bounds__(NT, NT > 128 ? 1 : 2) bbp_lrmsd_kernel(const f
     S0 = make_float2(ext[0] + S0.y, ext[0]); S1 = make_float2(ext[1] + S1.y, ext[1]);
     S2 = make_float2(ext[2] + S2.y, ext[2]); T0 = make_float2(ext[3] + T0.y, ext[3]);
     T1 = make_float2(ext[4] + T1.y, ext[4]); T2 = make_float2(ext[5] + T2.y, ext[5]);
-    const double lr = sqrt(fmax(double(tot7[6]), 0.0) * rcp_full(n));
-    const float sc = lr > 1e-12 ? float(rcp_full(n * lr)) : 0.f;  // 1/(N LRMSD); 0 where LRMSD vanishes
+    // the value from the fp32 sum of squares in fp32 (correctly rounded division and sqrt)
+    const float nf = float(n);
+    const float lr = sqrtf(fmaxf(tot7[6], 0.f) / nf);
+    const float sc = lr > 1e-12f ? 1.f / (nf * lr) : 0.f;  // 1/(N LRMSD); 0 where LRMSD vanishes
     if (tid == 0 && ok) {
-        loss_out[b] = float(lr);
+        loss_out[b] = lr;
         float* st = state_out + (size_t)b * 16;
 #pragma unroll
         for (int k = 0; k < 9; ++k) st[k] = U[k];
