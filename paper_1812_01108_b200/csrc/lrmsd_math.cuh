@@ -75,16 +75,29 @@ static __device__ __noinline__ void sym4_max_eigen(double A[4][4], double* lam, 
 // Newton step on it (instead of the ~100-cycle IEEE fp64 division / sqrt sequences;
 // 20 of those made the per-chain solve ~5000 cycles, tools/micro/solve_cost.cu).
 static __device__ __forceinline__ double rcp_approx(double x) { return double(__frcp_rn(float(x))); }
-static __device__ __forceinline__ double rcp_full(double x) {
-    if (!(fabs(x) > 1e-30 && fabs(x) < 1e30)) return 1.0 / x;  // outside the fp32 range
+static __device__ __forceinline__ double rcp_inrange(double x) {
     const double r = rcp_approx(x);
     return r * fma(-x, r, 2.0);  // ~1e-14 relative
 }
+static __device__ __forceinline__ double rsqrt_inrange(double x) {
+    const double y = double(rsqrtf(float(x)));
+    return y * fma(-0.5 * x * y, y, 1.5);  // Newton: ~1e-14 relative
+}
+// Outside the fp32 range the argument is scaled by an exact power of two (|R|-derived
+// quantities reach 1e35 near a superposition of long chains); only 0, inf and NaN take
+// the IEEE fp64 sequences.
+static __device__ __forceinline__ double rcp_full(double x) {
+    const double ax = fabs(x);
+    if (ax > 1e-30 && ax < 1e30) return rcp_inrange(x);
+    if (ax >= 1e30 && ax < 1e90) return rcp_inrange(x * 0x1p-200) * 0x1p-200;
+    if (ax <= 1e-30 && ax > 1e-90) return rcp_inrange(x * 0x1p200) * 0x1p200;
+    return 1.0 / x;
+}
 static __device__ __forceinline__ double rsqrt_full(double x) {
-    if (!(x > 1e-30 && x < 1e30)) return 1.0 / sqrt(x);
-    double y = double(rsqrtf(float(x)));
-    y = y * fma(-0.5 * x * y, y, 1.5);  // Newton: ~1e-14 relative
-    return y;
+    if (x > 1e-30 && x < 1e30) return rsqrt_inrange(x);
+    if (x >= 1e30 && x < 1e90) return rsqrt_inrange(x * 0x1p-200) * 0x1p-100;
+    if (x <= 1e-30 && x > 1e-90) return rsqrt_inrange(x * 0x1p200) * 0x1p100;
+    return 1.0 / sqrt(x);
 }
 
 static __device__ __forceinline__ double det3(double a, double b, double c, double d, double e, double f, double g,
